@@ -1,0 +1,350 @@
+"""ORACLE -- TEST INFRASTRUCTURE ONLY (parity checker, CPU baseline).
+
+Python side of the CPU restatement of the reference's hot path.  The loops
+live in ``ucp_oracle.c`` (host glibc exp/erf, OpenMP over independent
+outputs); this module restates the reference's NumPy glue around them with
+the same NumPy expressions, so on the same host every result is bitwise the
+reference's.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+CPU-baseline leg may import it; the product package never does.
+
+Each function cites the reference code it restates (paths relative to
+``/root/reference/pkg/src/ucpsolve``).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "_build" / "liboracle.so"
+
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_i64 = ctypes.c_int64
+_dbl = ctypes.c_double
+
+INV_SQRT_2PI = 1.0 / np.sqrt(2.0 * np.pi)  # numerics.py:22 / kernels.py:47
+
+
+def build(force: bool = False) -> Path:
+    """Compile ucp_oracle.c with the committed Makefile (gcc, OpenMP)."""
+    if force or not LIB_PATH.exists() or LIB_PATH.stat().st_mtime < (HERE / "ucp_oracle.c").stat().st_mtime:
+        subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    return LIB_PATH
+
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        build()
+        L = ctypes.CDLL(str(LIB_PATH))
+        L.orc_trapezoid.restype = _dbl
+        L.orc_trapezoid.argtypes = [_f64p, _i64, _dbl]
+        L.orc_segmented_argmin.restype = None
+        L.orc_segmented_argmin.argtypes = [_f64p, _i64p, _i64, _i64p]
+        L.orc_flatten_windows.restype = _i64
+        L.orc_flatten_windows.argtypes = [_f64p, _i64p, _i64p, _i64, ctypes.c_void_p, _i64p]
+        L.orc_gauss_moments_grid.restype = None
+        L.orc_gauss_moments_grid.argtypes = [_f64p, _i64, _f64p, _dbl, _dbl, _i64, _f64p, _f64p, _f64p]
+        L.orc_gauss_moments_points.restype = None
+        L.orc_gauss_moments_points.argtypes = [
+            _f64p, _i64, _f64p, _f64p, _i64, _dbl, _dbl, _i64, _f64p, _f64p, _f64p]
+        L.orc_wc_stage0_cost.restype = None
+        L.orc_wc_stage0_cost.argtypes = [
+            _f64p, _i64p, _i64, _f64p, _f64p, _f64p, _dbl, _dbl, _i64, _dbl, _f64p]
+        L.orc_wc_stage1_cost.restype = None
+        L.orc_wc_stage1_cost.argtypes = [
+            _f64p, _i64p, _i64, _f64p, _f64p, _f64p, _i64, _dbl, _dbl, _i64, _f64p]
+        L.orc_phi_cdf.restype = _dbl
+        L.orc_phi_cdf.argtypes = [_dbl]
+        L.orc_num_threads.restype = ctypes.c_int
+        L.orc_set_threads.restype = None
+        L.orc_set_threads.argtypes = [ctypes.c_int]
+        _LIB = L
+    return _LIB
+
+
+def _c(x, dt=np.float64):
+    return np.ascontiguousarray(x, dtype=dt)
+
+
+# ---------------------------------------------------------------- kernels.py
+
+
+def set_threads(n: int) -> None:
+    lib().orc_set_threads(int(n))
+
+
+def num_threads() -> int:
+    return int(lib().orc_num_threads())
+
+
+def trapezoid_sum(samples, spacing):  # kernels.py:136-144
+    s = _c(samples)
+    return float(lib().orc_trapezoid(s, s.size, float(spacing)))
+
+
+def segmented_argmin(costs, offsets):  # kernels.py:147-160
+    c, o = _c(costs), _c(offsets, np.int64)
+    out = np.empty(o.size - 1, np.int64)
+    lib().orc_segmented_argmin(c, o, o.size - 1, out)
+    return out
+
+
+def flatten_windows(values, lo, hi):  # kernels.py:163-187 (dedup variant)
+    v, lo, hi = _c(values), _c(lo, np.int64), _c(hi, np.int64)
+    offsets = np.empty(lo.size + 1, np.int64)
+    flat = np.empty(int(np.sum(hi - lo + 1)), np.float64)
+    n = lib().orc_flatten_windows(v, lo, hi, lo.size, flat.ctypes.data, offsets)
+    return flat[:n].copy(), offsets
+
+
+def gauss_moments_grid(s, v, a, h, d):  # kernels.py:406-445
+    s, v = _c(s), _c(v)
+    t0, t1, t2 = (np.empty(s.size) for _ in range(3))
+    lib().orc_gauss_moments_grid(s, s.size, v, float(a), float(h), int(d), t0, t1, t2)
+    return t0, t1, t2
+
+
+def gauss_moments_points(y, x, w, a, h, d):  # kernels.py:447-486
+    y, x, w = _c(y), _c(x), _c(w)
+    o = [np.empty(y.size) for _ in range(3)]
+    lib().orc_gauss_moments_points(y, y.size, x, w, x.size, float(a), float(h), int(d), *o)
+    return tuple(o)
+
+
+def phi_cdf(z):  # kernels.py:398-404
+    return float(lib().orc_phi_cdf(float(z)))
+
+
+# ------------------------------------------------------ grids / numerics glue
+
+
+def linspace_grid(a, b, d):  # grids.py:50 (np.linspace) and :55-56 (spacing)
+    return np.linspace(float(a), float(b), int(d)), (float(b) - float(a)) / (int(d) - 1)
+
+
+def gaussian_pdf(mean, std, x):  # numerics.py:49-60 (NumPy exp, not glibc)
+    z = (np.asarray(x, dtype=np.float64) - mean) / std
+    return np.exp(-0.5 * z * z) * (INV_SQRT_2PI / std)
+
+
+def node_window_bounds(points, a, h, d, r):  # grids.py:180-195 (+ nearest_indices :141-145)
+    lo = np.ceil((points - r - a) / h - 1e-9).astype(np.int64)
+    hi = np.floor((points + r - a) / h + 1e-9).astype(np.int64)
+    ic = np.clip(np.ceil((points - a) / h - 0.5).astype(np.int64), 0, d - 1)
+    lo = np.maximum(0, np.minimum(lo, ic))
+    hi = np.minimum(d - 1, np.maximum(hi, ic))
+    return lo, hi
+
+
+# ------------------------------------------------------------ Witsenhausen
+
+
+@dataclass
+class OracleWitsenhausen:
+    """Restates problems/witsenhausen.py:36-79 on plain arrays.
+
+    ``f0`` (stage-0 density at the stage-0 grid points) and ``fw0`` are the
+    host NumPy values the reference computes; they may be injected so
+    parity runs can share one set of host-computed constants.
+    """
+
+    k: float = 0.2
+    sigma: float = 5.0
+    grid0: tuple = (-25.0, 25.0, 2000)
+    grid1: tuple = (-25.0, 25.0, 2000)
+    f0: np.ndarray | None = None
+    fw0: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.y0, self.h0 = linspace_grid(*self.grid0)
+        self.y1, self.h1 = linspace_grid(*self.grid1)
+        self.d0, self.d1 = int(self.grid0[2]), int(self.grid1[2])
+        self.a0, self.a1 = float(self.grid0[0]), float(self.grid1[0])
+        if self.fw0 is None:  # witsenhausen.py:47-53
+            w0 = np.full(self.d0, self.h0)
+            w0[0] *= 0.5
+            w0[-1] *= 0.5
+            self.fw0 = w0 * gaussian_pdf(0.0, self.sigma, self.y0)
+        if self.f0 is None:
+            self.f0 = gaussian_pdf(0.0, self.sigma, self.y0)
+
+    def grid(self, m):
+        return (self.y0, self.a0, self.h0, self.d0) if m == 0 else (self.y1, self.a1, self.h1, self.d1)
+
+    # witsenhausen.py:59-79.  y_centers are always stage grid points here
+    # (indices `seg_idx`), whose f0 is the host-precomputed per-point value.
+    def cost_segmented(self, m, u_flat, offsets, seg_idx, u0, u1):
+        u_flat, offsets = _c(u_flat), _c(offsets, np.int64)
+        seg_idx = _c(seg_idx, np.int64)
+        out = np.empty(u_flat.size)
+        if m == 0:
+            y = _c(self.y0[seg_idx])
+            f0 = _c(self.f0[seg_idx])
+            lib().orc_wc_stage0_cost(u_flat, offsets, offsets.size - 1, y, f0, _c(u1),
+                                     self.a1, self.h1, self.d1, self.k, out)
+        else:
+            y = _c(self.y1[seg_idx])
+            x1 = self.y0 + u0
+            lib().orc_wc_stage1_cost(u_flat, offsets, offsets.size - 1, y, _c(x1), _c(self.fw0),
+                                     self.d0, self.a1, self.h1, self.d1, out)
+        return out
+
+    def cost_batch(self, m, u, idx, u0, u1):  # problem.py:69-76
+        u = _c(u)
+        return self.cost_segmented(m, u, np.arange(u.size + 1, dtype=np.int64), idx, u0, u1)
+
+
+class OracleNumericError(RuntimeError):
+    """Mirror of problem.NumericError (problem.py:25-26)."""
+
+
+# --------------------------------------------------------------- solver.py
+
+
+@dataclass(frozen=True)
+class OracleConfig:  # solver.py:47-97 (fields used on the hot path)
+    iters_per_round: int = 20
+    precision: float = 1e-10
+    grad_step: float = 0.1
+    search_radius: float | None = None
+    fd_step: float = 1e-4
+    curvature_min: float = 1e-9
+    newton_cap: float | None = None
+    max_rounds: int = 10000
+
+    def radius(self, a, b):
+        return self.search_radius if self.search_radius is not None else (b - a) / 100.0
+
+    def cap(self, a, b):
+        return self.newton_cap if self.newton_cap is not None else (b - a) / 10.0
+
+
+def _grid_ab(p, m):
+    g = p.grid0 if m == 0 else p.grid1
+    return float(g[0]), float(g[1])
+
+
+def _bad(p, m, phase, i):
+    y = p.grid(m)[0][int(i)]
+    return OracleNumericError(
+        f"witsenhausen: non-finite marginal cost in {phase} phase at stage {m}, "
+        f"grid point {int(i)} (y={y!r})")
+
+
+def local_update_phase(p: OracleWitsenhausen, m, u0, u1, cfg: OracleConfig, points=None):
+    """solver.py:179-203 with problem.py:88-102 and solver.py:146-149.
+
+    ``points`` restricts the sweep to a subset of grid indices (used for
+    bounded CPU-baseline samples); the default is the whole grid.
+    """
+    u_all = u0 if m == 0 else u1
+    idx = np.arange(u_all.size, dtype=np.int64) if points is None else _c(points, np.int64)
+    u = u_all[idx]
+    with np.errstate(over="ignore"):
+        h = cfg.fd_step * (1.0 + np.abs(u))
+    up = p.cost_batch(m, u + h, idx, u0, u1)
+    mid = p.cost_batch(m, u, idx, u0, u1)
+    dn = p.cost_batch(m, u - h, idx, u0, u1)
+    with np.errstate(over="ignore", invalid="ignore"):
+        c1 = (up - dn) / (2.0 * h)
+        c2 = (up - 2.0 * mid + dn) / (h * h)
+    bad = np.flatnonzero(~(np.isfinite(c1) & np.isfinite(c2)))
+    if bad.size:
+        raise _bad(p, m, "local-update", idx[bad[0]])
+    a, b = _grid_ab(p, m)
+    cap = cfg.cap(a, b)
+    newton = c2 > cfg.curvature_min
+    quot = np.divide(c1, c2, out=np.zeros_like(c1), where=newton)
+    stepped = np.where(newton, u - np.clip(quot, -cap, cap), u - cfg.grad_step * c1)
+    cost_old = p.cost_batch(m, u, idx, u0, u1)
+    cost_new = p.cost_batch(m, stepped, idx, u0, u1)
+    bad = np.flatnonzero(~(np.isfinite(cost_old) & np.isfinite(cost_new)))
+    if bad.size:
+        raise _bad(p, m, "local-update", idx[bad[0]])
+    return np.where(cost_new <= cost_old, stepped, u)
+
+
+def partial_exhaustion_phase(p: OracleWitsenhausen, m, u0, u1, cfg: OracleConfig, points=None):
+    """solver.py:206-223 with grids.py:180-195 and kernels.py:147-187."""
+    y, a, h, d = p.grid(m)
+    u = u0 if m == 0 else u1
+    lo, hi = node_window_bounds(y, a, h, d, cfg.radius(*_grid_ab(p, m)))
+    idx = np.arange(d, dtype=np.int64) if points is None else _c(points, np.int64)
+    cand, offsets = flatten_windows(u, lo[idx], hi[idx])
+    costs = p.cost_segmented(m, cand, offsets, idx, u0, u1)
+    bad = np.flatnonzero(~np.isfinite(costs))
+    if bad.size:
+        seg = int(np.searchsorted(offsets, bad[0], side="right") - 1)
+        raise _bad(p, m, "partial-exhaustion", idx[seg])
+    return cand[segmented_argmin(costs, offsets)]
+
+
+def objective(p: OracleWitsenhausen, u0, u1):  # problem.py:110-127
+    costs = p.cost_batch(0, u0, np.arange(p.d0, dtype=np.int64), u0, u1)
+    bad = np.flatnonzero(~np.isfinite(costs))
+    if bad.size:
+        i = int(bad[0])
+        raise OracleNumericError(
+            f"witsenhausen: non-finite objective integrand at stage 0, grid point {i} "
+            f"(y={p.y0[i]!r}, u={u0[i]!r})")
+    return trapezoid_sum(costs, p.h0)
+
+
+def adaptive_allocation(gl, ge, n):  # solver.py:152-167
+    total = gl + ge
+    if total <= 0.0:
+        nl = n // 2
+    else:
+        nl = min(max(math.floor(gl * n / total), 1), n - 1)
+    return nl, n - nl
+
+
+def solve(p: OracleWitsenhausen, cfg: OracleConfig | None = None, u0=None, u1=None):
+    """solver.py:234-290 (adaptive local/exhaustion rounds)."""
+    cfg = cfg or OracleConfig()
+    u0 = p.y0.copy() if u0 is None else _c(u0).copy()
+    u1 = p.y1.copy() if u1 is None else _c(u1).copy()
+    n = cfg.iters_per_round
+    n_local = n // 2
+    current = objective(p, u0, u1)
+    rounds = []
+    term = "max_rounds"
+    for r in range(1, cfg.max_rounds + 1):
+        for phase, iters in ((local_update_phase, n_local), (partial_exhaustion_phase, n - n_local)):
+            for _ in range(iters):
+                u0 = phase(p, 0, u0, u1, cfg)
+                u1 = phase(p, 1, u0, u1, cfg)
+            if phase is local_update_phase:
+                after_local = objective(p, u0, u1)
+        after_exh = objective(p, u0, u1)
+        gl, ge = abs(current - after_local), abs(after_local - after_exh)
+        rounds.append((r, after_exh, gl, ge, n_local, n - n_local, after_local))
+        current = after_exh
+        if gl + ge <= cfg.precision:
+            term = "converged"
+            break
+        n_local, _ = adaptive_allocation(gl, ge, n)
+    return u0, u1, current, rounds, term
+
+
+def host_cpu_description() -> dict:
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_count": os.cpu_count(), "model": model}
