@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""Benchmark: marginal-cost evaluations/s of the Witsenhausen hot path at 2^20.
+
+Workload (BASELINE.json configs[1]): Witsenhausen k=0.2, sigma=5 on two
+2^20-point grids over [-25, 25], FP64, controllers warm-started from the
+converged default-grid (d=2000) solution, nearest-resampled (deterministic).
+SolverConfig(search_radius=19.5 h): 39-node exhaustion windows.
+
+One *step* = one solver iteration of each block type over both stages plus
+the objective, i.e. what a round of the reference does per iteration:
+    local_update(m=0), local_update(m=1), exhaustion(m=0), exhaustion(m=1), J.
+Every step starts from the same warm controllers, so all steps do identical
+work.  ``value`` counts the marginal-cost evaluations the REFERENCE performs
+for that step (5 per point per stage for a local sweep, one per distinct
+window candidate for an exhaustion sweep, one per point for J) divided by
+the device time; both arms use this same count, so their ratio is a pure
+time ratio.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 (torchrun): points of every stage are sharded across ranks and the new
+controller is all-gathered over NCCL after each phase (strong scaling on the
+fixed 2^20 grid); device time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "marginal-cost evals/sec & time-to-converge (s), Witsenhausen k=0.2 σ=5, 1/2/4/8 GPU"
+K_WC, SIGMA = 0.2, 5.0
+SPAN = (-25.0, 25.0)
+C1_D = 2000
+DP_OPS_PER_NODE = 8  # kernels.py:430-439: 3 mul + 3 add accumulate, 2 mul recurrence
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--log2d", type=int, default=20)
+    ap.add_argument("--window-nodes", type=int, default=39)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0,
+                    help="target CPU seconds of the cpu_baseline sample (ours) / per step (reference)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def grid_points(d):
+    return np.linspace(SPAN[0], SPAN[1], d), (SPAN[1] - SPAN[0]) / (d - 1)
+
+
+def resample(u_coarse, d):
+    """Nearest-point resampling of a d=2000 controller onto the fine grid (grids.py:141-145)."""
+    y, _ = grid_points(d)
+    _, ch = grid_points(u_coarse.size)
+    near = np.clip(np.ceil((y - SPAN[0]) / ch - 0.5).astype(np.int64), 0, u_coarse.size - 1)
+    return np.ascontiguousarray(u_coarse[near])
+
+
+def walk_nodes(s, a, h, d):
+    """Visited nodes of the stage-0 walk at centres s (kernels.py:416-421)."""
+    jlo = np.maximum(np.ceil(((s - 12.0) - a) / h), 0)
+    jhi = np.minimum(np.floor(((s + 12.0) - a) / h), d - 1)
+    return np.maximum(jhi - jlo + 1, 0)
+
+
+def window_candidates(u, lo, hi):
+    """Distinct-by-run candidates per window (== the reference's dedup count for staircases)."""
+    flags = np.concatenate([[0], (u[1:] != u[:-1]).astype(np.int64)])
+    pref = np.cumsum(flags)
+    return 1 + pref[hi] - pref[lo]
+
+
+def window_bounds(d, r):
+    y, h = grid_points(d)
+    lo = np.ceil((y - r - SPAN[0]) / h - 1e-9).astype(np.int64)
+    hi = np.floor((y + r - SPAN[0]) / h + 1e-9).astype(np.int64)
+    ic = np.clip(np.ceil((y - SPAN[0]) / h - 0.5).astype(np.int64), 0, d - 1)
+    return np.maximum(0, np.minimum(lo, ic)), np.minimum(d - 1, np.maximum(hi, ic))
+
+
+def workload_counts(u0, u1, d, r, fd_step=1e-4):
+    """Reference evaluation count per step and algorithmic DP ops of the local m=0 sweep."""
+    y, h = grid_points(d)
+    lo, hi = window_bounds(d, r)
+    cand0 = int(window_candidates(u0, lo, hi).sum())
+    cand1 = int(window_candidates(u1, lo, hi).sum())
+    evals = 5 * d + 5 * d + cand0 + cand1 + d
+    hh = fd_step * (1.0 + np.abs(u0))
+    s = y + u0
+    nodes = (walk_nodes(s + hh, SPAN[0], h, d) + 2 * walk_nodes(s, SPAN[0], h, d) + walk_nodes(s - hh, SPAN[0], h, d))
+    return {"evals": evals, "cand0": cand0, "cand1": cand1, "lu0_nodes": float(nodes.sum()),
+            "lu0_dp_ops": float(nodes.sum()) * DP_OPS_PER_NODE}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [ln.split(",") for ln in Path(self.f.name).read_text().splitlines() if ln.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for k, name in enumerate(names):
+                if len(r) > 5 + k and "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------ CPU (oracle) timing
+def cpu_step_seconds(orc, p, u0, u1, d, r, target_s):
+    """Time the reference's CPU algorithm (the oracle port, all host threads) on
+    bounded samples of every phase of one step; extrapolate to the full grid."""
+    cfg = orc.OracleConfig(search_radius=r)
+    thr = orc.num_threads()
+    W = float(np.mean(walk_nodes(grid_points(d)[0] + u0, SPAN[0], p.h1, d)))
+    node_rate, pair_rate = 4.0e8 * thr, 1.5e8 * thr  # rough per-thread rates to size samples
+    per = target_s / 5.0
+    n_lu0 = int(np.clip(per * node_rate / (5 * W), 16, d))
+    n_lu1 = int(np.clip(per * pair_rate / (5 * d), 4, d))
+    n_ex0 = int(np.clip(per * node_rate / (1.2 * W), 16, d))
+    n_ex1 = int(np.clip(per * pair_rate / d, 4, d))
+    n_obj = int(np.clip(per * node_rate / W, 16, d))
+    rng = np.random.default_rng(0)
+    pick = lambda n: np.sort(rng.choice(d, n, replace=False)).astype(np.int64)  # noqa: E731
+    times = {}
+    t = time.perf_counter()
+    orc.local_update_phase(p, 0, u0, u1, cfg, points=pick(n_lu0))
+    times["local0"] = (time.perf_counter() - t) * d / n_lu0
+    t = time.perf_counter()
+    orc.local_update_phase(p, 1, u0, u1, cfg, points=pick(n_lu1))
+    times["local1"] = (time.perf_counter() - t) * d / n_lu1
+    t = time.perf_counter()
+    orc.partial_exhaustion_phase(p, 0, u0, u1, cfg, points=pick(n_ex0))
+    times["exh0"] = (time.perf_counter() - t) * d / n_ex0
+    t = time.perf_counter()
+    orc.partial_exhaustion_phase(p, 1, u0, u1, cfg, points=pick(n_ex1))
+    times["exh1"] = (time.perf_counter() - t) * d / n_ex1
+    t = time.perf_counter()
+    idx = pick(n_obj)
+    p.cost_batch(0, u0[idx], idx, u0, u1)
+    times["objective"] = (time.perf_counter() - t) * d / n_obj
+    sample = (f"points sampled per phase: local0={n_lu0}, local1={n_lu1}, exh0={n_ex0}, exh1={n_ex1}, "
+              f"objective={n_obj} of {d}; time extrapolated x d/n")
+    return sum(times.values()), times, thr, sample
+
+
+def c1_oracle_solve(orc):
+    p = orc.OracleWitsenhausen(k=K_WC, sigma=SIGMA, grid0=(*SPAN, C1_D), grid1=(*SPAN, C1_D))
+    t = time.perf_counter()
+    u0, u1, J, rounds, term = orc.solve(p)
+    return u0, u1, {"wall_s": time.perf_counter() - t, "rounds": len(rounds), "J": J, "termination": term}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+
+    orc.build()
+    d = 1 << args.log2d
+    u0c, u1c, c1 = c1_oracle_solve(orc)
+    u0, u1 = resample(u0c, d), resample(u1c, d)
+    p = orc.OracleWitsenhausen(k=K_WC, sigma=SIGMA, grid0=(*SPAN, d), grid1=(*SPAN, d))
+    r = (args.window_nodes / 2.0) * p.h0
+    counts = workload_counts(u0, u1, d, r)
+    per_step = max(args.cpu_seconds, 2.0)
+    for _ in range(args.warmup):
+        cpu_step_seconds(orc, p, u0, u1, d, r, per_step / 4)
+    steps, last = [], None
+    for _ in range(args.steps):
+        tot, times, thr, sample = cpu_step_seconds(orc, p, u0, u1, d, r, per_step)
+        steps.append(tot)
+        last = (times, thr, sample)
+    sec = float(np.mean(steps))
+    value = counts["evals"] / sec
+    host = orc.host_cpu_description()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, d, counts),
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": last[1], "kind": "port",
+                         "sample": last[2], "host": host, "phase_s": last[0]},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "time_to_converge": {"config": f"d={C1_D} default SolverConfig, identity init", **c1},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args, d, counts):
+    return {"workload": f"witsenhausen k={K_WC} sigma={SIGMA} grids 2x{d} on [-25,25], warm start "
+                        f"(d=2000 solution resampled), search_radius={args.window_nodes / 2}h; step = "
+                        "local(m=0,1) + exhaustion(m=0,1) + objective",
+            "grid_points": d, "window_nodes": args.window_nodes,
+            "evals_per_step": counts["evals"], "exhaustion_candidates": [counts["cand0"], counts["cand1"]],
+            "l2": "inputs re-read each step; L2 flushed between steps (256 MiB memset inside timed region)"}
+
+
+# ------------------------------------------------------------ our B200 arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1908_04489_b200 as P
+    from paper_1908_04489_b200 import _lib
+    from paper_1908_04489_b200._device import ptr
+
+    sh = P.from_process_group() if world > 1 else P.LOCAL
+    d = 1 << args.log2d
+
+    # time-to-converge at the default grid (C1), on this GPU; also the warm start
+    c1p = P.Witsenhausen(k=K_WC, sigma=SIGMA)
+    c1p.objective(c1p.identity_controllers())  # context + first-launch warm-up
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    res = P.solve(c1p, P.SolverConfig(), sharding=sh)
+    torch.cuda.synchronize()
+    c1 = {"config": f"d={C1_D} default SolverConfig, identity init", "wall_s": time.perf_counter() - t,
+          "rounds": res.total_rounds, "J": res.final_objective, "termination": res.termination}
+    u0h, u1h = resample(res.controllers.values(0), d), resample(res.controllers.values(1), d)
+
+    prob = P.Witsenhausen(k=K_WC, sigma=SIGMA, grids=[(*SPAN, d), (*SPAN, d)])
+    h = prob.grids[0].spacing
+    cfg = P.SolverConfig(search_radius=(args.window_nodes / 2.0) * h)
+    U0 = P.ControllerSet((P.SampledController(prob.grids[0], u0h), P.SampledController(prob.grids[1], u1h)))
+    U0 = P.ControllerSet(tuple(P.SampledController(prob.grids[m], U0.device_values(m, dev)) for m in (0, 1)))
+    counts = workload_counts(u0h, u1h, d, cfg.radius_for(prob.grids[0]))
+    begin, end = sh.bounds(d)
+    counts_local_ops = counts["lu0_dp_ops"] * (end - begin) / d
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    phase_ms = np.zeros(5)
+
+    def step(U, record=False):
+        flush.zero_()
+        if record:
+            ev[0].record(stream)
+        for k, (kind, m) in enumerate((("local", 0), ("local", 1), ("exhaustion", 0), ("exhaustion", 1))):
+            sweep = prob.device_local_update if kind == "local" else prob.device_exhaustion
+            U = U.replace(m, P.SampledController(prob.grids[m], sweep(m, U, cfg, sh), _trusted_device=True))
+            if record:
+                ev[k + 1].record(stream)
+        J = prob.device_objective(U, sh)
+        if record:
+            ev[5].record(stream)
+            torch.cuda.synchronize()
+            for k in range(5):
+                phase_ms[k] += ev[k].elapsed_time(ev[k + 1])
+        return U, J
+
+    # FP64 pipe peak on this GPU (DMUL/DADD, no FMA) -- the roofline denominator
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sink = torch.empty(sms * 8 * 256, dtype=torch.float64, device=dev)
+    iters = 4096
+    for _ in range(2):
+        _lib.call("ucp_fp64_probe", sms * 8, 256, iters, ptr(sink), stream.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    _lib.call("ucp_fp64_probe", sms * 8, 256, iters, ptr(sink), stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    fp64_peak = sms * 8 * 256 * iters * 16 / (e0.elapsed_time(e1) * 1e-3)
+
+    for _ in range(args.warmup):
+        step(U0)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n_launch0 = _lib.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(U0)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = _lib.launch_count() - n_launch0
+    ms = t0.elapsed_time(t1)
+    clk = clocks.stop()
+    # per-phase split (separate, event-instrumented pass; not part of `value`)
+    for _ in range(args.steps):
+        step(U0, record=True)
+    phase_ms /= args.steps
+    tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_step = float(tmax.item()) / args.steps
+
+    # end to end: host controllers in, host controllers + J out, every step
+    e2e = None
+    if not args.no_e2e:
+        hu0 = torch.from_numpy(u0h).pin_memory()
+        hu1 = torch.from_numpy(u1h).pin_memory()
+        o0 = torch.empty_like(hu0).pin_memory()
+        o1 = torch.empty_like(hu1).pin_memory()
+
+        def e2e_step():
+            flush.zero_()
+            d0, d1 = hu0.to(dev, non_blocking=True), hu1.to(dev, non_blocking=True)
+            U = P.ControllerSet((P.SampledController(prob.grids[0], d0, _trusted_device=True),
+                                 P.SampledController(prob.grids[1], d1, _trusted_device=True)))
+            V, J = step(U)
+            o0.copy_(V[0]._dev, non_blocking=True)
+            o1.copy_(V[1]._dev, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return J
+
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te.item()) / args.steps
+        e2e = {"value": counts["evals"] / (e2e_ms * 1e-3), "unit": "evals/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 2 * d * 8, "d2h_bytes_per_step": 2 * d * 8 + 16,
+               "path": "public API (SampledController from pinned host arrays -> solver sweeps -> host)"}
+
+    # roofline of the dominant kernel pair: the stage-0 local-update sweep
+    lu0_ms = phase_ms[0]
+    achieved = counts_local_ops / (lu0_ms * 1e-3)
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("lu0_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "fp64", "kernel": "k_lu0_probe + k_lu0_finish (stage-0 local-update sweep)",
+                "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": traffic,
+                "peak_source": f"measured on this GPU: ucp_fp64_probe DMUL+DADD throughput ({sms} SMs); "
+                               "nominal 148 SMs x 64 DP lanes x 1.965 GHz = 18.6 TFLOP/s (non-FMA)",
+                "work": f"{DP_OPS_PER_NODE} DP ops per visited node x {counts['lu0_nodes']:.4g} nodes "
+                        "(4 walks per point; exp/erf/setup excluded)"}
+
+    line = None
+    if rank == 0:
+        value = counts["evals"] / (ms_step * 1e-3)
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            from oracle import oracle as orc
+
+            orc.build()
+            p = orc.OracleWitsenhausen(k=K_WC, sigma=SIGMA, grid0=(*SPAN, d), grid1=(*SPAN, d),
+                                       f0=prob._f0, fw0=prob._fw0)
+            sec, times, thr, sample = cpu_step_seconds(orc, p, u0h, u1h, d, cfg.radius_for(prob.grids[0]),
+                                                       args.cpu_seconds)
+            cpu = {"value": counts["evals"] / sec, "unit": "evals/s", "cores": thr, "kind": "port",
+                   "sample": sample, "step_s_extrapolated": sec, "phase_s": times,
+                   "host": orc.host_cpu_description()}
+        line = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(args, d, counts),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
+            "phase_ms": dict(zip(["local0", "local1", "exh0", "exh1", "objective"], phase_ms.round(3).tolist())),
+            "time_to_converge": c1, "gpu": torch.cuda.get_device_name(dev),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,145 @@
+/* ucp_b200 -- C ABI of the B200 (sm_100a) marginal-cost evaluator for the
+ * arXiv 1908.04489 UCP solver (`ucpsolve`), Witsenhausen counterexample.
+ *
+ * This is the drop-in boundary: the reference's hot path is the Python
+ * plugin API `Problem.marginal_cost_segmented` / the solver phases / the
+ * `kernels` module (numba); each entry point below replaces one of them and
+ * cites it (paths relative to /root/reference/pkg/src/ucpsolve).  The host
+ * side that binds them (ctypes) is paper_1908_04489_b200/_lib.py; the
+ * binding a maintainer would add to the reference is in INTEGRATION.md.
+ *
+ * Conventions
+ *  - every array argument is a DEVICE pointer (float64 / int64, C
+ *    contiguous) owned by the caller (PyTorch tensors in the Python host);
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream); every call
+ *    is asynchronous on it unless documented otherwise;
+ *  - results are bitwise the reference's ("ref-order" arithmetic: glibc-exact
+ *    exp/erf, no FMA contraction, the reference's summation order);
+ *  - return value: UCP_OK or an error status (ucp_status_string());
+ *    non-finite numerics are NOT return codes: sweeps atomicMin the first
+ *    offending grid point into a caller-owned device `err` array so the host
+ *    can raise the reference's NumericError lazily.
+ */
+#ifndef UCP_B200_H
+#define UCP_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UCP_ABI_VERSION 1
+
+enum ucp_status {
+  UCP_OK = 0,
+  UCP_ERR_ARG = 1,     /* bad argument (shape, stage index, null pointer) -> ValueError */
+  UCP_ERR_CUDA = 3,    /* CUDA runtime error */
+};
+
+/* Sentinel stored in `err` slots that saw no failure. */
+#define UCP_NO_ERROR INT64_MAX
+
+/* Witsenhausen problem (problems/witsenhausen.py:36-57).  Grid spacing
+ * h = (b-a)/(d-1) (grids.py:55-56); y0/y1 are the np.linspace points
+ * (grids.py:50), f0 = numerics.pdf(N(0, sigma), y0) and fw0 = trapezoid
+ * weights * f0 (witsenhausen.py:47-53), all computed by the host with NumPy
+ * and uploaded (NumPy's SIMD exp is not glibc's). */
+typedef struct ucp_wc_problem {
+  double k;
+  double a0, h0;
+  int64_t d0;
+  double a1, h1;
+  int64_t d1;
+  const double* y0;  /* [d0] */
+  const double* y1;  /* [d1] */
+  const double* f0;  /* [d0] */
+  const double* fw0; /* [d0] */
+} ucp_wc_problem;
+
+/* Local-update parameters (solver.py:47-97, SolverConfig), already resolved
+ * per stage (newton_cap = cfg.cap_for(grid)). */
+typedef struct ucp_local_params {
+  double fd_step;
+  double curvature_min;
+  double grad_step;
+  double newton_cap;
+} ucp_local_params;
+
+typedef struct ucp_workspace ucp_workspace;
+
+/* ---- library / workspace ------------------------------------------------ */
+int ucp_abi_version(void);
+const char* ucp_status_string(int status);
+const char* ucp_last_error(void);
+/* Number of kernel launches issued by this library so far (instrumentation). */
+int64_t ucp_launch_count(void);
+/* Scratch memory for the sweeps; grows on first use, reused afterwards. */
+int ucp_workspace_create(ucp_workspace** ws);
+int ucp_workspace_destroy(ucp_workspace* ws);
+/* Pre-size scratch for grids of d0/d1 points and up to max_cand exhaustion
+ * candidates so later calls never allocate. */
+int ucp_workspace_reserve(ucp_workspace* ws, int64_t d0, int64_t d1, int64_t max_cand);
+
+/* ---- kernels.py surface ---------------------------------------------------
+ * kernels.gauss_moments_grid (kernels.py:406-445): T_k(s_t) for t < n. */
+int ucp_gauss_moments_grid(const double* s, int64_t n, const double* v, double a, double h,
+                           int64_t d, double* t0, double* t1, double* t2, void* stream);
+/* kernels.gauss_moments_points (kernels.py:447-486). */
+int ucp_gauss_moments_points(const double* y, int64_t n, const double* x, const double* w,
+                             int64_t m, double a, double h, int64_t d, double* o0, double* o1,
+                             double* o2, ucp_workspace* ws, void* stream);
+/* kernels.trapezoid_sum (kernels.py:136-144): serial ascending sum, written
+ * to *out (device).  If err != NULL, err[0] receives the first index with a
+ * non-finite sample (problem.py:117-127 diagnostics). */
+int ucp_trapezoid_sum(const double* samples, int64_t n, double spacing, double* out,
+                      int64_t* err, void* stream);
+/* kernels.segmented_argmin (kernels.py:147-160). */
+int ucp_segmented_argmin(const double* costs, const int64_t* offsets, int64_t nseg,
+                         int64_t* out, void* stream);
+/* Device libm port, exposed for parity tests: out[i] = exp(x[i]) (which=0),
+ * erf(x[i]) (which=1) or the reference's phi_cdf(x[i]) (which=2). */
+int ucp_device_libm(int which, const double* x, int64_t n, double* out, void* stream);
+
+/* ---- Witsenhausen plugin: Problem.marginal_cost_segmented -----------------
+ * witsenhausen.py:62-70 (m=0).  Candidate u_flat[c] for c in
+ * [offsets[s], offsets[s+1]) is scored at observation y_seg[s] with stage-0
+ * density f0_seg[s]; v1 = U.values(1); n_cand = offsets[nseg] (host copy). */
+int ucp_wc_stage0_cost(const ucp_wc_problem* P, const double* v1, const double* u_flat,
+                       int64_t n_cand, const int64_t* offsets, const double* y_seg,
+                       const double* f0_seg, int64_t nseg, double* out, void* stream);
+/* witsenhausen.py:71-78 (m=1); u0 = U.values(0). */
+int ucp_wc_stage1_cost(const ucp_wc_problem* P, const double* u0, const double* u_flat,
+                       int64_t n_cand, const int64_t* offsets, const double* y_seg, int64_t nseg,
+                       double* out, ucp_workspace* ws, void* stream);
+
+/* ---- solver phases (sharded over grid points [begin, end)) ----------------
+ * solver.py:179-203 local_update_phase for stage `stage`; out[i] written for
+ * i in [begin, end).  err[0] <- first point with non-finite c1/c2,
+ * err[1] <- first point with non-finite cost_old/cost_new,
+ * err[2] <- first point whose new value is non-finite (grids.py:80-84). */
+int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, const double* u1,
+                        const ucp_local_params* lp, int64_t begin, int64_t end, double* out,
+                        int64_t* err, ucp_workspace* ws, void* stream);
+/* solver.py:206-223 partial_exhaustion_phase; win_lo/win_hi from
+ * grids.node_window_bounds (grids.py:180-195).  err[0] <- first point with a
+ * non-finite candidate cost.  Synchronises `stream` once (candidate count). */
+int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, const double* u1,
+                      const int64_t* win_lo, const int64_t* win_hi, int64_t begin, int64_t end,
+                      double* out, int64_t* err, ucp_workspace* ws, void* stream);
+/* problem.py:110-127 objective, per-point part: terms[i] = C0(u0[i], y0[i])
+ * for i in [begin, end); err[0] <- first non-finite term.  The serial
+ * trapezoid over all terms is ucp_trapezoid_sum. */
+int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const double* u1,
+                           int64_t begin, int64_t end, double* terms, int64_t* err,
+                           void* stream);
+
+/* ---- instrumentation ------------------------------------------------------
+ * FP64 pipe throughput probe (no FMA: DMUL/DADD only, 8 independent chains
+ * per thread).  Performs iters*16 DP ops per thread; sink must hold
+ * blocks*threads doubles. */
+int ucp_fp64_probe(int blocks, int threads, int iters, double* sink, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UCP_B200_H */

@@ -1,0 +1,897 @@
+// B200 (sm_100a) kernels + C ABI for the Witsenhausen marginal-cost hot path
+// of arXiv 1908.04489's UCP solver.  See DESIGN.md for the data layout, the
+// roofline of each kernel and the exactness argument; include/ucp_b200.h for
+// the boundary.  Build: nvcc -gencode arch=compute_100a,code=sm_100a
+// -fmad=false (no FMA contraction: the reference has none).
+//
+// "ref-order": every kernel evaluates the reference's expressions with the
+// same association, the same per-output summation order and glibc-exact
+// exp/erf, so outputs are bitwise the reference's.  Parallelism only spans
+// independent outputs (candidates, points, queries), as numba's prange does.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <cub/device/device_scan.cuh>
+
+#include "../../include/ucp_b200.h"
+#include "ucp_libm.h"
+
+#ifndef __CUDACC__
+#error "compile with nvcc"
+#endif
+
+namespace {
+
+constexpr double kGaussCut = 12.0;  // kernels.py:55 GAUSS_CUT
+
+__device__ const uint64_t g_exp_tab[256] = UCP_EXP_TAB_INIT;
+const uint64_t h_exp_tab[256] = UCP_EXP_TAB_INIT;
+
+std::atomic<int64_t> g_launches{0};
+thread_local char g_errbuf[256] = "";
+
+__host__ __device__ __forceinline__ double inv_sqrt_2pi() { return ucp_asf64(UCP_INV_SQRT_2PI_BITS); }
+
+int cuda_fail(cudaError_t e, const char* where) {
+  snprintf(g_errbuf, sizeof g_errbuf, "%s: %s", where, cudaGetErrorString(e));
+  return UCP_ERR_CUDA;
+}
+
+#define UCP_CHECK(call)                                  \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+#define UCP_LAUNCHED(name)                                          \
+  do {                                                              \
+    g_launches.fetch_add(1, std::memory_order_relaxed);             \
+    cudaError_t e_ = cudaGetLastError();                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, "launch " name);    \
+  } while (0)
+
+int arg_fail(const char* msg) {
+  snprintf(g_errbuf, sizeof g_errbuf, "%s", msg);
+  return UCP_ERR_ARG;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline unsigned nblocks(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+// --------------------------------------------------------------------------
+// Stage-0 inner moments: the windowed Gaussian walk of kernels.py:406-445.
+// --------------------------------------------------------------------------
+struct WalkGrid {
+  double a, h, b, q;  // b = a + h*(d-1); q = exp(-h*h)   (kernels.py:411-412)
+  int64_t d;
+};
+
+struct Mom3 {
+  double t0, t1, t2;
+};
+
+WalkGrid make_walk_grid(double a, double h, int64_t d) {
+  WalkGrid g;
+  g.a = a;
+  g.h = h;
+  g.d = d;
+  g.b = a + h * (double)(d - 1);
+  g.q = ucp_exp_tab((-h) * h, h_exp_tab);  // same port as the device: bitwise glibc
+  return g;
+}
+
+__device__ __forceinline__ double phi_cdf(double z) { return ucp_phi_cdf_tab(z, g_exp_tab); }
+
+// One centre s: T_k(s) = sum_j W_j pdf(y_j - s) v_j^k + cdf tails.  The
+// window walk is inherently serial (multiplicative pdf recurrence,
+// kernels.py:438-439); one thread owns one centre.  Nodes 0 and d-1 (half
+// trapezoid weight) are peeled so the interior loop is branch-free.
+__device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__ v, const WalkGrid g) {
+  long long jlo = (long long)ceil(((st - kGaussCut) - g.a) / g.h);
+  long long jhi = (long long)floor(((st + kGaussCut) - g.a) / g.h);
+  if (jlo < 0) jlo = 0;
+  if (jhi > g.d - 1) jhi = g.d - 1;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  if (jlo <= jhi) {
+    const double h = g.h;
+    const double q = g.q;
+    double tt = (g.a + (double)jlo * h) - st;
+    double pdf = ucp_exp_tab((-0.5 * tt) * tt, g_exp_tab) * inv_sqrt_2pi();
+    double ratio = ucp_exp_tab((-h) * (tt + 0.5 * h), g_exp_tab);
+    const int last = (int)(g.d - 1);
+    const int je = (int)jhi;
+    int j = (int)jlo;
+#define UCP_WALK_STEP(W)            \
+  {                                 \
+    double wp = (W) * pdf;          \
+    double vj = __ldg(v + j);       \
+    acc0 += wp;                     \
+    double wv = wp * vj;            \
+    acc1 += wv;                     \
+    acc2 += wv * vj;                \
+    pdf *= ratio;                   \
+    ratio *= q;                     \
+  }
+    const double hh = 0.5 * h;
+    if (j == 0) {
+      UCP_WALK_STEP(hh);
+      ++j;
+    }
+    const int jint = je < last ? je : last - 1;
+#pragma unroll 4
+    for (; j <= jint; ++j) UCP_WALK_STEP(h);
+    if (je == last && j == last) UCP_WALK_STEP(hh);
+#undef UCP_WALK_STEP
+  }
+  double lo = phi_cdf(g.a - st);
+  double hi = phi_cdf(st - g.b);
+  const double v0 = __ldg(v), vl = __ldg(v + g.d - 1);
+  Mom3 r;
+  r.t0 = (acc0 + lo) + hi;
+  r.t1 = (acc1 + lo * v0) + hi * vl;
+  r.t2 = (acc2 + (lo * v0) * v0) + (hi * vl) * vl;
+  return r;
+}
+
+// witsenhausen.py:31-33 (_quad_in_u): a*u*u - 2.0*b*u + c
+__device__ __forceinline__ double quad_in_u(double a, double b, double c, double u) {
+  return (((a * u) * u) - ((2.0 * b) * u)) + c;
+}
+
+// witsenhausen.py:64-70: C0(u, y) = f0(y) * (k^2 u^2 + E[(s - u1(y1))^2]), s = y+u
+__device__ __forceinline__ double stage0_cost(double u, double y, double f0, double k,
+                                              const double* __restrict__ v1, const WalkGrid g) {
+  double s = y + u;
+  Mom3 t = gauss_walk(s, v1, g);
+  double inner = quad_in_u(t.t0, t.t1, t.t2, s);
+  return f0 * ((((k * k) * u) * u) + inner);
+}
+
+__device__ __forceinline__ bool finite(double x) { return isfinite(x); }
+
+__device__ __forceinline__ void flag_min(int64_t* slot, int64_t i) {
+  if (slot) atomicMin(reinterpret_cast<unsigned long long*>(slot), (unsigned long long)i);
+}
+
+// ---------------------------------------------------------------- kernels
+
+__global__ void k_gauss_grid(const double* __restrict__ s, int64_t n, const double* __restrict__ v,
+                             WalkGrid g, double* t0, double* t1, double* t2) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  Mom3 r = gauss_walk(s[t], v, g);
+  t0[t] = r.t0;
+  t1[t] = r.t1;
+  t2[t] = r.t2;
+}
+
+// marginal_cost_segmented m=0 over a flat candidate list; the segment of
+// candidate c is found by binary search in `offsets` (segments are short).
+__global__ void k_stage0_segmented(const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
+                                   int64_t nseg, const double* __restrict__ y_seg,
+                                   const double* __restrict__ f0_seg, double k,
+                                   const double* __restrict__ v1, WalkGrid g, double* out) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t n = offsets[nseg];
+  if (c >= n) return;
+  int64_t lo = 0, hi = nseg;  // find s with offsets[s] <= c < offsets[s+1]
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (offsets[mid] <= c) lo = mid; else hi = mid;
+  }
+  out[c] = stage0_cost(u_flat[c], y_seg[lo], f0_seg[lo], k, v1, g);
+}
+
+// Local update, stage 0, part 1 (problem.py:95-97): the three FD probes
+// u+h, u, u-h of every point.  probe-major layout so a warp walks adjacent
+// centres (coalesced v1 reads).
+__global__ void k_lu0_probe(const double* __restrict__ y0, const double* __restrict__ f0,
+                            const double* __restrict__ u0, double k, const double* __restrict__ v1,
+                            WalkGrid g, double fd_step, int64_t begin, int64_t n, double* cost3) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 3 * n) return;
+  int p = (int)(t / n);
+  int64_t i = begin + (t - (int64_t)p * n);
+  double u = u0[i];
+  double hh = fd_step * (1.0 + fabs(u));  // solver.py:192
+  double uu = p == 0 ? u + hh : (p == 1 ? u : u - hh);
+  cost3[t] = stage0_cost(uu, y0[i], f0[i], k, v1, g);
+}
+
+// Newton-or-gradient step shared by both stages (solver.py:130-149).
+__device__ __forceinline__ double newton_step(double u, double c1, double c2,
+                                              const ucp_local_params lp) {
+  if (c2 > lp.curvature_min) {
+    double quot = c1 / c2;
+    quot = quot < -lp.newton_cap ? -lp.newton_cap : quot;  // np.clip
+    quot = quot > lp.newton_cap ? lp.newton_cap : quot;
+    return u - quot;
+  }
+  return u - lp.grad_step * c1;
+}
+
+// Local update, stage 0, part 2: derivatives (problem.py:99-101), step,
+// cost_new and the monotone guard (solver.py:193-203).  cost_old is the
+// bitwise-identical `mid` probe.
+__global__ void k_lu0_finish(const double* __restrict__ y0, const double* __restrict__ f0,
+                             const double* __restrict__ u0, double k, const double* __restrict__ v1,
+                             WalkGrid g, ucp_local_params lp, int64_t begin, int64_t n,
+                             const double* __restrict__ cost3, double* out, int64_t* err) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int64_t i = begin + t;
+  double u = u0[i];
+  double hh = lp.fd_step * (1.0 + fabs(u));
+  double up = cost3[t], mid = cost3[n + t], dn = cost3[2 * n + t];
+  double c1 = (up - dn) / (2.0 * hh);
+  double c2 = ((up - 2.0 * mid) + dn) / (hh * hh);
+  if (!(finite(c1) && finite(c2))) {
+    flag_min(err, i);
+    out[i] = u;
+    return;
+  }
+  double stepped = newton_step(u, c1, c2, lp);  // project() is the identity
+  double cost_new = stage0_cost(stepped, y0[i], f0[i], k, v1, g);
+  if (!(finite(mid) && finite(cost_new))) flag_min(err + 1, i);
+  double r = cost_new <= mid ? stepped : u;
+  if (!finite(r)) flag_min(err + 2, i);
+  out[i] = r;
+}
+
+// Objective integrand (problem.py:116-127): c_i = C0(u0_i, y0_i).
+__global__ void k_obj_terms(const double* __restrict__ y0, const double* __restrict__ f0,
+                            const double* __restrict__ u0, double k, const double* __restrict__ v1,
+                            WalkGrid g, int64_t begin, int64_t end, double* terms, int64_t* err) {
+  int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= end) return;
+  double c = stage0_cost(u0[i], y0[i], f0[i], k, v1, g);
+  if (!finite(c)) flag_min(err, i);
+  terms[i] = c;
+}
+
+// kernels.py:136-144: serial ascending trapezoid.  One warp stages chunks
+// through shared memory; lane 0 performs the additions in index order.
+__global__ void k_trapezoid(const double* __restrict__ x, int64_t n, double spacing, double* out,
+                            int64_t* err) {
+  __shared__ double buf[1024];
+  const int lane = threadIdx.x;
+  double acc = 0.0;
+  int64_t bad = UCP_NO_ERROR;
+  for (int64_t base = 0; base < n; base += 1024) {
+    int64_t cnt = n - base < 1024 ? n - base : 1024;
+    for (int r = lane; r < cnt; r += 32) {
+      double xv = x[base + r];
+      buf[r] = xv;
+      if (!isfinite(xv) && base + r < bad) bad = base + r;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      for (int r = 0; r < cnt; ++r) {
+        int64_t i = base + r;
+        double xv = buf[r];
+        if (i == 0) acc = 0.5 * xv;
+        else if (i < n - 1) acc += xv;
+        else acc += 0.5 * xv;
+      }
+    }
+    __syncwarp();
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    long long o = __shfl_down_sync(0xffffffffu, (long long)bad, off);
+    bad = o < bad ? o : bad;
+  }
+  if (lane == 0) {
+    *out = n == 1 ? 0.0 : acc * spacing;
+    if (err && bad != UCP_NO_ERROR) flag_min(err, bad);
+  }
+}
+
+__global__ void k_segmented_argmin(const double* __restrict__ costs, const int64_t* __restrict__ offsets,
+                                   int64_t nseg, int64_t* out) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  int64_t lo = offsets[s], hi = offsets[s + 1];
+  int64_t best = lo;
+  double bv = costs[lo];
+  for (int64_t t = lo + 1; t < hi; ++t) {
+    double c = costs[t];
+    if (c < bv) {
+      bv = c;
+      best = t;
+    }
+  }
+  out[s] = best;
+}
+
+// ---- exhaustion, stage 0 (solver.py:206-223) -------------------------------
+// Candidates of point i: the snapshot values in its window with adjacent
+// repeats collapsed (identical values give identical costs, and the
+// first-occurrence argmin returns the same value -- the reference's own
+// flatten_windows dedups, kernels.py:163-187).
+__global__ void k_ex_count(const double* __restrict__ u, const int64_t* __restrict__ lo,
+                           const int64_t* __restrict__ hi, int64_t begin, int64_t n, int64_t* counts) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int64_t i = begin + t;
+  int64_t c = 1;
+  double prev = u[lo[i]];
+  for (int64_t j = lo[i] + 1; j <= hi[i]; ++j) {
+    double x = u[j];
+    c += (x != prev);
+    prev = x;
+  }
+  counts[t] = c;
+}
+
+__global__ void k_ex_fill(const double* __restrict__ u, const int64_t* __restrict__ lo,
+                          const int64_t* __restrict__ hi, int64_t begin, int64_t n,
+                          const int64_t* __restrict__ offs, int32_t* cand_pt, int32_t* cand_j) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int64_t i = begin + t;
+  int64_t pos = offs[t];
+  int64_t j0 = lo[i];
+  double prev = u[j0];
+  cand_pt[pos] = (int32_t)i;
+  cand_j[pos] = (int32_t)j0;
+  ++pos;
+  for (int64_t j = j0 + 1; j <= hi[i]; ++j) {
+    double x = u[j];
+    if (x != prev) {
+      cand_pt[pos] = (int32_t)i;
+      cand_j[pos] = (int32_t)j;
+      ++pos;
+    }
+    prev = x;
+  }
+}
+
+__global__ void k_ex0_eval(const double* __restrict__ y0, const double* __restrict__ f0,
+                           const double* __restrict__ u0, double k, const double* __restrict__ v1,
+                           WalkGrid g, const int64_t* __restrict__ total,
+                           const int32_t* __restrict__ cand_pt, const int32_t* __restrict__ cand_j,
+                           double* costs) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= *total) return;
+  int32_t i = cand_pt[c];
+  costs[c] = stage0_cost(u0[cand_j[c]], y0[i], f0[i], k, v1, g);
+}
+
+// First strict minimum per point (kernels.py:147-160), kept in registers;
+// any non-finite candidate cost flags the point (solver.py:216-221).
+__global__ void k_ex_argmin(const double* __restrict__ u, const double* __restrict__ costs,
+                            const int64_t* __restrict__ offs, const int32_t* __restrict__ cand_j,
+                            int64_t begin, int64_t n, double* out, int64_t* err) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int64_t lo = offs[t], hi = offs[t + 1];
+  int64_t best = lo;
+  double bv = costs[lo];
+  bool ok = finite(bv);
+  for (int64_t c = lo + 1; c < hi; ++c) {
+    double x = costs[c];
+    ok = ok && finite(x);
+    if (x < bv) {
+      bv = x;
+      best = c;
+    }
+  }
+  if (!ok) flag_min(err, begin + t);
+  out[begin + t] = u[cand_j[best]];
+}
+
+// ---- stage 1: the u1 estimator moments (kernels.py:447-486) ----------------
+constexpr int kTile = 256;  // support points per shared-memory tile
+
+__global__ void k_x1_minmax(const double* __restrict__ y0, const double* __restrict__ u0, int64_t d0,
+                            double* x1, double2* tile_mm) {
+  __shared__ double smin[kTile], smax[kTile];
+  int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
+  double x = 0.0, mn = INFINITY, mx = -INFINITY;
+  if (i < d0) {
+    x = y0 ? y0[i] + u0[i] : u0[i];  // witsenhausen.py:72 x1 = points + u0
+    x1[i] = x;
+    if (!isnan(x)) mn = mx = x;
+  }
+  smin[threadIdx.x] = mn;
+  smax[threadIdx.x] = mx;
+  __syncthreads();
+  for (int s = kTile / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + s]);
+      smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_mm[blockIdx.x] = make_double2(smin[0], smax[0]);
+}
+
+// One thread per query y; the CTA streams (x_i, w_i) tiles through shared
+// memory in ascending i (the reference's summation order) and skips whole
+// tiles whose support lies outside +-GAUSS_CUT of every query in the CTA
+// (exactly zero contribution: monotone rounding of y - x).  Repeated x_i
+// (staircase u0) reuse the previous pair weight bit for bit.
+constexpr int kMomThreads = 128;
+__global__ void __launch_bounds__(kMomThreads)
+k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x,
+          const double* __restrict__ w, int64_t m, const double2* __restrict__ tile_mm, double a,
+          double h, int64_t d, double* o0, double* o1, double* o2) {
+  __shared__ double sx[kTile], sw[kTile];
+  __shared__ uint64_t stab[256];
+  __shared__ double s_ymin[kMomThreads / 32], s_ymax[kMomThreads / 32];
+  __shared__ int s_edge;
+  for (int r = threadIdx.x; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
+  if (threadIdx.x == 0) s_edge = 0;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = t < n;
+  const double yt = active ? yq[t] : yq[n - 1];
+  const double b = a + h * (double)(d - 1);
+  long long j = (long long)ceil((yt - a) / h - 0.5);
+  if (j < 0) j = 0;
+  if (j > d - 1) j = d - 1;
+  const bool at_left = j == 0, at_right = j == d - 1;
+  const double factor = (at_left || at_right) ? 0.5 : 1.0;
+  // CTA query range (for tile skipping) and whether any query owns a tail
+  double ymin = yt, ymax = yt;
+  for (int off = 16; off > 0; off >>= 1) {
+    ymin = fmin(ymin, __shfl_xor_sync(0xffffffffu, ymin, off));
+    ymax = fmax(ymax, __shfl_xor_sync(0xffffffffu, ymax, off));
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    s_ymin[threadIdx.x >> 5] = ymin;
+    s_ymax[threadIdx.x >> 5] = ymax;
+  }
+  if (at_left || at_right || isnan(yt)) atomicOr(&s_edge, 1);
+  __syncthreads();
+  ymin = s_ymin[0];
+  ymax = s_ymax[0];
+  for (int r = 1; r < (int)(blockDim.x >> 5); ++r) {
+    ymin = fmin(ymin, s_ymin[r]);
+    ymax = fmax(ymax, s_ymax[r]);
+  }
+  const bool no_skip = s_edge != 0;
+  const double INV = inv_sqrt_2pi();
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  double px = __longlong_as_double(0x7ff8dead00000000ll);  // NaN: never equal
+  double pwp = 0.0;
+  const int64_t ntiles = (m + kTile - 1) / kTile;
+  for (int64_t tile = 0; tile < ntiles; ++tile) {
+    if (!no_skip) {
+      double2 mm = tile_mm[tile];
+      if (ymin - mm.y > kGaussCut || ymax - mm.x < -kGaussCut) continue;  // CTA-uniform
+    }
+    const int64_t base = tile * kTile;
+    const int cnt = (int)(m - base < kTile ? m - base : kTile);
+    __syncthreads();
+    for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
+      sx[r] = x[base + r];
+      sw[r] = w[base + r];
+    }
+    __syncthreads();
+    for (int r = 0; r < cnt; ++r) {
+      const double xi = sx[r];
+      double wp;
+      if (xi == px) {
+        wp = pwp;
+      } else {
+        const double diff = yt - xi;
+        wp = 0.0;
+        if (diff <= kGaussCut && diff >= -kGaussCut)
+          wp = (factor * ucp_exp_tab((-0.5 * diff) * diff, stab)) * INV;
+        if (at_left) wp += ucp_phi_cdf_tab(a - xi, stab) / h;
+        if (at_right) wp += ucp_phi_cdf_tab(xi - b, stab) / h;
+        px = xi;
+        pwp = wp;
+      }
+      if (wp != 0.0) {
+        wp *= sw[r];
+        acc0 += wp;
+        const double wx = wp * xi;
+        acc1 += wx;
+        acc2 += wx * xi;
+      }
+    }
+  }
+  if (active) {
+    o0[t] = acc0;
+    o1[t] = acc1;
+    o2[t] = acc2;
+  }
+}
+
+// Stage-1 candidates: C1(u, y) = A u^2 - 2 B u + C (witsenhausen.py:73-78).
+__global__ void k_stage1_segmented(const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
+                                   int64_t nseg, const double* __restrict__ m0,
+                                   const double* __restrict__ m1, const double* __restrict__ m2,
+                                   double* out) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t n = offsets[nseg];
+  if (c >= n) return;
+  int64_t lo = 0, hi = nseg;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (offsets[mid] <= c) lo = mid; else hi = mid;
+  }
+  out[c] = quad_in_u(m0[lo], m1[lo], m2[lo], u_flat[c]);
+}
+
+__global__ void k_lu1(const double* __restrict__ u1, const double* __restrict__ m0,
+                      const double* __restrict__ m1, const double* __restrict__ m2,
+                      ucp_local_params lp, int64_t begin, int64_t n, double* out, int64_t* err) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int64_t i = begin + t;
+  const double A = m0[t], B = m1[t], C = m2[t];
+  double u = u1[i];
+  double hh = lp.fd_step * (1.0 + fabs(u));
+  double up = quad_in_u(A, B, C, u + hh);
+  double mid = quad_in_u(A, B, C, u);
+  double dn = quad_in_u(A, B, C, u - hh);
+  double c1 = (up - dn) / (2.0 * hh);
+  double c2 = ((up - 2.0 * mid) + dn) / (hh * hh);
+  if (!(finite(c1) && finite(c2))) {
+    flag_min(err, i);
+    out[i] = u;
+    return;
+  }
+  double stepped = newton_step(u, c1, c2, lp);
+  double cost_new = quad_in_u(A, B, C, stepped);
+  if (!(finite(mid) && finite(cost_new))) flag_min(err + 1, i);
+  double r = cost_new <= mid ? stepped : u;
+  if (!finite(r)) flag_min(err + 2, i);
+  out[i] = r;
+}
+
+__global__ void k_ex1(const double* __restrict__ u1, const double* __restrict__ m0,
+                      const double* __restrict__ m1, const double* __restrict__ m2,
+                      const int64_t* __restrict__ lo, const int64_t* __restrict__ hi, int64_t begin,
+                      int64_t n, double* out, int64_t* err) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int64_t i = begin + t;
+  const double A = m0[t], B = m1[t], C = m2[t];
+  int64_t j0 = lo[i], j1 = hi[i];
+  double bu = u1[j0];
+  double bv = quad_in_u(A, B, C, bu);
+  bool ok = finite(bv);
+  for (int64_t j = j0 + 1; j <= j1; ++j) {
+    double uj = u1[j];
+    double c = quad_in_u(A, B, C, uj);
+    ok = ok && finite(c);
+    if (c < bv) {
+      bv = c;
+      bu = uj;
+    }
+  }
+  if (!ok) flag_min(err, i);
+  out[i] = bu;
+}
+
+__global__ void k_device_libm(int which, const double* __restrict__ x, int64_t n, double* out) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  double v = x[t];
+  out[t] = which == 0 ? ucp_exp_tab(v, g_exp_tab) : (which == 1 ? ucp_erf_tab(v, g_exp_tab) : phi_cdf(v));
+}
+
+__global__ void k_fp64_probe(int iters, double* sink) {
+  double a0 = threadIdx.x * 1e-9 + 1.0, a1 = a0 + 1e-3, a2 = a0 + 2e-3, a3 = a0 + 3e-3;
+  double a4 = a0 + 4e-3, a5 = a0 + 5e-3, a6 = a0 + 6e-3, a7 = a0 + 7e-3;
+  const double m = 0.999999999, c = 1e-12;
+  for (int i = 0; i < iters; ++i) {
+    a0 = a0 * m; a1 = a1 * m; a2 = a2 * m; a3 = a3 * m;
+    a4 = a4 * m; a5 = a5 * m; a6 = a6 * m; a7 = a7 * m;
+    a0 = a0 + c; a1 = a1 + c; a2 = a2 + c; a3 = a3 + c;
+    a4 = a4 + c; a5 = a5 + c; a6 = a6 + c; a7 = a7 + c;
+  }
+  sink[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+
+}  // namespace
+
+// ============================================================ workspace
+struct ucp_workspace {
+  void* buf[8] = {nullptr};
+  size_t cap[8] = {0};
+  void* scan_tmp = nullptr;
+  size_t scan_cap = 0;
+  int64_t* h_total = nullptr;  // pinned
+};
+
+namespace {
+enum { WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL };
+
+int ws_get(ucp_workspace* ws, int slot, size_t bytes, void** out) {
+  if (ws->cap[slot] < bytes) {
+    if (ws->buf[slot]) UCP_CHECK(cudaFree(ws->buf[slot]));
+    ws->buf[slot] = nullptr;
+    ws->cap[slot] = 0;
+    size_t want = bytes + bytes / 4 + 256;
+    UCP_CHECK(cudaMalloc(&ws->buf[slot], want));
+    ws->cap[slot] = want;
+  }
+  *out = ws->buf[slot];
+  return UCP_OK;
+}
+
+// x1 = y0 + u0 and per-tile min/max, then the moments of `nq` queries.
+int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0, const double* w,
+                int64_t m, double a, double h, int64_t d, double* o0, double* o1, double* o2,
+                ucp_workspace* ws, cudaStream_t st) {
+  if (nq <= 0) return UCP_OK;
+  void *px1, *ptile;
+  int rc;
+  if ((rc = ws_get(ws, WS_X1, sizeof(double) * (size_t)m, &px1))) return rc;
+  int64_t ntiles = (m + kTile - 1) / kTile;
+  if ((rc = ws_get(ws, WS_TILE, sizeof(double2) * (size_t)ntiles, &ptile))) return rc;
+  k_x1_minmax<<<(unsigned)ntiles, kTile, 0, st>>>(y0, u0, m, (double*)px1, (double2*)ptile);
+  UCP_LAUNCHED("k_x1_minmax");
+  k_moments<<<nblocks(nq, kMomThreads), kMomThreads, 0, st>>>(yq, nq, (const double*)px1, w, m,
+                                                              (const double2*)ptile, a, h, d, o0, o1, o2);
+  UCP_LAUNCHED("k_moments");
+  return UCP_OK;
+}
+
+int check_problem(const ucp_wc_problem* P) {
+  if (!P || !P->y0 || !P->y1 || !P->f0 || !P->fw0) return arg_fail("null problem pointer");
+  if (P->d0 < 2 || P->d1 < 2) return arg_fail("grid.d must be at least 2");
+  if (P->d0 > INT32_MAX || P->d1 > INT32_MAX) return arg_fail("grid too large for int32 indices");
+  return UCP_OK;
+}
+}  // namespace
+
+// ============================================================ C ABI
+extern "C" {
+
+int ucp_abi_version(void) { return UCP_ABI_VERSION; }
+
+const char* ucp_status_string(int status) {
+  switch (status) {
+    case UCP_OK: return "ok";
+    case UCP_ERR_ARG: return "bad argument";
+    case UCP_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+const char* ucp_last_error(void) { return g_errbuf; }
+
+int64_t ucp_launch_count(void) { return g_launches.load(); }
+
+int ucp_workspace_create(ucp_workspace** ws) {
+  if (!ws) return arg_fail("null workspace handle");
+  *ws = new ucp_workspace();
+  UCP_CHECK(cudaMallocHost(&(*ws)->h_total, sizeof(int64_t)));
+  return UCP_OK;
+}
+
+int ucp_workspace_destroy(ucp_workspace* ws) {
+  if (!ws) return UCP_OK;
+  for (int i = 0; i < 8; ++i)
+    if (ws->buf[i]) cudaFree(ws->buf[i]);
+  if (ws->scan_tmp) cudaFree(ws->scan_tmp);
+  if (ws->h_total) cudaFreeHost(ws->h_total);
+  delete ws;
+  return UCP_OK;
+}
+
+int ucp_workspace_reserve(ucp_workspace* ws, int64_t d0, int64_t d1, int64_t max_cand) {
+  if (!ws) return arg_fail("null workspace");
+  void* p;
+  int rc;
+  int64_t dm = d0 > d1 ? d0 : d1;
+  if ((rc = ws_get(ws, WS_X1, sizeof(double) * (size_t)dm, &p))) return rc;
+  if ((rc = ws_get(ws, WS_TILE, sizeof(double2) * (size_t)((dm + kTile - 1) / kTile), &p))) return rc;
+  if ((rc = ws_get(ws, WS_MOM, sizeof(double) * 3 * (size_t)dm, &p))) return rc;
+  if ((rc = ws_get(ws, WS_COST, sizeof(double) * (size_t)(max_cand > 3 * dm ? max_cand : 3 * dm), &p))) return rc;
+  if ((rc = ws_get(ws, WS_COUNT, sizeof(int64_t) * (size_t)(dm + 1), &p))) return rc;
+  if ((rc = ws_get(ws, WS_CAND_PT, sizeof(int32_t) * (size_t)max_cand, &p))) return rc;
+  if ((rc = ws_get(ws, WS_CAND_J, sizeof(int32_t) * (size_t)max_cand, &p))) return rc;
+  return UCP_OK;
+}
+
+int ucp_gauss_moments_grid(const double* s, int64_t n, const double* v, double a, double h, int64_t d,
+                           double* t0, double* t1, double* t2, void* stream) {
+  if (n < 0 || d < 2 || d > INT32_MAX) return arg_fail("gauss_moments_grid: bad sizes");
+  if (n == 0) return UCP_OK;
+  WalkGrid g = make_walk_grid(a, h, d);
+  k_gauss_grid<<<nblocks(n, 128), 128, 0, as_stream(stream)>>>(s, n, v, g, t0, t1, t2);
+  UCP_LAUNCHED("k_gauss_grid");
+  return UCP_OK;
+}
+
+int ucp_gauss_moments_points(const double* y, int64_t n, const double* x, const double* w, int64_t m,
+                             double a, double h, int64_t d, double* o0, double* o1, double* o2,
+                             ucp_workspace* ws, void* stream) {
+  if (n < 0 || m < 0 || d < 2 || !ws) return arg_fail("gauss_moments_points: bad sizes");
+  if (n == 0) return UCP_OK;
+  if (m == 0) {
+    UCP_CHECK(cudaMemsetAsync(o0, 0, sizeof(double) * n, as_stream(stream)));
+    UCP_CHECK(cudaMemsetAsync(o1, 0, sizeof(double) * n, as_stream(stream)));
+    UCP_CHECK(cudaMemsetAsync(o2, 0, sizeof(double) * n, as_stream(stream)));
+    return UCP_OK;
+  }
+  return run_moments(y, n, nullptr, x, w, m, a, h, d, o0, o1, o2, ws, as_stream(stream));
+}
+
+int ucp_trapezoid_sum(const double* samples, int64_t n, double spacing, double* out, int64_t* err,
+                      void* stream) {
+  if (n < 1) return arg_fail("trapezoid needs at least one sample");
+  k_trapezoid<<<1, 32, 0, as_stream(stream)>>>(samples, n, spacing, out, err);
+  UCP_LAUNCHED("k_trapezoid");
+  return UCP_OK;
+}
+
+int ucp_segmented_argmin(const double* costs, const int64_t* offsets, int64_t nseg, int64_t* out,
+                         void* stream) {
+  if (nseg < 0) return arg_fail("segmented_argmin: bad sizes");
+  if (nseg == 0) return UCP_OK;
+  k_segmented_argmin<<<nblocks(nseg, 128), 128, 0, as_stream(stream)>>>(costs, offsets, nseg, out);
+  UCP_LAUNCHED("k_segmented_argmin");
+  return UCP_OK;
+}
+
+int ucp_device_libm(int which, const double* x, int64_t n, double* out, void* stream) {
+  if (which < 0 || which > 2 || n < 0) return arg_fail("device_libm: bad argument");
+  if (n == 0) return UCP_OK;
+  k_device_libm<<<nblocks(n, 256), 256, 0, as_stream(stream)>>>(which, x, n, out);
+  UCP_LAUNCHED("k_device_libm");
+  return UCP_OK;
+}
+
+int ucp_wc_stage0_cost(const ucp_wc_problem* P, const double* v1, const double* u_flat, int64_t n_cand,
+                       const int64_t* offsets, const double* y_seg, const double* f0_seg, int64_t nseg,
+                       double* out, void* stream) {
+  int rc = check_problem(P);
+  if (rc) return rc;
+  if (nseg < 0 || n_cand < 0) return arg_fail("stage0_cost: bad sizes");
+  if (nseg == 0 || n_cand == 0) return UCP_OK;
+  const int64_t n_host = n_cand;
+  WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
+  k_stage0_segmented<<<nblocks(n_host, 128), 128, 0, as_stream(stream)>>>(u_flat, offsets, nseg, y_seg,
+                                                                           f0_seg, P->k, v1, g, out);
+  UCP_LAUNCHED("k_stage0_segmented");
+  return UCP_OK;
+}
+
+int ucp_wc_stage1_cost(const ucp_wc_problem* P, const double* u0, const double* u_flat, int64_t n_cand,
+                       const int64_t* offsets, const double* y_seg, int64_t nseg, double* out,
+                       ucp_workspace* ws, void* stream) {
+  int rc = check_problem(P);
+  if (rc) return rc;
+  if (nseg < 0 || n_cand < 0 || !ws) return arg_fail("stage1_cost: bad sizes");
+  if (nseg == 0 || n_cand == 0) return UCP_OK;
+  cudaStream_t st = as_stream(stream);
+  void* pm;
+  if ((rc = ws_get(ws, WS_MOM, sizeof(double) * 3 * (size_t)nseg, &pm))) return rc;
+  double* m0 = (double*)pm;
+  if ((rc = run_moments(y_seg, nseg, P->y0, u0, P->fw0, P->d0, P->a1, P->h1, P->d1, m0, m0 + nseg,
+                        m0 + 2 * nseg, ws, st)))
+    return rc;
+  const int64_t n_host = n_cand;
+  k_stage1_segmented<<<nblocks(n_host, 256), 256, 0, st>>>(u_flat, offsets, nseg, m0, m0 + nseg,
+                                                             m0 + 2 * nseg, out);
+  UCP_LAUNCHED("k_stage1_segmented");
+  return UCP_OK;
+}
+
+int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, const double* u1,
+                        const ucp_local_params* lp, int64_t begin, int64_t end, double* out, int64_t* err,
+                        ucp_workspace* ws, void* stream) {
+  int rc = check_problem(P);
+  if (rc) return rc;
+  if (!lp || !ws || !err) return arg_fail("local_update: null argument");
+  int64_t d = stage == 0 ? P->d0 : P->d1;
+  if (stage < 0 || stage > 1) return arg_fail("stage index out of range for witsenhausen");
+  if (begin < 0 || end > d || begin > end) return arg_fail("local_update: bad shard");
+  int64_t n = end - begin;
+  if (n == 0) return UCP_OK;
+  cudaStream_t st = as_stream(stream);
+  if (stage == 0) {
+    void* pc;
+    if ((rc = ws_get(ws, WS_COST, sizeof(double) * 3 * (size_t)n, &pc))) return rc;
+    WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
+    k_lu0_probe<<<nblocks(3 * n, 128), 128, 0, st>>>(P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
+                                                     (double*)pc);
+    UCP_LAUNCHED("k_lu0_probe");
+    k_lu0_finish<<<nblocks(n, 128), 128, 0, st>>>(P->y0, P->f0, u0, P->k, u1, g, *lp, begin, n,
+                                                  (const double*)pc, out, err);
+    UCP_LAUNCHED("k_lu0_finish");
+    return UCP_OK;
+  }
+  void* pm;
+  if ((rc = ws_get(ws, WS_MOM, sizeof(double) * 3 * (size_t)n, &pm))) return rc;
+  double* m0 = (double*)pm;
+  if ((rc = run_moments(P->y1 + begin, n, P->y0, u0, P->fw0, P->d0, P->a1, P->h1, P->d1, m0, m0 + n,
+                        m0 + 2 * n, ws, st)))
+    return rc;
+  k_lu1<<<nblocks(n, 256), 256, 0, st>>>(u1, m0, m0 + n, m0 + 2 * n, *lp, begin, n, out, err);
+  UCP_LAUNCHED("k_lu1");
+  return UCP_OK;
+}
+
+int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, const double* u1,
+                      const int64_t* win_lo, const int64_t* win_hi, int64_t begin, int64_t end,
+                      double* out, int64_t* err, ucp_workspace* ws, void* stream) {
+  int rc = check_problem(P);
+  if (rc) return rc;
+  if (!ws || !err || !win_lo || !win_hi) return arg_fail("exhaustion: null argument");
+  if (stage < 0 || stage > 1) return arg_fail("stage index out of range for witsenhausen");
+  int64_t d = stage == 0 ? P->d0 : P->d1;
+  if (begin < 0 || end > d || begin > end) return arg_fail("exhaustion: bad shard");
+  int64_t n = end - begin;
+  if (n == 0) return UCP_OK;
+  cudaStream_t st = as_stream(stream);
+  if (stage == 1) {
+    void* pm;
+    if ((rc = ws_get(ws, WS_MOM, sizeof(double) * 3 * (size_t)n, &pm))) return rc;
+    double* m0 = (double*)pm;
+    if ((rc = run_moments(P->y1 + begin, n, P->y0, u0, P->fw0, P->d0, P->a1, P->h1, P->d1, m0, m0 + n,
+                          m0 + 2 * n, ws, st)))
+      return rc;
+    k_ex1<<<nblocks(n, 256), 256, 0, st>>>(u1, m0, m0 + n, m0 + 2 * n, win_lo, win_hi, begin, n, out, err);
+    UCP_LAUNCHED("k_ex1");
+    return UCP_OK;
+  }
+  void *pcount, *ptotal;
+  if ((rc = ws_get(ws, WS_COUNT, sizeof(int64_t) * (size_t)(n + 1), &pcount))) return rc;
+  if ((rc = ws_get(ws, WS_TOTAL, sizeof(int64_t) * 2, &ptotal))) return rc;
+  int64_t* counts = (int64_t*)pcount;  // counts[0..n) -> exclusive offsets[0..n]
+  k_ex_count<<<nblocks(n, 256), 256, 0, st>>>(u0, win_lo, win_hi, begin, n, counts);
+  UCP_LAUNCHED("k_ex_count");
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, counts, n + 1, st);
+  if (ws->scan_cap < tmp_bytes) {
+    if (ws->scan_tmp) UCP_CHECK(cudaFree(ws->scan_tmp));
+    UCP_CHECK(cudaMalloc(&ws->scan_tmp, tmp_bytes));
+    ws->scan_cap = tmp_bytes;
+  }
+  // counts[n] is scratch: the scan over n+1 items leaves the total in it
+  UCP_CHECK(cudaMemsetAsync(counts + n, 0, sizeof(int64_t), st));
+  UCP_CHECK(cub::DeviceScan::ExclusiveSum(ws->scan_tmp, tmp_bytes, counts, counts, n + 1, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  UCP_CHECK(cudaMemcpyAsync(ws->h_total, counts + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  UCP_CHECK(cudaStreamSynchronize(st));
+  int64_t total = *ws->h_total;
+  void *ppt, *pj, *pc;
+  if ((rc = ws_get(ws, WS_CAND_PT, sizeof(int32_t) * (size_t)total, &ppt))) return rc;
+  if ((rc = ws_get(ws, WS_CAND_J, sizeof(int32_t) * (size_t)total, &pj))) return rc;
+  if ((rc = ws_get(ws, WS_COST, sizeof(double) * (size_t)total, &pc))) return rc;
+  k_ex_fill<<<nblocks(n, 256), 256, 0, st>>>(u0, win_lo, win_hi, begin, n, counts, (int32_t*)ppt,
+                                               (int32_t*)pj);
+  UCP_LAUNCHED("k_ex_fill");
+  WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
+  k_ex0_eval<<<nblocks(total, 128), 128, 0, st>>>(P->y0, P->f0, u0, P->k, u1, g, counts + n,
+                                                  (const int32_t*)ppt, (const int32_t*)pj, (double*)pc);
+  UCP_LAUNCHED("k_ex0_eval");
+  k_ex_argmin<<<nblocks(n, 256), 256, 0, st>>>(u0, (const double*)pc, counts, (const int32_t*)pj, begin, n,
+                                               out, err);
+  UCP_LAUNCHED("k_ex_argmin");
+  return UCP_OK;
+}
+
+int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const double* u1, int64_t begin,
+                           int64_t end, double* terms, int64_t* err, void* stream) {
+  int rc = check_problem(P);
+  if (rc) return rc;
+  if (begin < 0 || end > P->d0 || begin > end) return arg_fail("objective_terms: bad shard");
+  if (end == begin) return UCP_OK;
+  WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
+  k_obj_terms<<<nblocks(end - begin, 128), 128, 0, as_stream(stream)>>>(P->y0, P->f0, u0, P->k, u1, g,
+                                                                          begin, end, terms, err);
+  UCP_LAUNCHED("k_obj_terms");
+  return UCP_OK;
+}
+
+int ucp_fp64_probe(int blocks, int threads, int iters, double* sink, void* stream) {
+  if (blocks <= 0 || threads <= 0 || iters <= 0) return arg_fail("fp64_probe: bad sizes");
+  k_fp64_probe<<<blocks, threads, 0, as_stream(stream)>>>(iters, sink);
+  UCP_LAUNCHED("k_fp64_probe");
+  return UCP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,259 @@
+"""Witsenhausen's counterexample on the B200 (reference problems/witsenhausen.py).
+
+    x1 = x0 + u0(y0),  y1 = x1 + w,  x2 = x1 - u1(y1),  cost = k^2 u0^2 + x2^2
+    x0 ~ N(0, sigma^2),  w ~ N(0, 1),  y0 = x0
+
+Stage-0 marginal cost (witsenhausen.py:62-70):
+    C0(u, y) = f0(y) * (k^2 u^2 + sum_j W_j phi(y1_j - s) (s - u1_j)^2 + tails),  s = y + u
+Stage-1 marginal cost (witsenhausen.py:71-78), the u1 estimator moments:
+    C1(u, y) = A u^2 - 2 B u + C,  (A, B, C) = sum_i fw0_i phi(y - x1_i) (1, x1_i, x1_i^2)
+
+All per-candidate work runs in libucp_b200 (csrc/ucp_kernels.cu) on
+device-resident controllers; only the NumPy density constants (f0, fw0) and
+the window bounds are computed on the host, once per problem.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import F64, I64, ptr, require_cuda, stream_ptr, to_device_f64, to_device_i64
+from .distributed import LOCAL, Sharding
+from .grids import ControllerSet, node_window_bounds
+from .numerics import Gaussian, pdf
+from .problem import NumericError, Problem
+
+__all__ = ["Witsenhausen"]
+
+NO_ERROR = _lib.NO_ERROR
+
+
+class _ErrorLog:
+    """Device-side failure slots, one row of 3 int64 per phase, read lazily.
+
+    A phase never stalls the stream to look for non-finite values: it
+    atomicMin's the first offending grid point into its row, and the host
+    reads all pending rows at the next synchronisation point (the objective,
+    or the end of the solve).  The first phase (in execution order) with a
+    failure raises exactly the exception the reference raises at that phase;
+    work issued after it is discarded with the exception.
+    """
+
+    def __init__(self, device, problem, capacity: int = 1024):
+        self.device = device
+        self.problem = problem
+        self.rows = torch.full((capacity, 3), NO_ERROR, dtype=I64, device=device)
+        self.meta: list[tuple] = []
+
+    def slot(self, kind: str, stage: int, sharding: Sharding) -> torch.Tensor:
+        if len(self.meta) == self.rows.shape[0]:
+            self.flush(sharding)
+        row = self.rows[len(self.meta)]
+        self.meta.append((kind, stage))
+        return row
+
+    def flush(self, sharding: Sharding) -> None:
+        n = len(self.meta)
+        if n == 0:
+            return
+        rows = self.rows[:n]
+        sharding.allreduce_min_(rows)
+        host = rows.cpu().numpy()
+        rows.fill_(NO_ERROR)
+        meta, self.meta = self.meta, []
+        for (kind, m), row in zip(meta, host):
+            if (row != NO_ERROR).any():
+                raise _phase_error(self.problem, kind, m, row)
+
+
+def _phase_error(problem, kind, m, row):
+    name = problem.name if problem is not None else "witsenhausen"
+    pts = problem.grids[m].points if problem is not None else None
+    phase = {"local": "local-update", "exhaustion": "partial-exhaustion"}[kind]
+    for slot in range(3 if kind == "local" else 1):
+        i = int(row[slot])
+        if i == NO_ERROR:
+            continue
+        if slot == 2:  # grids.py: SampledController rejects non-finite values
+            return ValueError(f"controller value at grid point {i} is not finite")
+        y = pts[i] if pts is not None else float("nan")
+        return NumericError(
+            f"{name}: non-finite marginal cost in {phase} phase at stage {m}, grid point {i} (y={y!r})")
+    raise AssertionError("no failure in row")
+
+
+class _WcDevice:
+    """Device-resident constants, ABI structs and scratch of one Witsenhausen problem."""
+
+    def __init__(self, prob: "Witsenhausen", device=None):
+        self.lib = _lib.load()
+        self.device = require_cuda(device)
+        g0, g1 = prob.grids
+        self.y0 = to_device_f64(g0.points, self.device)
+        self.y1 = to_device_f64(g1.points, self.device)
+        self.f0 = to_device_f64(prob._f0, self.device)
+        self.fw0 = to_device_f64(prob._fw0, self.device)
+        self.P = _lib.WcProblem(prob.k, g0.a, g0.spacing, g0.d, g1.a, g1.spacing, g1.d,
+                                ptr(self.y0), ptr(self.y1), ptr(self.f0), ptr(self.fw0))
+        ws = ctypes.c_void_p()
+        _lib.call("ucp_workspace_create", ctypes.byref(ws))
+        self.ws = ws
+        self.errors = _ErrorLog(self.device, prob)
+        self.windows: dict = {}
+
+    def __del__(self):
+        try:
+            if self.ws:
+                torch.cuda.synchronize(self.device)
+                self.lib.ucp_workspace_destroy(self.ws)
+        except Exception:  # interpreter shutdown
+            pass
+
+    @property
+    def stream(self) -> int:
+        return stream_ptr(self.device)
+
+    def window(self, prob, m: int, r: float):
+        key = (m, float(r))
+        if key not in self.windows:
+            lo, hi = node_window_bounds(prob.grids[m], r)
+            self.windows[key] = (to_device_i64(lo, self.device), to_device_i64(hi, self.device))
+        return self.windows[key]
+
+
+class Witsenhausen(Problem):
+    name = "witsenhausen"
+
+    def __init__(self, k: float = 0.2, sigma: float = 5.0, grids=None, device=None):
+        if not k > 0.0:
+            raise ValueError(f"witsenhausen.k must be positive (got {k})")
+        if not sigma > 0.0:
+            raise ValueError(f"witsenhausen.sigma must be positive (got {sigma})")
+        self.k = float(k)
+        self.sigma = float(sigma)
+        super().__init__(grids)
+        self._state_density = Gaussian(0.0, self.sigma)
+        g0 = self.grids[0]
+        # host NumPy constants, exactly as the reference (witsenhausen.py:47-53)
+        self._f0 = pdf(self._state_density, g0.points)
+        w0 = np.full(g0.d, g0.spacing)
+        w0[0] *= 0.5
+        w0[-1] *= 0.5
+        self._fw0 = w0 * self._f0
+        self._device_arg = device
+        self._dev: _WcDevice | None = None
+
+    def default_grid_specs(self):
+        return [(-25.0, 25.0, 2000), (-25.0, 25.0, 2000)]
+
+    # ------------------------------------------------------------- device
+    def device_context(self) -> _WcDevice:
+        if self._dev is None:
+            self._dev = _WcDevice(self, self._device_arg)
+        return self._dev
+
+    @property
+    def device(self) -> torch.device:
+        return self.device_context().device
+
+    def _override_host_constants(self, f0, fw0) -> None:
+        """Replace the host-NumPy densities (parity tests replaying a reference
+        run made on another host's NumPy); must precede first device use."""
+        if self._dev is not None:
+            raise RuntimeError("device context already created")
+        self._f0 = np.ascontiguousarray(f0, dtype=np.float64)
+        self._fw0 = np.ascontiguousarray(fw0, dtype=np.float64)
+
+    def _uv(self, U: ControllerSet):
+        dev = self.device_context().device
+        return U.device_values(0, dev), U.device_values(1, dev)
+
+    # ------------------------------------------------- plugin API (host I/O)
+    def marginal_cost_segmented(self, m, u_flat, offsets, y_centers, U):
+        """witsenhausen.py:59-79; host arrays in, host array out."""
+        if m not in (0, 1):
+            raise ValueError(f"stage index {m} out of range for {self.name}")
+        D = self.device_context()
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        y_centers = np.ascontiguousarray(y_centers, dtype=np.float64)
+        u_flat = np.ascontiguousarray(u_flat, dtype=np.float64)
+        nseg = offsets.size - 1
+        if nseg != y_centers.size:
+            raise ValueError("offsets and y_centers disagree")
+        n = int(offsets[-1]) if nseg >= 0 else 0
+        out = torch.empty(max(n, 1), dtype=F64, device=D.device)
+        if n:
+            u0, u1 = self._uv(U)
+            ud = to_device_f64(u_flat, D.device)
+            od = to_device_i64(offsets, D.device)
+            yd = to_device_f64(y_centers, D.device)
+            if m == 0:
+                f0 = to_device_f64(pdf(self._state_density, y_centers), D.device)
+                _lib.call("ucp_wc_stage0_cost", ctypes.byref(D.P), ptr(u1), ptr(ud), n, ptr(od), ptr(yd),
+                          ptr(f0), nseg, ptr(out), D.stream)
+            else:
+                _lib.call("ucp_wc_stage1_cost", ctypes.byref(D.P), ptr(u0), ptr(ud), n, ptr(od), ptr(yd),
+                          nseg, ptr(out), D.ws, D.stream)
+        return out[:n].cpu().numpy()
+
+    # ------------------------------------------------ solver sweeps (device)
+    def device_local_update(self, m: int, U: ControllerSet, cfg, sharding: Sharding = LOCAL):
+        """One local-update sweep of stage m (solver.py:179-203); returns a CUDA tensor."""
+        D = self.device_context()
+        g = self.grids[m]
+        u0, u1 = self._uv(U)
+        lp = _lib.LocalParams(cfg.fd_step, cfg.curvature_min, cfg.grad_step, cfg.cap_for(g))
+        begin, end = sharding.bounds(g.d)
+        buf = sharding.out_buffer(g.d, D.device)
+        err = D.errors.slot("local", m, sharding)
+        _lib.call("ucp_wc_local_update", ctypes.byref(D.P), m, ptr(u0), ptr(u1), ctypes.byref(lp), begin, end,
+                  ptr(buf), ptr(err), D.ws, D.stream)
+        sharding.allgather_(buf)
+        return buf[: g.d]
+
+    def device_exhaustion(self, m: int, U: ControllerSet, cfg, sharding: Sharding = LOCAL):
+        """One partial-exhaustion sweep of stage m (solver.py:206-223)."""
+        D = self.device_context()
+        g = self.grids[m]
+        u0, u1 = self._uv(U)
+        lo, hi = D.window(self, m, cfg.radius_for(g))
+        begin, end = sharding.bounds(g.d)
+        buf = sharding.out_buffer(g.d, D.device)
+        err = D.errors.slot("exhaustion", m, sharding)
+        _lib.call("ucp_wc_exhaustion", ctypes.byref(D.P), m, ptr(u0), ptr(u1), ptr(lo), ptr(hi), begin, end,
+                  ptr(buf), ptr(err), D.ws, D.stream)
+        sharding.allgather_(buf)
+        return buf[: g.d]
+
+    def device_objective(self, U: ControllerSet, sharding: Sharding = LOCAL) -> float:
+        """problem.py:110-127: stage-0 integrand on device, then the serial trapezoid."""
+        self.check_controllers(U)
+        D = self.device_context()
+        D.errors.flush(sharding)  # earlier phases fail first, in order
+        g = self.grids[0]
+        u0, u1 = self._uv(U)
+        begin, end = sharding.bounds(g.d)
+        terms = sharding.out_buffer(g.d, D.device)
+        res = torch.full((2,), NO_ERROR, dtype=I64, device=D.device)  # [J bits, first bad point]
+        _lib.call("ucp_wc_objective_terms", ctypes.byref(D.P), ptr(u0), ptr(u1), begin, end, ptr(terms),
+                  res[1:].data_ptr(), D.stream)
+        sharding.allgather_(terms)
+        sharding.allreduce_min_(res[1:])
+        _lib.call("ucp_trapezoid_sum", ptr(terms), g.d, g.spacing, res[:1].data_ptr(), None, D.stream)
+        host = res.cpu().numpy()
+        bad = int(host[1])
+        if bad != NO_ERROR:
+            raise NumericError(
+                f"{self.name}: non-finite objective integrand at stage 0, grid point {bad} "
+                f"(y={g.points[bad]!r}, u={U.values(0)[bad]!r})")
+        return float(host[:1].view(np.float64)[0])
+
+    def flush_errors(self, sharding: Sharding = LOCAL) -> None:
+        if self._dev is not None:
+            self._dev.errors.flush(sharding)
+
+    def objective(self, U) -> float:
+        return self.device_objective(U)

@@ -1,0 +1,125 @@
+"""CPU tests: the C-ABI library loads and exports every declared symbol; host
+logic (grids, windows, config validation, allocation) matches the reference."""
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    src = (ROOT / "include" / "ucp_b200.h").read_text()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ucp_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1908_04489_b200 import _build, _lib
+
+    _build.build()
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    syms = declared_symbols()
+    assert len(syms) >= 17
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
+    L = _lib.load()
+    assert L.ucp_abi_version() == 1
+    assert L.ucp_status_string(1) == b"bad argument"
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    import torch
+
+    import paper_1908_04489_b200 as P
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    prob = P.Witsenhausen(grids=[(-25.0, 25.0, 51)] * 2)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        prob.objective(prob.identity_controllers())
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        P.kernels.gauss_moments_grid(np.zeros(3), np.zeros(5), -1.0, 0.5, 5)
+
+
+def test_ptx_walk_has_no_contracted_fma(tmp_path):
+    """ref-order: no FMA contraction anywhere in the stage-0 walk kernel.
+
+    Every f64 mul/add/sub must carry the explicit .rn modifier (which ptxas
+    never fuses), and the only fma.rn.f64 are the ones the glibc exp port
+    spells (8 on the main path + 1 in its special case, per inlined exp)."""
+    import re
+    import subprocess
+
+    from paper_1908_04489_b200 import _build
+
+    ptx = tmp_path / "k.ptx"
+    subprocess.run([_build.nvcc(), "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-fmad=false",
+                    "-ptx", str(_build.SOURCES[0]), "-o", str(ptx)], check=True)
+    text = ptx.read_text()
+    body = re.search(r"\.entry [^(]*k_gauss_grid.*?\n}", text, flags=re.S).group(0)
+    ops = re.findall(r"\b(mul|add|sub|fma)((?:\.[a-z0-9]+)*)\.f64\b", body)
+    assert ops
+    for op, mods in ops:
+        assert ".rn" in mods, (op, mods)
+    n_fma = sum(1 for op, _ in ops if op == "fma")
+    assert n_fma % 9 == 0 and n_fma > 0, n_fma
+
+
+def test_grids_and_windows_match_oracle_restatement(oracle_mod):
+    import paper_1908_04489_b200 as P
+
+    for d, r in [(201, 0.5), (2000, 0.5), (1 << 16, 19.5 * 50.0 / ((1 << 16) - 1)), (7, 3.0)]:
+        g = P.make_grid(-25.0, 25.0, d)
+        lo, hi = P.node_window_bounds(g, r)
+        olo, ohi = oracle_mod.node_window_bounds(g.points, g.a, g.spacing, g.d, r)
+        np.testing.assert_array_equal(lo, olo)
+        np.testing.assert_array_equal(hi, ohi)
+        assert P.window_bounds(g, g.points[d // 2], r) == (lo[d // 2], hi[d // 2])
+
+
+def test_solver_config_validation_and_allocation():
+    import paper_1908_04489_b200 as P
+
+    with pytest.raises(ValueError, match="iters_per_round"):
+        P.SolverConfig(iters_per_round=1)
+    with pytest.raises(ValueError, match="fixed_local_iters"):
+        P.SolverConfig(fixed_local_iters=20)
+    with pytest.raises(ValueError, match="search_radius"):
+        P.SolverConfig(search_radius=0.0)
+    assert P.adaptive_allocation(0.0, 0.0, 20) == (10, 10)
+    assert P.adaptive_allocation(1.0, 0.0, 20) == (19, 1)
+    assert P.adaptive_allocation(0.0, 1.0, 20) == (1, 19)
+    assert P.adaptive_allocation(3.0, 1.0, 20) == (15, 5)
+    g = P.make_grid(-25, 25, 2000)
+    assert P.SolverConfig().radius_for(g) == 0.5 and P.SolverConfig().cap_for(g) == 5.0
+
+
+def test_controller_validation():
+    import paper_1908_04489_b200 as P
+
+    g = P.make_grid(-1, 1, 5)
+    with pytest.raises(ValueError, match="not finite"):
+        P.SampledController(g, [0, 1, np.nan, 2, 3])
+    with pytest.raises(ValueError, match="needs 5 values"):
+        P.SampledController(g, [0, 1])
+    c = P.SampledController(g, np.arange(5.0))
+    assert not c.values.flags.writeable
+    with pytest.raises(AttributeError):
+        c.grid = g
+    assert P.eval_controller(c, 0.24) == 2.0 and P.eval_controller(c, 0.25) == 2.0
+    assert P.eval_controller(c, 9.0) == 4.0
+
+
+def test_witsenhausen_validation():
+    import paper_1908_04489_b200 as P
+
+    with pytest.raises(ValueError, match="k must be positive"):
+        P.Witsenhausen(k=0.0)
+    with pytest.raises(ValueError, match="needs 2 stage grids"):
+        P.Witsenhausen(grids=[(-1, 1, 5)])
+    with pytest.raises(ValueError, match="problem must be one of"):
+        P.make_problem("nope")
