@@ -35,13 +35,19 @@ def stream_ptr(device: torch.device) -> int:
 def to_device_f64(x, device) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=F64).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(device)
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    if not a.flags.writeable:
+        a = a.copy()
+    return torch.from_numpy(a).to(device)
 
 
 def to_device_i64(x, device) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=I64).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64)).to(device)
+    a = np.ascontiguousarray(x, dtype=np.int64)
+    if not a.flags.writeable:
+        a = a.copy()
+    return torch.from_numpy(a).to(device)
 
 
 def to_host_f64(x) -> np.ndarray:
