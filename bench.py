@@ -2,15 +2,14 @@
 """Benchmark: marginal-cost evaluations/s of the Witsenhausen hot path at 2^20.
 
 Workload (BASELINE.json configs[1]): Witsenhausen k=0.2, sigma=5 on two
-2^20-point grids over [-25, 25], FP64, controllers warm-started from the
-converged default-grid (d=2000) solution, nearest-resampled (deterministic).
+2^20-point grids over [-25, 25], FP64.  Controllers: the converged
+default-grid (d=2000) solution, linearly interpolated onto the fine grid
+(deterministic; every value distinct, like controllers after a local sweep).
 SolverConfig(search_radius=19.5 h): 39-node exhaustion windows.
 
-One *step* = one solver iteration of each block type over both stages plus
-the objective, i.e. what a round of the reference does per iteration:
+One *step* = every hot-path phase once on that controller snapshot:
     local_update(m=0), local_update(m=1), exhaustion(m=0), exhaustion(m=1), J.
-Every step starts from the same warm controllers, so all steps do identical
-work.  ``value`` counts the marginal-cost evaluations the REFERENCE performs
+Every step reads the same snapshot, so all steps do identical work.  ``value`` counts the marginal-cost evaluations the REFERENCE performs
 for that step (5 per point per stage for a local sweep, one per distinct
 window candidate for an exhaustion sweep, one per point for J) divided by
 the device time; both arms use this same count, so their ratio is a pure
@@ -43,12 +42,15 @@ K_WC, SIGMA = 0.2, 5.0
 SPAN = (-25.0, 25.0)
 C1_D = 2000
 DP_OPS_PER_NODE = 8  # kernels.py:430-439: 3 mul + 3 add accumulate, 2 mul recurrence
+# kernels.py:466-482 per in-range pair: sub, 2 compares, 2 mul, exp (12 DP on the glibc
+# FMA3 path), *factor, *INV, != 0, *w, 3 add, 2 mul
+DP_OPS_PER_PAIR = 27
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--log2d", type=int, default=20)
@@ -66,11 +68,10 @@ def grid_points(d):
 
 
 def resample(u_coarse, d):
-    """Nearest-point resampling of a d=2000 controller onto the fine grid (grids.py:141-145)."""
+    """Linear interpolation of a d=2000 controller onto the fine grid."""
     y, _ = grid_points(d)
-    _, ch = grid_points(u_coarse.size)
-    near = np.clip(np.ceil((y - SPAN[0]) / ch - 0.5).astype(np.int64), 0, u_coarse.size - 1)
-    return np.ascontiguousarray(u_coarse[near])
+    yc, _ = grid_points(u_coarse.size)
+    return np.ascontiguousarray(np.interp(y, yc, u_coarse))
 
 
 def walk_nodes(s, a, h, d):
@@ -95,8 +96,27 @@ def window_bounds(d, r):
     return np.maximum(0, np.minimum(lo, ic)), np.minimum(d - 1, np.maximum(hi, ic))
 
 
+def exhaustion_nodes(u0, y, lo, hi, h, d):
+    """Visited walk nodes of all exhaustion candidates (run-start dedup, as the kernels)."""
+    total = 0.0
+    flags = np.concatenate([[True], u0[1:] != u0[:-1]])
+    for k in range(int((hi - lo).max()) + 1):
+        j = lo + k
+        ok = j <= hi
+        jj = np.minimum(j, d - 1)
+        first = ok & ((k == 0) | flags[jj])
+        total += float(walk_nodes(y[first] + u0[jj[first]], SPAN[0], h, d).sum())
+    return total
+
+
+def moments_pairs(x1, yq):
+    """In-range (|y - x| <= 12) support pairs of the stage-1 moments."""
+    xs = np.sort(x1)
+    return float((np.searchsorted(xs, yq + 12.0, side="right") - np.searchsorted(xs, yq - 12.0)).sum())
+
+
 def workload_counts(u0, u1, d, r, fd_step=1e-4):
-    """Reference evaluation count per step and algorithmic DP ops of the local m=0 sweep."""
+    """Reference evaluation count per step and algorithmic work of the kernels."""
     y, h = grid_points(d)
     lo, hi = window_bounds(d, r)
     cand0 = int(window_candidates(u0, lo, hi).sum())
@@ -105,8 +125,12 @@ def workload_counts(u0, u1, d, r, fd_step=1e-4):
     hh = fd_step * (1.0 + np.abs(u0))
     s = y + u0
     nodes = (walk_nodes(s + hh, SPAN[0], h, d) + 2 * walk_nodes(s, SPAN[0], h, d) + walk_nodes(s - hh, SPAN[0], h, d))
+    ex_nodes = exhaustion_nodes(u0, y, lo, hi, h, d)
+    pairs = moments_pairs(y + u0, y)
     return {"evals": evals, "cand0": cand0, "cand1": cand1, "lu0_nodes": float(nodes.sum()),
-            "lu0_dp_ops": float(nodes.sum()) * DP_OPS_PER_NODE}
+            "lu0_dp_ops": float(nodes.sum()) * DP_OPS_PER_NODE, "ex0_nodes": ex_nodes,
+            "ex0_dp_ops": ex_nodes * DP_OPS_PER_NODE, "moment_pairs": pairs,
+            "moment_dp_ops": pairs * DP_OPS_PER_PAIR}
 
 
 class ClockSampler:
@@ -149,7 +173,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------ CPU (oracle) timing
-def cpu_step_seconds(orc, p, u0, u1, d, r, target_s):
+def cpu_step_seconds(orc, p, u0, u1, d, r, target_s, cand_per_point=1.0):
     """Time the reference's CPU algorithm (the oracle port, all host threads) on
     bounded samples of every phase of one step; extrapolate to the full grid."""
     cfg = orc.OracleConfig(search_radius=r)
@@ -159,7 +183,7 @@ def cpu_step_seconds(orc, p, u0, u1, d, r, target_s):
     per = target_s / 5.0
     n_lu0 = int(np.clip(per * node_rate / (5 * W), 16, d))
     n_lu1 = int(np.clip(per * pair_rate / (5 * d), 4, d))
-    n_ex0 = int(np.clip(per * node_rate / (1.2 * W), 16, d))
+    n_ex0 = int(np.clip(per * node_rate / (cand_per_point * W), 16, d))
     n_ex1 = int(np.clip(per * pair_rate / d, 4, d))
     n_obj = int(np.clip(per * node_rate / W, 16, d))
     rng = np.random.default_rng(0)
@@ -207,11 +231,12 @@ def run_reference(args):
     r = (args.window_nodes / 2.0) * p.h0
     counts = workload_counts(u0, u1, d, r)
     per_step = max(args.cpu_seconds, 2.0)
+    cpp = counts["cand0"] / d
     for _ in range(args.warmup):
-        cpu_step_seconds(orc, p, u0, u1, d, r, per_step / 4)
+        cpu_step_seconds(orc, p, u0, u1, d, r, per_step / 4, cpp)
     steps, last = [], None
     for _ in range(args.steps):
-        tot, times, thr, sample = cpu_step_seconds(orc, p, u0, u1, d, r, per_step)
+        tot, times, thr, sample = cpu_step_seconds(orc, p, u0, u1, d, r, per_step, cpp)
         steps.append(tot)
         last = (times, thr, sample)
     sec = float(np.mean(steps))
@@ -232,15 +257,18 @@ def run_reference(args):
 
 
 def config_dict(args, d, counts):
-    return {"workload": f"witsenhausen k={K_WC} sigma={SIGMA} grids 2x{d} on [-25,25], warm start "
-                        f"(d=2000 solution resampled), search_radius={args.window_nodes / 2}h; step = "
-                        "local(m=0,1) + exhaustion(m=0,1) + objective",
+    return {"workload": f"witsenhausen k={K_WC} sigma={SIGMA} grids 2x{d} on [-25,25], controllers = "
+                        f"d=2000 solution linearly interpolated, search_radius={args.window_nodes / 2}h; step = every "
+                        "phase once on that snapshot: local(m=0,1) + exhaustion(m=0,1) + objective",
             "grid_points": d, "window_nodes": args.window_nodes,
             "evals_per_step": counts["evals"], "exhaustion_candidates": [counts["cand0"], counts["cand1"]],
             "l2": "inputs re-read each step; L2 flushed between steps (256 MiB memset inside timed region)"}
 
 
 # ------------------------------------------------------------ our B200 arm
+PHASES = (("local0", "local", 0), ("local1", "local", 1), ("exh0", "exhaustion", 0), ("exh1", "exhaustion", 1))
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -259,9 +287,9 @@ def run_ours(args):
     sh = P.from_process_group() if world > 1 else P.LOCAL
     d = 1 << args.log2d
 
-    # time-to-converge at the default grid (C1), on this GPU; also the warm start
+    # time-to-converge at the default grid (C1) on the GPU(s); it also gives the snapshot
     c1p = P.Witsenhausen(k=K_WC, sigma=SIGMA)
-    c1p.objective(c1p.identity_controllers())  # context + first-launch warm-up
+    c1p.objective(c1p.identity_controllers())  # context creation + first launches
     torch.cuda.synchronize()
     t = time.perf_counter()
     res = P.solve(c1p, P.SolverConfig(), sharding=sh)
@@ -273,43 +301,40 @@ def run_ours(args):
     prob = P.Witsenhausen(k=K_WC, sigma=SIGMA, grids=[(*SPAN, d), (*SPAN, d)])
     h = prob.grids[0].spacing
     cfg = P.SolverConfig(search_radius=(args.window_nodes / 2.0) * h)
-    U0 = P.ControllerSet((P.SampledController(prob.grids[0], u0h), P.SampledController(prob.grids[1], u1h)))
-    U0 = P.ControllerSet(tuple(P.SampledController(prob.grids[m], U0.device_values(m, dev)) for m in (0, 1)))
+    U0 = P.ControllerSet(tuple(P.SampledController(prob.grids[m], torch.from_numpy(u).to(dev))
+                               for m, u in ((0, u0h), (1, u1h))))
     counts = workload_counts(u0h, u1h, d, cfg.radius_for(prob.grids[0]))
     begin, end = sh.bounds(d)
-    counts_local_ops = counts["lu0_dp_ops"] * (end - begin) / d
+    frac_rank = (end - begin) / d
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-    phase_ms = np.zeros(5)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
 
-    def step(U, record=False):
+    def step(U, evs=None):
         flush.zero_()
-        if record:
-            ev[0].record(stream)
-        for k, (kind, m) in enumerate((("local", 0), ("local", 1), ("exhaustion", 0), ("exhaustion", 1))):
+        if evs:
+            evs[0].record(stream)
+        outs = []
+        for k, (_, kind, m) in enumerate(PHASES):
             sweep = prob.device_local_update if kind == "local" else prob.device_exhaustion
-            U = U.replace(m, P.SampledController(prob.grids[m], sweep(m, U, cfg, sh), _trusted_device=True))
-            if record:
-                ev[k + 1].record(stream)
+            outs.append(sweep(m, U, cfg, sh))
+            if evs:
+                evs[k + 1].record(stream)
         J = prob.device_objective(U, sh)
-        if record:
-            ev[5].record(stream)
-            torch.cuda.synchronize()
-            for k in range(5):
-                phase_ms[k] += ev[k].elapsed_time(ev[k + 1])
-        return U, J
+        if evs:
+            evs[5].record(stream)
+        return outs, J
 
-    # FP64 pipe peak on this GPU (DMUL/DADD, no FMA) -- the roofline denominator
+    # FP64 pipe peak of this GPU (DMUL/DADD, no FMA) -- the roofline denominator
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     sink = torch.empty(sms * 8 * 256, dtype=torch.float64, device=dev)
     iters = 4096
-    for _ in range(2):
-        _lib.call("ucp_fp64_probe", sms * 8, 256, iters, ptr(sink), stream.cuda_stream)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    _lib.call("ucp_fp64_probe", sms * 8, 256, iters, ptr(sink), stream.cuda_stream)
+    for rep in range(3):
+        if rep == 2:
+            e0.record(stream)
+        _lib.call("ucp_fp64_probe", sms * 8, 256, iters, ptr(sink), stream.cuda_stream)
     e1.record(stream)
     torch.cuda.synchronize()
     fp64_peak = sms * 8 * 256 * iters * 16 / (e0.elapsed_time(e1) * 1e-3)
@@ -322,81 +347,83 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     n_launch0 = _lib.launch_count()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(args.steps):
-        step(U0)
-    t1.record(stream)
+    for k in range(args.steps):
+        step(U0, ev[k])
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = _lib.launch_count() - n_launch0
-    ms = t0.elapsed_time(t1)
     clk = clocks.stop()
-    # per-phase split (separate, event-instrumented pass; not part of `value`)
-    for _ in range(args.steps):
-        step(U0, record=True)
-    phase_ms /= args.steps
+    ms = ev[0][0].elapsed_time(ev[-1][5])
+    phase_ms = np.array([[e[q].elapsed_time(e[q + 1]) for q in range(5)] for e in ev]).mean(axis=0)
     tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_step = float(tmax.item()) / args.steps
 
-    # end to end: host controllers in, host controllers + J out, every step
+    # end to end through the public API: host controllers in, every phase's
+    # new host controller + J out, each step
     e2e = None
     if not args.no_e2e:
-        hu0 = torch.from_numpy(u0h).pin_memory()
-        hu1 = torch.from_numpy(u1h).pin_memory()
-        o0 = torch.empty_like(hu0).pin_memory()
-        o1 = torch.empty_like(hu1).pin_memory()
+        hu = [torch.from_numpy(u0h).pin_memory(), torch.from_numpy(u1h).pin_memory()]
+        ho = [torch.empty(d, dtype=torch.float64).pin_memory() for _ in PHASES]
 
         def e2e_step():
             flush.zero_()
-            d0, d1 = hu0.to(dev, non_blocking=True), hu1.to(dev, non_blocking=True)
-            U = P.ControllerSet((P.SampledController(prob.grids[0], d0, _trusted_device=True),
-                                 P.SampledController(prob.grids[1], d1, _trusted_device=True)))
-            V, J = step(U)
-            o0.copy_(V[0]._dev, non_blocking=True)
-            o1.copy_(V[1]._dev, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            U = P.ControllerSet(tuple(P.SampledController(prob.grids[m], hu[m].to(dev, non_blocking=True))
+                                      for m in (0, 1)))
+            outs, J = step(U)
+            for o, hbuf in zip(outs, ho):
+                hbuf.copy_(o, non_blocking=True)
+            stream.synchronize()
             return J
 
         e2e_step()
+        e2e_steps = max(1, min(args.steps, 2))
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(e2e_steps):
             e2e_step()
         t1.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_ms = float(te.item()) / args.steps
+        e2e_ms = float(te.item()) / e2e_steps
         e2e = {"value": counts["evals"] / (e2e_ms * 1e-3), "unit": "evals/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": 2 * d * 8, "d2h_bytes_per_step": 2 * d * 8 + 16,
-               "path": "public API (SampledController from pinned host arrays -> solver sweeps -> host)"}
+               "steps": e2e_steps, "h2d_bytes_per_step": 2 * d * 8,
+               "d2h_bytes_per_step": len(PHASES) * d * 8 + 16,
+               "path": "public API: SampledController from pinned host arrays -> 4 device sweeps + objective "
+                       "-> new controllers copied back to pinned host buffers, J to host"}
 
-    # roofline of the dominant kernel pair: the stage-0 local-update sweep
-    lu0_ms = phase_ms[0]
-    achieved = counts_local_ops / (lu0_ms * 1e-3)
+    # roofline: every kernel family, and the dominant one
+    kernels = {
+        "exh0": ("k_ex0_eval (stage-0 exhaustion candidates)", counts["ex0_dp_ops"], phase_ms[2]),
+        "local0": ("k_lu0_probe + k_lu0_finish (stage-0 local update)", counts["lu0_dp_ops"], phase_ms[0]),
+        "local1": ("k_moments (u1 estimator) + k_lu1", counts["moment_dp_ops"], phase_ms[1]),
+    }
+    fam = {k: {"kernel": v[0], "achieved_tflops": v[1] * frac_rank / (v[2] * 1e-3) / 1e12,
+               "frac": v[1] * frac_rank / (v[2] * 1e-3) / fp64_peak, "ms": v[2]} for k, v in kernels.items()}
+    top = max(kernels, key=lambda k: kernels[k][2])
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("lu0_dram_bytes_per_launch")
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch", {}).get(top)
         except Exception:
             traffic = None
-    roofline = {"bound": "fp64", "kernel": "k_lu0_probe + k_lu0_finish (stage-0 local-update sweep)",
-                "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "traffic": traffic,
-                "peak_source": f"measured on this GPU: ucp_fp64_probe DMUL+DADD throughput ({sms} SMs); "
-                               "nominal 148 SMs x 64 DP lanes x 1.965 GHz = 18.6 TFLOP/s (non-FMA)",
-                "work": f"{DP_OPS_PER_NODE} DP ops per visited node x {counts['lu0_nodes']:.4g} nodes "
-                        "(4 walks per point; exp/erf/setup excluded)"}
+    roofline = {"bound": "fp64", "kernel": kernels[top][0], "achieved": fam[top]["achieved_tflops"],
+                "peak": fp64_peak / 1e12, "unit": "TFLOP/s", "frac": fam[top]["frac"], "traffic": traffic,
+                "peak_source": f"measured on this GPU at bench start: ucp_fp64_probe DMUL+DADD throughput "
+                               f"({sms} SMs); nominal 148 x 64 DP lanes x 1.965 GHz = 18.6 TFLOP/s (non-FMA)",
+                "work": f"{DP_OPS_PER_NODE} DP ops per visited walk node ({counts['ex0_nodes']:.4g} nodes in "
+                        f"exh0, {counts['lu0_nodes']:.4g} in local0), {DP_OPS_PER_PAIR} per in-range moment pair "
+                        f"({counts['moment_pairs']:.4g}); exp/erf/setup outside the loops excluded",
+                "families": fam}
 
-    line = None
     if rank == 0:
         value = counts["evals"] / (ms_step * 1e-3)
         cpu = None
@@ -407,7 +434,7 @@ def run_ours(args):
             p = orc.OracleWitsenhausen(k=K_WC, sigma=SIGMA, grid0=(*SPAN, d), grid1=(*SPAN, d),
                                        f0=prob._f0, fw0=prob._fw0)
             sec, times, thr, sample = cpu_step_seconds(orc, p, u0h, u1h, d, cfg.radius_for(prob.grids[0]),
-                                                       args.cpu_seconds)
+                                                       args.cpu_seconds, counts["cand0"] / d)
             cpu = {"value": counts["evals"] / sec, "unit": "evals/s", "cores": thr, "kind": "port",
                    "sample": sample, "step_s_extrapolated": sec, "phase_s": times,
                    "host": orc.host_cpu_description()}

@@ -253,15 +253,18 @@ __global__ void k_obj_terms(const double* __restrict__ y0, const double* __restr
 }
 
 // kernels.py:136-144: serial ascending trapezoid.  One warp stages chunks
-// through shared memory; lane 0 performs the additions in index order.
+// through shared memory; lane 0 performs the additions in index order
+// (interior chunk body unrolled so the shared loads run ahead of the
+// dependent adds).
 __global__ void k_trapezoid(const double* __restrict__ x, int64_t n, double spacing, double* out,
                             int64_t* err) {
-  __shared__ double buf[1024];
+  constexpr int kChunk = 2048;
+  __shared__ double buf[kChunk];
   const int lane = threadIdx.x;
   double acc = 0.0;
   int64_t bad = UCP_NO_ERROR;
-  for (int64_t base = 0; base < n; base += 1024) {
-    int64_t cnt = n - base < 1024 ? n - base : 1024;
+  for (int64_t base = 0; base < n; base += kChunk) {
+    const int cnt = (int)(n - base < kChunk ? n - base : kChunk);
     for (int r = lane; r < cnt; r += 32) {
       double xv = x[base + r];
       buf[r] = xv;
@@ -269,13 +272,20 @@ __global__ void k_trapezoid(const double* __restrict__ x, int64_t n, double spac
     }
     __syncwarp();
     if (lane == 0) {
-      for (int r = 0; r < cnt; ++r) {
-        int64_t i = base + r;
-        double xv = buf[r];
-        if (i == 0) acc = 0.5 * xv;
-        else if (i < n - 1) acc += xv;
-        else acc += 0.5 * xv;
+      int r = 0;
+      if (base == 0) {
+        acc = 0.5 * buf[0];
+        r = 1;
       }
+      const int stop = base + cnt == n ? cnt - 1 : cnt;  // index n-1 gets the half weight
+      for (; r + 8 <= stop; r += 8) {
+        double v0 = buf[r], v1 = buf[r + 1], v2 = buf[r + 2], v3 = buf[r + 3];
+        double v4 = buf[r + 4], v5 = buf[r + 5], v6 = buf[r + 6], v7 = buf[r + 7];
+        acc += v0; acc += v1; acc += v2; acc += v3;
+        acc += v4; acc += v5; acc += v6; acc += v7;
+      }
+      for (; r < stop; ++r) acc += buf[r];
+      if (base + cnt == n && n > 1) acc += 0.5 * buf[cnt - 1];
     }
     __syncwarp();
   }
@@ -412,8 +422,15 @@ __global__ void k_x1_minmax(const double* __restrict__ y0, const double* __restr
 // One thread per query y; the CTA streams (x_i, w_i) tiles through shared
 // memory in ascending i (the reference's summation order) and skips whole
 // tiles whose support lies outside +-GAUSS_CUT of every query in the CTA
-// (exactly zero contribution: monotone rounding of y - x).  Repeated x_i
-// (staircase u0) reuse the previous pair weight bit for bit.
+// (exactly zero contribution: fl(y - x) is monotone in both arguments).
+//
+// Interior queries (factor 1, no tail terms -- every CTA except the one
+// holding the first/last grid node) take the fast path: four pairs per
+// iteration with their exp() evaluated independently (ILP), then
+// accumulated strictly in order.  For them `wp != 0` <=> |y - x| <= 12
+// (exp(-72) * INV > 0), so the reference's branch reduces to the range test,
+// and factor*e == e bitwise.  CTAs with an edge query run the general loop,
+// a line-by-line restatement of kernels.py:466-482.
 constexpr int kMomThreads = 128;
 __global__ void __launch_bounds__(kMomThreads)
 k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x,
@@ -453,46 +470,62 @@ k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x
     ymin = fmin(ymin, s_ymin[r]);
     ymax = fmax(ymax, s_ymax[r]);
   }
-  const bool no_skip = s_edge != 0;
+  const bool general = s_edge != 0;
   const double INV = inv_sqrt_2pi();
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-  double px = __longlong_as_double(0x7ff8dead00000000ll);  // NaN: never equal
-  double pwp = 0.0;
   const int64_t ntiles = (m + kTile - 1) / kTile;
   for (int64_t tile = 0; tile < ntiles; ++tile) {
-    if (!no_skip) {
+    if (!general) {
       double2 mm = tile_mm[tile];
       if (ymin - mm.y > kGaussCut || ymax - mm.x < -kGaussCut) continue;  // CTA-uniform
     }
     const int64_t base = tile * kTile;
     const int cnt = (int)(m - base < kTile ? m - base : kTile);
     __syncthreads();
-    for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
-      sx[r] = x[base + r];
-      sw[r] = w[base + r];
+    for (int r = threadIdx.x; r < kTile; r += blockDim.x) {
+      // padding slots are +inf: out of range for every query, never accumulated
+      sx[r] = r < cnt ? x[base + r] : INFINITY;
+      sw[r] = r < cnt ? w[base + r] : 0.0;
     }
     __syncthreads();
-    for (int r = 0; r < cnt; ++r) {
-      const double xi = sx[r];
-      double wp;
-      if (xi == px) {
-        wp = pwp;
-      } else {
+    if (!general) {
+      for (int r = 0; r < cnt; r += 4) {
+        double e[4];
+        bool in[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double diff = yt - sx[r + q];
+          in[q] = fabs(diff) <= kGaussCut;
+          e[q] = ucp_exp_tab(in[q] ? (-0.5 * diff) * diff : 0.0, stab);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (in[q]) {
+            const double xi = sx[r + q];
+            const double wp = (e[q] * INV) * sw[r + q];
+            acc0 += wp;
+            const double wx = wp * xi;
+            acc1 += wx;
+            acc2 += wx * xi;
+          }
+        }
+      }
+    } else {
+      for (int r = 0; r < cnt; ++r) {
+        const double xi = sx[r];
         const double diff = yt - xi;
-        wp = 0.0;
+        double wp = 0.0;
         if (diff <= kGaussCut && diff >= -kGaussCut)
           wp = (factor * ucp_exp_tab((-0.5 * diff) * diff, stab)) * INV;
         if (at_left) wp += ucp_phi_cdf_tab(a - xi, stab) / h;
         if (at_right) wp += ucp_phi_cdf_tab(xi - b, stab) / h;
-        px = xi;
-        pwp = wp;
-      }
-      if (wp != 0.0) {
-        wp *= sw[r];
-        acc0 += wp;
-        const double wx = wp * xi;
-        acc1 += wx;
-        acc2 += wx * xi;
+        if (wp != 0.0) {
+          wp *= sw[r];
+          acc0 += wp;
+          const double wx = wp * xi;
+          acc1 += wx;
+          acc2 += wx * xi;
+        }
       }
     }
   }
