@@ -396,15 +396,25 @@ __global__ void k_ex_argmin(const double* __restrict__ u, const double* __restri
 // ---- stage 1: the u1 estimator moments (kernels.py:447-486) ----------------
 constexpr int kTile = 256;  // support points per shared-memory tile
 
-__global__ void k_x1_minmax(const double* __restrict__ y0, const double* __restrict__ u0, int64_t d0,
-                            double* x1, double2* tile_mm) {
+// Per support point: x1 = y0 + u0 (witsenhausen.py:72), the two edge-tail
+// weights the first/last query need (kernels.py:477-480, hoisted out of the
+// serial loop: same operands, same bits), and per-tile min/max of x1 for
+// tile skipping (a tile holding a NaN is never skipped: NaN contributes to
+// the tail-weighted edge queries).
+__global__ void k_x1_prepare(const double* __restrict__ y0, const double* __restrict__ u0, int64_t d0,
+                             double a, double h, double b, double* x1, double2* tails, double2* tile_mm) {
   __shared__ double smin[kTile], smax[kTile];
+  __shared__ int snan;
+  if (threadIdx.x == 0) snan = 0;
+  __syncthreads();
   int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
   double x = 0.0, mn = INFINITY, mx = -INFINITY;
   if (i < d0) {
-    x = y0 ? y0[i] + u0[i] : u0[i];  // witsenhausen.py:72 x1 = points + u0
+    x = y0 ? y0[i] + u0[i] : u0[i];
     x1[i] = x;
-    if (!isnan(x)) mn = mx = x;
+    tails[i] = make_double2(phi_cdf(a - x) / h, phi_cdf(x - b) / h);
+    if (isnan(x)) snan = 1;
+    else mn = mx = x;
   }
   smin[threadIdx.x] = mn;
   smax[threadIdx.x] = mx;
@@ -416,93 +426,132 @@ __global__ void k_x1_minmax(const double* __restrict__ y0, const double* __restr
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) tile_mm[blockIdx.x] = make_double2(smin[0], smax[0]);
+  if (threadIdx.x == 0)
+    tile_mm[blockIdx.x] = snan ? make_double2(-INFINITY, INFINITY) : make_double2(smin[0], smax[0]);
 }
 
 // One thread per query y; the CTA streams (x_i, w_i) tiles through shared
 // memory in ascending i (the reference's summation order) and skips whole
-// tiles whose support lies outside +-GAUSS_CUT of every query in the CTA
-// (exactly zero contribution: fl(y - x) is monotone in both arguments).
+// tiles that contribute exactly nothing to any query of the CTA:
+//  - Gaussian term: every |y - x| > GAUSS_CUT (fl(y - x) is monotone in both
+//    arguments, so the tile min/max decide it);
+//  - edge tails (only CTAs holding the first/last grid node): phi_cdf(a - x)
+//    and phi_cdf(x - b) are exactly 0 once a - x <= -12 / x - b <= -12.
 //
-// Interior queries (factor 1, no tail terms -- every CTA except the one
-// holding the first/last grid node) take the fast path: four pairs per
-// iteration with their exp() evaluated independently (ILP), then
-// accumulated strictly in order.  For them `wp != 0` <=> |y - x| <= 12
-// (exp(-72) * INV > 0), so the reference's branch reduces to the range test,
-// and factor*e == e bitwise.  CTAs with an edge query run the general loop,
-// a line-by-line restatement of kernels.py:466-482.
+// Interior CTAs take the fast path: four pairs per iteration, their exp()
+// evaluated back to back (independent, ILP) with the branch-free main-path
+// exp (bitwise glibc for |arg| < 512; out-of-range pairs compute garbage that
+// is never accumulated), then accumulated strictly in order.  For interior
+// queries `wp != 0` <=> |y - x| <= 12 (exp(-72) * INV > 0) and factor*e == e
+// bitwise.  CTAs with an edge query run the general loop, a line-by-line
+// restatement of kernels.py:466-482 with the tail weights precomputed.
+//
+// Persistent CTAs pull 128-query blocks from an atomic counter, the two edge
+// blocks first (they visit the most tiles).
 constexpr int kMomThreads = 128;
-__global__ void __launch_bounds__(kMomThreads)
+constexpr int kMomUnroll = 4;
+__global__ void __launch_bounds__(kMomThreads, 6)
 k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x,
-          const double* __restrict__ w, int64_t m, const double2* __restrict__ tile_mm, double a,
-          double h, int64_t d, double* o0, double* o1, double* o2) {
-  __shared__ double sx[kTile], sw[kTile];
-  __shared__ uint64_t stab[256];
+          const double* __restrict__ w, const double2* __restrict__ tails, int64_t m,
+          const double2* __restrict__ tile_mm, double a, double h, int64_t d, double* o0, double* o1,
+          double* o2, int* work_counter) {
+  __shared__ double2 sxw[kTile];
+  __shared__ double2 slr[kTile];
+  __shared__ __align__(16) uint64_t stab[256];
   __shared__ double s_ymin[kMomThreads / 32], s_ymax[kMomThreads / 32];
-  __shared__ int s_edge;
+  __shared__ int s_left, s_right;
+  __shared__ long long s_work;
   for (int r = threadIdx.x; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
-  if (threadIdx.x == 0) s_edge = 0;
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = t < n;
-  const double yt = active ? yq[t] : yq[n - 1];
+  const ucp_exp_entry* stab2 = reinterpret_cast<const ucp_exp_entry*>(stab);
+  const int64_t nqb = (n + kMomThreads - 1) / kMomThreads;
   const double b = a + h * (double)(d - 1);
-  long long j = (long long)ceil((yt - a) / h - 0.5);
-  if (j < 0) j = 0;
-  if (j > d - 1) j = d - 1;
-  const bool at_left = j == 0, at_right = j == d - 1;
-  const double factor = (at_left || at_right) ? 0.5 : 1.0;
-  // CTA query range (for tile skipping) and whether any query owns a tail
-  double ymin = yt, ymax = yt;
-  for (int off = 16; off > 0; off >>= 1) {
-    ymin = fmin(ymin, __shfl_xor_sync(0xffffffffu, ymin, off));
-    ymax = fmax(ymax, __shfl_xor_sync(0xffffffffu, ymax, off));
-  }
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) {
-    s_ymin[threadIdx.x >> 5] = ymin;
-    s_ymax[threadIdx.x >> 5] = ymax;
-  }
-  if (at_left || at_right || isnan(yt)) atomicOr(&s_edge, 1);
-  __syncthreads();
-  ymin = s_ymin[0];
-  ymax = s_ymax[0];
-  for (int r = 1; r < (int)(blockDim.x >> 5); ++r) {
-    ymin = fmin(ymin, s_ymin[r]);
-    ymax = fmax(ymax, s_ymax[r]);
-  }
-  const bool general = s_edge != 0;
   const double INV = inv_sqrt_2pi();
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
   const int64_t ntiles = (m + kTile - 1) / kTile;
-  for (int64_t tile = 0; tile < ntiles; ++tile) {
-    if (!general) {
-      double2 mm = tile_mm[tile];
-      if (ymin - mm.y > kGaussCut || ymax - mm.x < -kGaussCut) continue;  // CTA-uniform
+  if (threadIdx.x == 0) s_work = blockIdx.x;
+  __syncthreads();
+  for (;;) {
+    const int64_t k = s_work;
+    if (k >= nqb) break;
+    const int64_t qb = k == 0 ? 0 : (k == 1 ? nqb - 1 : k - 1);  // edge blocks first
+    if (threadIdx.x == 0) s_left = s_right = 0;
+    const int64_t t = qb * kMomThreads + threadIdx.x;
+    const bool active = t < n;
+    const double yt = active ? yq[t] : yq[n - 1];
+    long long j = (long long)ceil((yt - a) / h - 0.5);
+    if (j < 0) j = 0;
+    if (j > d - 1) j = d - 1;
+    const bool at_left = j == 0, at_right = j == d - 1;
+    const double factor = (at_left || at_right) ? 0.5 : 1.0;
+    double ymin = yt, ymax = yt;
+    for (int off = 16; off > 0; off >>= 1) {
+      ymin = fmin(ymin, __shfl_xor_sync(0xffffffffu, ymin, off));
+      ymax = fmax(ymax, __shfl_xor_sync(0xffffffffu, ymax, off));
     }
-    const int64_t base = tile * kTile;
-    const int cnt = (int)(m - base < kTile ? m - base : kTile);
     __syncthreads();
-    for (int r = threadIdx.x; r < kTile; r += blockDim.x) {
-      // padding slots are +inf: out of range for every query, never accumulated
-      sx[r] = r < cnt ? x[base + r] : INFINITY;
-      sw[r] = r < cnt ? w[base + r] : 0.0;
+    if ((threadIdx.x & 31) == 0) {
+      s_ymin[threadIdx.x >> 5] = ymin;
+      s_ymax[threadIdx.x >> 5] = ymax;
     }
+    if (at_left) atomicOr(&s_left, 1);
+    if (at_right) atomicOr(&s_right, 1);
     __syncthreads();
-    if (!general) {
-      for (int r = 0; r < cnt; r += 4) {
-        double e[4];
-        bool in[4];
+    ymin = s_ymin[0];
+    ymax = s_ymax[0];
+    for (int r = 1; r < kMomThreads / 32; ++r) {
+      ymin = fmin(ymin, s_ymin[r]);
+      ymax = fmax(ymax, s_ymax[r]);
+    }
+    const bool has_left = s_left != 0, has_right = s_right != 0;
+    const bool general = has_left || has_right;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    for (int64_t tile = 0; tile < ntiles; ++tile) {
+      const double2 mm = tile_mm[tile];
+      const bool gauss_out = ymin - mm.y > kGaussCut || ymax - mm.x < -kGaussCut;
+      const bool left_out = !has_left || a - mm.x <= -kGaussCut;
+      const bool right_out = !has_right || mm.y - b <= -kGaussCut;
+      if (gauss_out && left_out && right_out) continue;  // CTA-uniform
+      const int64_t base = tile * kTile;
+      const int cnt = (int)(m - base < kTile ? m - base : kTile);
+      __syncthreads();
+      for (int r = threadIdx.x; r < kTile; r += kMomThreads) {
+        // padding slots are +inf: out of range for every query, never accumulated
+        sxw[r] = r < cnt ? make_double2(x[base + r], w[base + r]) : make_double2(INFINITY, 0.0);
+        if (general) slr[r] = r < cnt ? tails[base + r] : make_double2(0.0, 0.0);
+      }
+      __syncthreads();
+      if (!general) {
+        for (int r = 0; r < cnt; r += kMomUnroll) {
+          double e[kMomUnroll];
+          bool in[kMomUnroll];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double diff = yt - sx[r + q];
-          in[q] = fabs(diff) <= kGaussCut;
-          e[q] = ucp_exp_tab(in[q] ? (-0.5 * diff) * diff : 0.0, stab);
+          for (int q = 0; q < kMomUnroll; ++q) {
+            const double diff = yt - sxw[r + q].x;
+            in[q] = fabs(diff) <= kGaussCut;
+            e[q] = ucp_exp_core((-0.5 * diff) * diff, stab2);
+          }
+#pragma unroll
+          for (int q = 0; q < kMomUnroll; ++q) {
+            if (in[q]) {
+              const double2 xw = sxw[r + q];
+              const double wp = (e[q] * INV) * xw.y;
+              acc0 += wp;
+              const double wx = wp * xw.x;
+              acc1 += wx;
+              acc2 += wx * xw.x;
+            }
+          }
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (in[q]) {
-            const double xi = sx[r + q];
-            const double wp = (e[q] * INV) * sw[r + q];
+      } else {
+        for (int r = 0; r < cnt; ++r) {
+          const double xi = sxw[r].x;
+          const double diff = yt - xi;
+          double wp = 0.0;
+          if (diff <= kGaussCut && diff >= -kGaussCut)
+            wp = (factor * ucp_exp_core((-0.5 * diff) * diff, stab2)) * INV;
+          if (at_left) wp += slr[r].x;   // phi_cdf(a - xi) / h
+          if (at_right) wp += slr[r].y;  // phi_cdf(xi - b) / h
+          if (wp != 0.0) {
+            wp *= sxw[r].y;
             acc0 += wp;
             const double wx = wp * xi;
             acc1 += wx;
@@ -510,29 +559,15 @@ k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x
           }
         }
       }
-    } else {
-      for (int r = 0; r < cnt; ++r) {
-        const double xi = sx[r];
-        const double diff = yt - xi;
-        double wp = 0.0;
-        if (diff <= kGaussCut && diff >= -kGaussCut)
-          wp = (factor * ucp_exp_tab((-0.5 * diff) * diff, stab)) * INV;
-        if (at_left) wp += ucp_phi_cdf_tab(a - xi, stab) / h;
-        if (at_right) wp += ucp_phi_cdf_tab(xi - b, stab) / h;
-        if (wp != 0.0) {
-          wp *= sw[r];
-          acc0 += wp;
-          const double wx = wp * xi;
-          acc1 += wx;
-          acc2 += wx * xi;
-        }
-      }
     }
-  }
-  if (active) {
-    o0[t] = acc0;
-    o1[t] = acc1;
-    o2[t] = acc2;
+    if (active) {
+      o0[t] = acc0;
+      o1[t] = acc1;
+      o2[t] = acc2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_work = gridDim.x + atomicAdd(work_counter, 1);
+    __syncthreads();
   }
 }
 
@@ -628,15 +663,15 @@ __global__ void k_fp64_probe(int iters, double* sink) {
 
 // ============================================================ workspace
 struct ucp_workspace {
-  void* buf[8] = {nullptr};
-  size_t cap[8] = {0};
+  void* buf[16] = {nullptr};
+  size_t cap[16] = {0};
   void* scan_tmp = nullptr;
   size_t scan_cap = 0;
   int64_t* h_total = nullptr;  // pinned
 };
 
 namespace {
-enum { WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL };
+enum { WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS, WS_NSLOTS };
 
 int ws_get(ucp_workspace* ws, int slot, size_t bytes, void** out) {
   if (ws->cap[slot] < bytes) {
@@ -656,15 +691,28 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
                 int64_t m, double a, double h, int64_t d, double* o0, double* o1, double* o2,
                 ucp_workspace* ws, cudaStream_t st) {
   if (nq <= 0) return UCP_OK;
-  void *px1, *ptile;
+  void *px1, *ptile, *pctr, *ptails;
   int rc;
   if ((rc = ws_get(ws, WS_X1, sizeof(double) * (size_t)m, &px1))) return rc;
+  if ((rc = ws_get(ws, WS_TAILS, sizeof(double2) * (size_t)m, &ptails))) return rc;
   int64_t ntiles = (m + kTile - 1) / kTile;
   if ((rc = ws_get(ws, WS_TILE, sizeof(double2) * (size_t)ntiles, &ptile))) return rc;
-  k_x1_minmax<<<(unsigned)ntiles, kTile, 0, st>>>(y0, u0, m, (double*)px1, (double2*)ptile);
-  UCP_LAUNCHED("k_x1_minmax");
-  k_moments<<<nblocks(nq, kMomThreads), kMomThreads, 0, st>>>(yq, nq, (const double*)px1, w, m,
-                                                              (const double2*)ptile, a, h, d, o0, o1, o2);
+  if ((rc = ws_get(ws, WS_TOTAL, sizeof(int64_t) * 2, &pctr))) return rc;
+  const double b = a + h * (double)(d - 1);
+  k_x1_prepare<<<(unsigned)ntiles, kTile, 0, st>>>(y0, u0, m, a, h, b, (double*)px1, (double2*)ptails,
+                                                   (double2*)ptile);
+  UCP_LAUNCHED("k_x1_prepare");
+  int* counter = (int*)((int64_t*)pctr + 1);
+  UCP_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), st));
+  int dev = 0, sms = 0, per_sm = 0;
+  UCP_CHECK(cudaGetDevice(&dev));
+  UCP_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  UCP_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_moments, kMomThreads, 0));
+  int64_t nqb = (nq + kMomThreads - 1) / kMomThreads;
+  int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > nqb) grid = nqb;
+  k_moments<<<(unsigned)grid, kMomThreads, 0, st>>>(yq, nq, (const double*)px1, w, (const double2*)ptails, m,
+                                                      (const double2*)ptile, a, h, d, o0, o1, o2, counter);
   UCP_LAUNCHED("k_moments");
   return UCP_OK;
 }
@@ -704,7 +752,7 @@ int ucp_workspace_create(ucp_workspace** ws) {
 
 int ucp_workspace_destroy(ucp_workspace* ws) {
   if (!ws) return UCP_OK;
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 16; ++i)
     if (ws->buf[i]) cudaFree(ws->buf[i]);
   if (ws->scan_tmp) cudaFree(ws->scan_tmp);
   if (ws->h_total) cudaFreeHost(ws->h_total);
@@ -718,6 +766,8 @@ int ucp_workspace_reserve(ucp_workspace* ws, int64_t d0, int64_t d1, int64_t max
   int rc;
   int64_t dm = d0 > d1 ? d0 : d1;
   if ((rc = ws_get(ws, WS_X1, sizeof(double) * (size_t)dm, &p))) return rc;
+  if ((rc = ws_get(ws, WS_TAILS, sizeof(double2) * (size_t)dm, &p))) return rc;
+  if ((rc = ws_get(ws, WS_TOTAL, sizeof(int64_t) * 2, &p))) return rc;
   if ((rc = ws_get(ws, WS_TILE, sizeof(double2) * (size_t)((dm + kTile - 1) / kTile), &p))) return rc;
   if ((rc = ws_get(ws, WS_MOM, sizeof(double) * 3 * (size_t)dm, &p))) return rc;
   if ((rc = ws_get(ws, WS_COST, sizeof(double) * (size_t)(max_cand > 3 * dm ? max_cand : 3 * dm), &p))) return rc;

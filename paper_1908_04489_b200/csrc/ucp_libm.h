@@ -117,6 +117,34 @@ UCP_HD double ucp_exp_tab(double x, const uint64_t* tab) {
   return UCP_FMA(scale, tmp, scale);
 }
 
+/* Main path of ucp_exp_tab only, for |x| < 512 (every exp argument of the
+ * Witsenhausen kernels lies in [-72.1, 0]).  Bitwise identical to
+ * ucp_exp_tab there: for |x| < 2^-54 the main path yields fma(1, x, 1) ==
+ * 1.0 + x, the value of glibc's tiny-argument branch (kd = 0, r = x, tmp = x).
+ * `tab2[i]` = {tail bits, scale bits} of entry i, so one 128-bit load fetches
+ * both (LDS.128 from shared memory). */
+typedef struct { uint64_t tail, sbits; } ucp_exp_entry;
+
+UCP_HD double ucp_exp_core(double x, const ucp_exp_entry* tab2) {
+  double kd = UCP_FMA(x, ucp_asf64(UCP_EXP_INVLN2N), ucp_asf64(UCP_EXP_SHIFT));
+  uint64_t ki = ucp_asu64(kd);
+  kd = kd - ucp_asf64(UCP_EXP_SHIFT);
+  double r = UCP_FMA(kd, ucp_asf64(UCP_EXP_NEGLN2HIN), x);
+  r = UCP_FMA(kd, ucp_asf64(UCP_EXP_NEGLN2LON), r);
+  ucp_exp_entry e = tab2[ki & 127u];
+  double tail = ucp_asf64(e.tail);
+  uint64_t sbits = e.sbits + (ki << 45);
+  double p23 = UCP_FMA(r, ucp_asf64(UCP_EXP_C3), ucp_asf64(UCP_EXP_C2));
+  double tr = r + tail;
+  double r2 = r * r;
+  double p45 = UCP_FMA(r, ucp_asf64(UCP_EXP_C5), ucp_asf64(UCP_EXP_C4));
+  double t1 = UCP_FMA(p23, r2, tr);
+  double r4 = r2 * r2;
+  double tmp = UCP_FMA(r4, p45, t1);
+  double scale = ucp_asf64(sbits);
+  return UCP_FMA(scale, tmp, scale);
+}
+
 /* fdlibm erf coefficients (bit patterns of glibc's s_erf.c constants). */
 #define UCP_D(u) ucp_asf64(u##ull)
 

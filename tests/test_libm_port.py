@@ -19,6 +19,9 @@ def port():
     L.compare_uniform.restype = ctypes.c_int64
     L.compare_uniform.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double,
                                   ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
+    L.compare_core.restype = ctypes.c_int64
+    L.compare_core.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
+                               ctypes.POINTER(ctypes.c_double)]
     L.compare_bits.restype = ctypes.c_int64
     L.compare_bits.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_uint64,
                                ctypes.POINTER(ctypes.c_double)]
@@ -48,4 +51,12 @@ def test_uniform_ranges_bitwise(port, which, lo, hi):
 def test_random_bit_patterns(port, which):
     first = ctypes.c_double(0.0)
     bad = port.compare_bits(which, 2_000_000, 99, ctypes.byref(first))
+    assert bad == 0, f"{bad} mismatches, first at {first.value!r}"
+
+
+@pytest.mark.parametrize("lo,hi", [(-72.5, 0.0), (-511.9, 511.9), (-1e-3, 1e-3)])
+def test_exp_core_main_path_equivalence(port, lo, hi):
+    """The kernels' branch-free exp (main path only) == glibc exp for |x| < 512."""
+    first = ctypes.c_double(0.0)
+    bad = port.compare_core(3_000_000, 5, lo, hi, ctypes.byref(first))
     assert bad == 0, f"{bad} mismatches, first at {first.value!r}"
