@@ -26,6 +26,11 @@
 namespace {
 
 constexpr double kGaussCut = 12.0;  // kernels.py:55 GAUSS_CUT
+// Walk kernels (one serial Gaussian walk per thread): 128-thread CTAs, at
+// least 12 resident per SM (<= 42 registers) so 12 warps per scheduler hide
+// the L1 latency of the v1 stream behind the FP64 pipe.
+constexpr int kWalkThreads = 128;
+constexpr int kWalkMinBlocks = 12;
 
 __device__ const uint64_t g_exp_tab[256] = UCP_EXP_TAB_INIT;
 const uint64_t h_exp_tab[256] = UCP_EXP_TAB_INIT;
@@ -104,16 +109,20 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
     const int last = (int)(g.d - 1);
     const int je = (int)jhi;
     int j = (int)jlo;
-#define UCP_WALK_STEP(W)            \
+#define UCP_WALK_STEP_V(W, VJ)      \
   {                                 \
     double wp = (W) * pdf;          \
-    double vj = __ldg(v + j);       \
     acc0 += wp;                     \
-    double wv = wp * vj;            \
+    double wv = wp * (VJ);          \
     acc1 += wv;                     \
-    acc2 += wv * vj;                \
+    acc2 += wv * (VJ);              \
     pdf *= ratio;                   \
     ratio *= q;                     \
+  }
+#define UCP_WALK_STEP(W)            \
+  {                                 \
+    const double vj_ = __ldg(v + j); \
+    UCP_WALK_STEP_V(W, vj_);        \
   }
     const double hh = 0.5 * h;
     if (j == 0) {
@@ -121,10 +130,24 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
       ++j;
     }
     const int jint = je < last ? je : last - 1;
-#pragma unroll 4
+    // interior nodes, two per 16-byte load (v1 is 16-byte aligned: checked
+    // by the host); an odd first node is peeled so the order is unchanged
+    if ((j & 1) && j <= jint) {
+      UCP_WALK_STEP(h);
+      ++j;
+    }
+    for (; j + 3 <= jint; j += 4) {
+      const double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
+      const double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
+      UCP_WALK_STEP_V(h, p0.x);
+      UCP_WALK_STEP_V(h, p0.y);
+      UCP_WALK_STEP_V(h, p1.x);
+      UCP_WALK_STEP_V(h, p1.y);
+    }
     for (; j <= jint; ++j) UCP_WALK_STEP(h);
     if (je == last && j == last) UCP_WALK_STEP(hh);
 #undef UCP_WALK_STEP
+#undef UCP_WALK_STEP_V
   }
   double lo = phi_cdf(g.a - st);
   double hi = phi_cdf(st - g.b);
@@ -158,7 +181,7 @@ __device__ __forceinline__ void flag_min(int64_t* slot, int64_t i) {
 
 // ---------------------------------------------------------------- kernels
 
-__global__ void k_gauss_grid(const double* __restrict__ s, int64_t n, const double* __restrict__ v,
+__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_gauss_grid(const double* __restrict__ s, int64_t n, const double* __restrict__ v,
                              WalkGrid g, double* t0, double* t1, double* t2) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
@@ -170,7 +193,7 @@ __global__ void k_gauss_grid(const double* __restrict__ s, int64_t n, const doub
 
 // marginal_cost_segmented m=0 over a flat candidate list; the segment of
 // candidate c is found by binary search in `offsets` (segments are short).
-__global__ void k_stage0_segmented(const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
+__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_stage0_segmented(const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
                                    int64_t nseg, const double* __restrict__ y_seg,
                                    const double* __restrict__ f0_seg, double k,
                                    const double* __restrict__ v1, WalkGrid g, double* out) {
@@ -188,7 +211,7 @@ __global__ void k_stage0_segmented(const double* __restrict__ u_flat, const int6
 // Local update, stage 0, part 1 (problem.py:95-97): the three FD probes
 // u+h, u, u-h of every point.  probe-major layout so a warp walks adjacent
 // centres (coalesced v1 reads).
-__global__ void k_lu0_probe(const double* __restrict__ y0, const double* __restrict__ f0,
+__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_lu0_probe(const double* __restrict__ y0, const double* __restrict__ f0,
                             const double* __restrict__ u0, double k, const double* __restrict__ v1,
                             WalkGrid g, double fd_step, int64_t begin, int64_t n, double* cost3) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -216,7 +239,7 @@ __device__ __forceinline__ double newton_step(double u, double c1, double c2,
 // Local update, stage 0, part 2: derivatives (problem.py:99-101), step,
 // cost_new and the monotone guard (solver.py:193-203).  cost_old is the
 // bitwise-identical `mid` probe.
-__global__ void k_lu0_finish(const double* __restrict__ y0, const double* __restrict__ f0,
+__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_lu0_finish(const double* __restrict__ y0, const double* __restrict__ f0,
                              const double* __restrict__ u0, double k, const double* __restrict__ v1,
                              WalkGrid g, ucp_local_params lp, int64_t begin, int64_t n,
                              const double* __restrict__ cost3, double* out, int64_t* err) {
@@ -242,7 +265,7 @@ __global__ void k_lu0_finish(const double* __restrict__ y0, const double* __rest
 }
 
 // Objective integrand (problem.py:116-127): c_i = C0(u0_i, y0_i).
-__global__ void k_obj_terms(const double* __restrict__ y0, const double* __restrict__ f0,
+__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_obj_terms(const double* __restrict__ y0, const double* __restrict__ f0,
                             const double* __restrict__ u0, double k, const double* __restrict__ v1,
                             WalkGrid g, int64_t begin, int64_t end, double* terms, int64_t* err) {
   int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -359,7 +382,7 @@ __global__ void k_ex_fill(const double* __restrict__ u, const int64_t* __restric
   }
 }
 
-__global__ void k_ex0_eval(const double* __restrict__ y0, const double* __restrict__ f0,
+__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_ex0_eval(const double* __restrict__ y0, const double* __restrict__ f0,
                            const double* __restrict__ u0, double k, const double* __restrict__ v1,
                            WalkGrid g, const int64_t* __restrict__ total,
                            const int32_t* __restrict__ cand_pt, const int32_t* __restrict__ cand_j,
@@ -717,6 +740,11 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   return UCP_OK;
 }
 
+int check_aligned(const void* v) {
+  if (reinterpret_cast<uintptr_t>(v) & 15u) return arg_fail("controller arrays must be 16-byte aligned");
+  return UCP_OK;
+}
+
 int check_problem(const ucp_wc_problem* P) {
   if (!P || !P->y0 || !P->y1 || !P->f0 || !P->fw0) return arg_fail("null problem pointer");
   if (P->d0 < 2 || P->d1 < 2) return arg_fail("grid.d must be at least 2");
@@ -781,6 +809,7 @@ int ucp_gauss_moments_grid(const double* s, int64_t n, const double* v, double a
                            double* t0, double* t1, double* t2, void* stream) {
   if (n < 0 || d < 2 || d > INT32_MAX) return arg_fail("gauss_moments_grid: bad sizes");
   if (n == 0) return UCP_OK;
+  if (int rc_ = check_aligned(v)) return rc_;
   WalkGrid g = make_walk_grid(a, h, d);
   k_gauss_grid<<<nblocks(n, 128), 128, 0, as_stream(stream)>>>(s, n, v, g, t0, t1, t2);
   UCP_LAUNCHED("k_gauss_grid");
@@ -834,6 +863,7 @@ int ucp_wc_stage0_cost(const ucp_wc_problem* P, const double* v1, const double* 
   if (nseg < 0 || n_cand < 0) return arg_fail("stage0_cost: bad sizes");
   if (nseg == 0 || n_cand == 0) return UCP_OK;
   const int64_t n_host = n_cand;
+  if (int rc_ = check_aligned(v1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
   k_stage0_segmented<<<nblocks(n_host, 128), 128, 0, as_stream(stream)>>>(u_flat, offsets, nseg, y_seg,
                                                                            f0_seg, P->k, v1, g, out);
@@ -877,6 +907,7 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
   if (stage == 0) {
     void* pc;
     if ((rc = ws_get(ws, WS_COST, sizeof(double) * 3 * (size_t)n, &pc))) return rc;
+    if (int rc_ = check_aligned(u1)) return rc_;
     WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
     k_lu0_probe<<<nblocks(3 * n, 128), 128, 0, st>>>(P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
                                                      (double*)pc);
@@ -947,6 +978,7 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
   k_ex_fill<<<nblocks(n, 256), 256, 0, st>>>(u0, win_lo, win_hi, begin, n, counts, (int32_t*)ppt,
                                                (int32_t*)pj);
   UCP_LAUNCHED("k_ex_fill");
+  if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
   k_ex0_eval<<<nblocks(total, 128), 128, 0, st>>>(P->y0, P->f0, u0, P->k, u1, g, counts + n,
                                                   (const int32_t*)ppt, (const int32_t*)pj, (double*)pc);
@@ -963,6 +995,7 @@ int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const doub
   if (rc) return rc;
   if (begin < 0 || end > P->d0 || begin > end) return arg_fail("objective_terms: bad shard");
   if (end == begin) return UCP_OK;
+  if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
   k_obj_terms<<<nblocks(end - begin, 128), 128, 0, as_stream(stream)>>>(P->y0, P->f0, u0, P->k, u1, g,
                                                                           begin, end, terms, err);
