@@ -50,6 +50,12 @@ class Sharding:
         import torch.distributed as dist
 
         c = buf.numel() // self.world
+        if buf.is_cuda and dist.get_backend(self.group) == "gloo":
+            # CPU-collective plumbing (multi-process tests on one GPU); NCCL in production
+            host = buf.cpu()
+            dist.all_gather_into_tensor(host, host[self.rank * c:(self.rank + 1) * c], group=self.group)
+            buf.copy_(host)
+            return
         dist.all_gather_into_tensor(buf, buf[self.rank * c:(self.rank + 1) * c], group=self.group)
 
     def allreduce_min_(self, t: torch.Tensor) -> None:
@@ -57,6 +63,11 @@ class Sharding:
             return
         import torch.distributed as dist
 
+        if t.is_cuda and dist.get_backend(self.group) == "gloo":
+            host = t.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.MIN, group=self.group)
+            t.copy_(host)
+            return
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
 
 

@@ -1,0 +1,176 @@
+"""Multi-rank plumbing: world_size-2 process groups.
+
+CPU (gloo): the Sharding partition/collectives, and the solver's block loop
+driven by a test-only oracle-backed problem -> bitwise identical to one rank.
+GPU (gloo, 2 processes on one GPU): the real device sweeps sharded over two
+ranks, bitwise identical to the single-process result.  (NCCL is the
+production backend; its collectives are the same two calls.)
+"""
+import os
+import socket
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _init(rank, world, port):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _spawn(fn, world, *args):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=fn, args=(r, world, port, q, *args)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return {r: v for r, v in out}
+
+
+# ------------------------------------------------------------- primitives
+def _prim_worker(rank, world, port, q):
+    _init(rank, world, port)
+    from paper_1908_04489_b200.distributed import Sharding, from_process_group
+
+    sh = from_process_group()
+    res = {}
+    for d in (1, 2, 3, 7, 201, 1000):
+        b, e = sh.bounds(d)
+        buf = sh.out_buffer(d, "cpu")
+        buf.fill_(-1.0)
+        buf[b:e] = torch.arange(b, e, dtype=torch.float64)
+        sh.allgather_(buf)
+        res[d] = (b, e, buf[:d].numpy().copy())
+    t = torch.tensor([10 + rank, 5 - rank, (1 << 63) - 1], dtype=torch.int64)
+    sh.allreduce_min_(t)
+    res["min"] = t.numpy().copy()
+    dist.destroy_process_group()
+    q.put((rank, res))
+
+
+def test_sharding_primitives_world2():
+    out = _spawn(_prim_worker, 2)
+    for d in (1, 2, 3, 7, 201, 1000):
+        (b0, e0, g0), (b1, e1, g1) = out[0][d], out[1][d]
+        assert b0 == 0 and e0 == b1 and e1 == d  # contiguous cover, no overlap
+        np.testing.assert_array_equal(g0, np.arange(d, dtype=np.float64))
+        np.testing.assert_array_equal(g1, g0)
+    np.testing.assert_array_equal(out[0]["min"], [10, 4, (1 << 63) - 1])
+
+
+# ------------------------------------- solver block loop over an oracle fake
+def _make_fake(orc, P, d):
+    p = orc.OracleWitsenhausen(grid0=(-25.0, 25.0, d), grid1=(-25.0, 25.0, d))
+    ocfg = orc.OracleConfig()
+
+    class OracleSharded(P.Problem):
+        """Test-only stand-in for the device sweeps: each rank computes its
+        shard with the oracle, then the shared Sharding all-gather."""
+
+        name = "witsenhausen"
+
+        def default_grid_specs(self):
+            return [(-25.0, 25.0, d)] * 2
+
+        def marginal_cost_segmented(self, *a):
+            raise NotImplementedError
+
+        def objective(self, U):
+            return orc.objective(p, U.values(0), U.values(1))
+
+        def _sweep(self, fn, m, U, sharding):
+            b, e = sharding.bounds(d)
+            buf = sharding.out_buffer(d, "cpu")
+            buf[b:e] = torch.from_numpy(fn(p, m, np.array(U.values(0)), np.array(U.values(1)), ocfg,
+                                           points=np.arange(b, e)))
+            sharding.allgather_(buf)
+            return buf[:d].numpy().copy()
+
+        def device_local_update(self, m, U, cfg, sharding):
+            return self._sweep(orc.local_update_phase, m, U, sharding)
+
+        def device_exhaustion(self, m, U, cfg, sharding):
+            return self._sweep(orc.partial_exhaustion_phase, m, U, sharding)
+
+    return OracleSharded(), p
+
+
+def _block_worker(rank, world, port, q, d):
+    _init(rank, world, port)
+    import paper_1908_04489_b200 as P
+    from oracle import oracle as orc
+
+    prob, p = _make_fake(orc, P, d)
+    sh = P.from_process_group()
+    rng = np.random.default_rng(3)
+    U = P.ControllerSet(tuple(P.SampledController(g, g.points + rng.uniform(-1, 1, d)) for g in prob.grids))
+    V = P.run_block(prob, U, P.SolverConfig(), 2, "local", sh)
+    V = P.run_block(prob, V, P.SolverConfig(), 1, "exhaustion", sh)
+    dist.destroy_process_group()
+    q.put((rank, (np.array(V.values(0)), np.array(V.values(1)))))
+
+
+@pytest.mark.parametrize("d", [201, 64])
+def test_block_loop_shard_invariant(oracle_mod, d):
+    import paper_1908_04489_b200 as P
+
+    out = _spawn(_block_worker, 2, d)
+    prob, p = _make_fake(oracle_mod, P, d)
+    rng = np.random.default_rng(3)
+    U = P.ControllerSet(tuple(P.SampledController(g, g.points + rng.uniform(-1, 1, d)) for g in prob.grids))
+    V = P.run_block(prob, U, P.SolverConfig(), 2, "local")
+    V = P.run_block(prob, V, P.SolverConfig(), 1, "exhaustion")
+    for r in (0, 1):
+        for m in (0, 1):
+            np.testing.assert_array_equal(out[r][m].view(np.uint64), np.asarray(V.values(m)).view(np.uint64))
+
+
+# ------------------------------------------------ real device sweeps, 2 ranks
+def _gpu_solve_worker(rank, world, port, q, d):
+    _init(rank, world, port)
+    import paper_1908_04489_b200 as P
+
+    torch.cuda.set_device(0)
+    prob = P.Witsenhausen(grids=[(-25.0, 25.0, d)] * 2)
+    res = P.solve(prob, P.SolverConfig(max_rounds=3), sharding=P.from_process_group())
+    out = (np.array(res.controllers.values(0)), np.array(res.controllers.values(1)), res.final_objective,
+           [r.objective for r in res.rounds])
+    dist.destroy_process_group()
+    q.put((rank, out))
+
+
+@pytest.mark.gpu
+def test_sharded_device_solve_bitwise_world2():
+    import paper_1908_04489_b200 as P
+
+    d = 301
+    out = _spawn(_gpu_solve_worker, 2, d)
+    prob = P.Witsenhausen(grids=[(-25.0, 25.0, d)] * 2)
+    ref = P.solve(prob, P.SolverConfig(max_rounds=3))
+    for r in (0, 1):
+        u0, u1, J, Js = out[r]
+        np.testing.assert_array_equal(u0.view(np.uint64), np.asarray(ref.controllers.values(0)).view(np.uint64))
+        np.testing.assert_array_equal(u1.view(np.uint64), np.asarray(ref.controllers.values(1)).view(np.uint64))
+        assert np.float64(J).view(np.uint64) == np.float64(ref.final_objective).view(np.uint64)
+        assert Js == [rr.objective for rr in ref.rounds]
