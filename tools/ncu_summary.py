@@ -17,7 +17,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 PROF = ROOT / "profiles"
-UNIT = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+UNIT = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}
 FAMILY = {"k_ex0_eval": "exh0", "k_lu0_probe": "local0", "k_lu0_finish": "local0", "k_moments": "local1"}
 
 
