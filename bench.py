@@ -412,7 +412,7 @@ def run_ours(args):
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch", {}).get(top)
+            traffic = json.loads(prof.read_text()).get(f"dram_bytes_per_launch_2p{args.log2d}", {}).get(top)
         except Exception:
             traffic = None
     roofline = {"bound": "fp64", "kernel": kernels[top][0], "achieved": fam[top]["achieved_tflops"],

@@ -91,6 +91,7 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--rep", action="append", default=[])
     ap.add_argument("--tag", required=True)
+    ap.add_argument("--log2d", type=int, default=None, help="grid size of the captured run (for traffic)")
     args = ap.parse_args()
     PROF.mkdir(exist_ok=True)
     summ_path = PROF / "ncu_summary.json"
@@ -102,10 +103,11 @@ def main():
     for rep in args.rep:
         for d in full(rep, args.tag + "_" + Path(rep).stem):
             fam = FAMILY.get(d["kernel"])
-            if fam and "dram__bytes_read.sum" in d:
+            if fam and args.log2d and "dram__bytes_read.sum" in d:
                 b = to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"])
-                summ.setdefault("dram_bytes_per_launch", {})[fam] = b
-                summ.setdefault("dram_source", {})[fam] = f"{rep} ({args.tag})"
+                if b == b:  # skip NaN captures
+                    summ.setdefault(f"dram_bytes_per_launch_2p{args.log2d}", {})[fam] = b
+                    summ.setdefault(f"dram_source_2p{args.log2d}", {})[fam] = f"{rep} ({args.tag})"
     summ_path.write_text(json.dumps(summ, indent=1) + "\n")
     print(json.dumps(summ, indent=1))
 
