@@ -94,6 +94,13 @@ __device__ __forceinline__ double phi_cdf(double z) { return ucp_phi_cdf_tab(z, 
 // window walk is inherently serial (multiplicative pdf recurrence,
 // kernels.py:438-439); one thread owns one centre.  Nodes 0 and d-1 (half
 // trapezoid weight) are peeled so the interior loop is branch-free.
+//
+// kLat (latency mode, used when a launch has too few walks to fill the GPU,
+// e.g. d = 2000): the thread prefetches its whole v1 window into L1 first and
+// issues each group's loads one group ahead, so a lone warp per scheduler is
+// bound by its DMUL chain instead of L2 latency.  Throughput mode (large d)
+// keeps the register footprint at 40 so 12 CTAs/SM hide the latency instead.
+template <bool kLat>
 __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__ v, const WalkGrid g) {
   long long jlo = (long long)ceil(((st - kGaussCut) - g.a) / g.h);
   long long jhi = (long long)floor(((st + kGaussCut) - g.a) / g.h);
@@ -124,6 +131,9 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
     const double vj_ = __ldg(v + j); \
     UCP_WALK_STEP_V(W, vj_);        \
   }
+    if (kLat) {
+      for (int p = j & ~15; p <= je; p += 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(v + p));
+    }
     const double hh = 0.5 * h;
     if (j == 0) {
       UCP_WALK_STEP(hh);
@@ -136,13 +146,35 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
       UCP_WALK_STEP(h);
       ++j;
     }
-    for (; j + 3 <= jint; j += 4) {
-      const double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
-      const double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
-      UCP_WALK_STEP_V(h, p0.x);
-      UCP_WALK_STEP_V(h, p0.y);
-      UCP_WALK_STEP_V(h, p1.x);
-      UCP_WALK_STEP_V(h, p1.y);
+    if (kLat) {
+      if (j + 3 <= jint) {
+        double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
+        double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
+        for (; j + 7 <= jint; j += 4) {
+          const double2 n0 = __ldg(reinterpret_cast<const double2*>(v + j + 4));
+          const double2 n1 = __ldg(reinterpret_cast<const double2*>(v + j + 6));
+          UCP_WALK_STEP_V(h, p0.x);
+          UCP_WALK_STEP_V(h, p0.y);
+          UCP_WALK_STEP_V(h, p1.x);
+          UCP_WALK_STEP_V(h, p1.y);
+          p0 = n0;
+          p1 = n1;
+        }
+        UCP_WALK_STEP_V(h, p0.x);
+        UCP_WALK_STEP_V(h, p0.y);
+        UCP_WALK_STEP_V(h, p1.x);
+        UCP_WALK_STEP_V(h, p1.y);
+        j += 4;
+      }
+    } else {
+      for (; j + 3 <= jint; j += 4) {
+        const double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
+        const double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
+        UCP_WALK_STEP_V(h, p0.x);
+        UCP_WALK_STEP_V(h, p0.y);
+        UCP_WALK_STEP_V(h, p1.x);
+        UCP_WALK_STEP_V(h, p1.y);
+      }
     }
     for (; j <= jint; ++j) UCP_WALK_STEP(h);
     if (je == last && j == last) UCP_WALK_STEP(hh);
@@ -165,10 +197,11 @@ __device__ __forceinline__ double quad_in_u(double a, double b, double c, double
 }
 
 // witsenhausen.py:64-70: C0(u, y) = f0(y) * (k^2 u^2 + E[(s - u1(y1))^2]), s = y+u
+template <bool kLat>
 __device__ __forceinline__ double stage0_cost(double u, double y, double f0, double k,
                                               const double* __restrict__ v1, const WalkGrid g) {
   double s = y + u;
-  Mom3 t = gauss_walk(s, v1, g);
+  Mom3 t = gauss_walk<kLat>(s, v1, g);
   double inner = quad_in_u(t.t0, t.t1, t.t2, s);
   return f0 * ((((k * k) * u) * u) + inner);
 }
@@ -181,11 +214,12 @@ __device__ __forceinline__ void flag_min(int64_t* slot, int64_t i) {
 
 // ---------------------------------------------------------------- kernels
 
-__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_gauss_grid(const double* __restrict__ s, int64_t n, const double* __restrict__ v,
+template <bool kLat>
+__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_gauss_grid(const double* __restrict__ s, int64_t n, const double* __restrict__ v,
                              WalkGrid g, double* t0, double* t1, double* t2) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  Mom3 r = gauss_walk(s[t], v, g);
+  Mom3 r = gauss_walk<kLat>(s[t], v, g);
   t0[t] = r.t0;
   t1[t] = r.t1;
   t2[t] = r.t2;
@@ -193,7 +227,8 @@ __global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_gauss_grid(con
 
 // marginal_cost_segmented m=0 over a flat candidate list; the segment of
 // candidate c is found by binary search in `offsets` (segments are short).
-__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_stage0_segmented(const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
+template <bool kLat>
+__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_stage0_segmented(const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
                                    int64_t nseg, const double* __restrict__ y_seg,
                                    const double* __restrict__ f0_seg, double k,
                                    const double* __restrict__ v1, WalkGrid g, double* out) {
@@ -205,13 +240,14 @@ __global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_stage0_segment
     int64_t mid = (lo + hi) >> 1;
     if (offsets[mid] <= c) lo = mid; else hi = mid;
   }
-  out[c] = stage0_cost(u_flat[c], y_seg[lo], f0_seg[lo], k, v1, g);
+  out[c] = stage0_cost<kLat>(u_flat[c], y_seg[lo], f0_seg[lo], k, v1, g);
 }
 
 // Local update, stage 0, part 1 (problem.py:95-97): the three FD probes
 // u+h, u, u-h of every point.  probe-major layout so a warp walks adjacent
 // centres (coalesced v1 reads).
-__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_lu0_probe(const double* __restrict__ y0, const double* __restrict__ f0,
+template <bool kLat>
+__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_lu0_probe(const double* __restrict__ y0, const double* __restrict__ f0,
                             const double* __restrict__ u0, double k, const double* __restrict__ v1,
                             WalkGrid g, double fd_step, int64_t begin, int64_t n, double* cost3) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -221,7 +257,7 @@ __global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_lu0_probe(cons
   double u = u0[i];
   double hh = fd_step * (1.0 + fabs(u));  // solver.py:192
   double uu = p == 0 ? u + hh : (p == 1 ? u : u - hh);
-  cost3[t] = stage0_cost(uu, y0[i], f0[i], k, v1, g);
+  cost3[t] = stage0_cost<kLat>(uu, y0[i], f0[i], k, v1, g);
 }
 
 // Newton-or-gradient step shared by both stages (solver.py:130-149).
@@ -239,7 +275,8 @@ __device__ __forceinline__ double newton_step(double u, double c1, double c2,
 // Local update, stage 0, part 2: derivatives (problem.py:99-101), step,
 // cost_new and the monotone guard (solver.py:193-203).  cost_old is the
 // bitwise-identical `mid` probe.
-__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_lu0_finish(const double* __restrict__ y0, const double* __restrict__ f0,
+template <bool kLat>
+__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_lu0_finish(const double* __restrict__ y0, const double* __restrict__ f0,
                              const double* __restrict__ u0, double k, const double* __restrict__ v1,
                              WalkGrid g, ucp_local_params lp, int64_t begin, int64_t n,
                              const double* __restrict__ cost3, double* out, int64_t* err) {
@@ -257,7 +294,7 @@ __global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_lu0_finish(con
     return;
   }
   double stepped = newton_step(u, c1, c2, lp);  // project() is the identity
-  double cost_new = stage0_cost(stepped, y0[i], f0[i], k, v1, g);
+  double cost_new = stage0_cost<kLat>(stepped, y0[i], f0[i], k, v1, g);
   if (!(finite(mid) && finite(cost_new))) flag_min(err + 1, i);
   double r = cost_new <= mid ? stepped : u;
   if (!finite(r)) flag_min(err + 2, i);
@@ -265,12 +302,13 @@ __global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_lu0_finish(con
 }
 
 // Objective integrand (problem.py:116-127): c_i = C0(u0_i, y0_i).
-__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_obj_terms(const double* __restrict__ y0, const double* __restrict__ f0,
+template <bool kLat>
+__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_obj_terms(const double* __restrict__ y0, const double* __restrict__ f0,
                             const double* __restrict__ u0, double k, const double* __restrict__ v1,
                             WalkGrid g, int64_t begin, int64_t end, double* terms, int64_t* err) {
   int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= end) return;
-  double c = stage0_cost(u0[i], y0[i], f0[i], k, v1, g);
+  double c = stage0_cost<kLat>(u0[i], y0[i], f0[i], k, v1, g);
   if (!finite(c)) flag_min(err, i);
   terms[i] = c;
 }
@@ -382,7 +420,8 @@ __global__ void k_ex_fill(const double* __restrict__ u, const int64_t* __restric
   }
 }
 
-__global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_ex0_eval(const double* __restrict__ y0, const double* __restrict__ f0,
+template <bool kLat>
+__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_ex0_eval(const double* __restrict__ y0, const double* __restrict__ f0,
                            const double* __restrict__ u0, double k, const double* __restrict__ v1,
                            WalkGrid g, const int64_t* __restrict__ total,
                            const int32_t* __restrict__ cand_pt, const int32_t* __restrict__ cand_j,
@@ -390,7 +429,7 @@ __global__ void __launch_bounds__(kWalkThreads, kWalkMinBlocks) k_ex0_eval(const
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= *total) return;
   int32_t i = cand_pt[c];
-  costs[c] = stage0_cost(u0[cand_j[c]], y0[i], f0[i], k, v1, g);
+  costs[c] = stage0_cost<kLat>(u0[cand_j[c]], y0[i], f0[i], k, v1, g);
 }
 
 // First strict minimum per point (kernels.py:147-160), kept in registers;
@@ -594,6 +633,69 @@ k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x
   }
 }
 
+// Small query sets (d ~ 2000): the direct kernel above would run a handful of
+// CTAs whose serial pair loops are pure latency.  Two-phase form instead:
+//  (A) every (support point i, query q) pair's pre-weight -- the reference's
+//      `wp` before `wp *= w[i]` (kernels.py:474-480) -- in parallel, stored
+//      q-contiguous;
+//  (B) one thread per query accumulates them in ascending i exactly as the
+//      reference does (`if wp != 0: wp *= w[i]; acc += ...`).
+// Same operations in the same order per pair and per accumulator: bitwise
+// equal to the direct kernel.
+constexpr int kPairChunk = 64;
+__global__ void __launch_bounds__(128)
+k_mom_pairs(const double* __restrict__ yq, int64_t n, const double* __restrict__ x,
+            const double2* __restrict__ tails, int64_t m, double a, double h, int64_t d, double* pre) {
+  __shared__ __align__(16) uint64_t stab[256];
+  for (int r = threadIdx.x; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
+  __syncthreads();
+  const ucp_exp_entry* stab2 = reinterpret_cast<const ucp_exp_entry*>(stab);
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const double yt = yq[q];
+  long long j = (long long)ceil((yt - a) / h - 0.5);
+  if (j < 0) j = 0;
+  if (j > d - 1) j = d - 1;
+  const bool at_left = j == 0, at_right = j == d - 1;
+  const double factor = (at_left || at_right) ? 0.5 : 1.0;
+  const double INV = inv_sqrt_2pi();
+  const int64_t i0 = (int64_t)blockIdx.y * kPairChunk;
+  const int64_t i1 = i0 + kPairChunk < m ? i0 + kPairChunk : m;
+  for (int64_t i = i0; i < i1; ++i) {
+    const double xi = x[i];
+    const double diff = yt - xi;
+    double wp = 0.0;
+    if (diff <= kGaussCut && diff >= -kGaussCut) wp = (factor * ucp_exp_core((-0.5 * diff) * diff, stab2)) * INV;
+    if (at_left) wp += tails[i].x;
+    if (at_right) wp += tails[i].y;
+    pre[i * n + q] = wp;
+  }
+}
+
+__global__ void __launch_bounds__(128)
+k_mom_accum(const double* __restrict__ pre, int64_t n, const double* __restrict__ x,
+            const double* __restrict__ w, int64_t m, double* o0, double* o1, double* o2) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  const double* col = pre + q;
+#pragma unroll 8
+  for (int64_t i = 0; i < m; ++i) {
+    double wp = col[i * n];
+    if (wp != 0.0) {
+      const double xi = __ldg(x + i);
+      wp *= __ldg(w + i);
+      acc0 += wp;
+      const double wx = wp * xi;
+      acc1 += wx;
+      acc2 += wx * xi;
+    }
+  }
+  o0[q] = acc0;
+  o1[q] = acc1;
+  o2[q] = acc2;
+}
+
 // Stage-1 candidates: C1(u, y) = A u^2 - 2 B u + C (witsenhausen.py:73-78).
 __global__ void k_stage1_segmented(const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
                                    int64_t nseg, const double* __restrict__ m0,
@@ -694,7 +796,10 @@ struct ucp_workspace {
 };
 
 namespace {
-enum { WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS, WS_NSLOTS };
+enum { WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS, WS_PAIRS, WS_NSLOTS };
+// two-phase moments when the query set cannot fill the GPU with the direct kernel
+constexpr int64_t kTwoPhaseMaxQueries = 8192;
+constexpr int64_t kTwoPhaseMaxPairs = (int64_t)1 << 25;  // 256 MiB of pre-weights
 
 int ws_get(ucp_workspace* ws, int slot, size_t bytes, void** out) {
   if (ws->cap[slot] < bytes) {
@@ -725,6 +830,17 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   k_x1_prepare<<<(unsigned)ntiles, kTile, 0, st>>>(y0, u0, m, a, h, b, (double*)px1, (double2*)ptails,
                                                    (double2*)ptile);
   UCP_LAUNCHED("k_x1_prepare");
+  if (nq <= kTwoPhaseMaxQueries && nq * m <= kTwoPhaseMaxPairs) {
+    void* ppre;
+    if ((rc = ws_get(ws, WS_PAIRS, sizeof(double) * (size_t)(nq * m), &ppre))) return rc;
+    dim3 grid_a(nblocks(nq, 128), (unsigned)((m + kPairChunk - 1) / kPairChunk));
+    k_mom_pairs<<<grid_a, 128, 0, st>>>(yq, nq, (const double*)px1, (const double2*)ptails, m, a, h, d,
+                                        (double*)ppre);
+    UCP_LAUNCHED("k_mom_pairs");
+    k_mom_accum<<<nblocks(nq, 128), 128, 0, st>>>((const double*)ppre, nq, (const double*)px1, w, m, o0, o1, o2);
+    UCP_LAUNCHED("k_mom_accum");
+    return UCP_OK;
+  }
   int* counter = (int*)((int64_t*)pctr + 1);
   UCP_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), st));
   int dev = 0, sms = 0, per_sm = 0;
@@ -739,6 +855,25 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   UCP_LAUNCHED("k_moments");
   return UCP_OK;
 }
+
+// Walk launches below one full wave of resident CTAs run the latency-mode walk.
+bool walk_latency_mode(int64_t n_walks) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+  }
+  return n_walks < (int64_t)sms * kWalkMinBlocks * kWalkThreads;
+}
+
+#define UCP_WALK_LAUNCH(kernel, n_walks, grid, stream, ...)                              \
+  do {                                                                                  \
+    if (walk_latency_mode(n_walks))                                                     \
+      kernel<true><<<(grid), kWalkThreads, 0, (stream)>>>(__VA_ARGS__);                 \
+    else                                                                                \
+      kernel<false><<<(grid), kWalkThreads, 0, (stream)>>>(__VA_ARGS__);                \
+  } while (0)
 
 int check_aligned(const void* v) {
   if (reinterpret_cast<uintptr_t>(v) & 15u) return arg_fail("controller arrays must be 16-byte aligned");
@@ -811,7 +946,7 @@ int ucp_gauss_moments_grid(const double* s, int64_t n, const double* v, double a
   if (n == 0) return UCP_OK;
   if (int rc_ = check_aligned(v)) return rc_;
   WalkGrid g = make_walk_grid(a, h, d);
-  k_gauss_grid<<<nblocks(n, 128), 128, 0, as_stream(stream)>>>(s, n, v, g, t0, t1, t2);
+  UCP_WALK_LAUNCH(k_gauss_grid, n, nblocks(n, kWalkThreads), as_stream(stream), s, n, v, g, t0, t1, t2);
   UCP_LAUNCHED("k_gauss_grid");
   return UCP_OK;
 }
@@ -865,7 +1000,7 @@ int ucp_wc_stage0_cost(const ucp_wc_problem* P, const double* v1, const double* 
   const int64_t n_host = n_cand;
   if (int rc_ = check_aligned(v1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
-  k_stage0_segmented<<<nblocks(n_host, 128), 128, 0, as_stream(stream)>>>(u_flat, offsets, nseg, y_seg,
+  UCP_WALK_LAUNCH(k_stage0_segmented, n_host, nblocks(n_host, kWalkThreads), as_stream(stream), u_flat, offsets, nseg, y_seg,
                                                                            f0_seg, P->k, v1, g, out);
   UCP_LAUNCHED("k_stage0_segmented");
   return UCP_OK;
@@ -909,10 +1044,10 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
     if ((rc = ws_get(ws, WS_COST, sizeof(double) * 3 * (size_t)n, &pc))) return rc;
     if (int rc_ = check_aligned(u1)) return rc_;
     WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
-    k_lu0_probe<<<nblocks(3 * n, 128), 128, 0, st>>>(P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
+    UCP_WALK_LAUNCH(k_lu0_probe, 3 * n, nblocks(3 * n, kWalkThreads), st, P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
                                                      (double*)pc);
     UCP_LAUNCHED("k_lu0_probe");
-    k_lu0_finish<<<nblocks(n, 128), 128, 0, st>>>(P->y0, P->f0, u0, P->k, u1, g, *lp, begin, n,
+    UCP_WALK_LAUNCH(k_lu0_finish, n, nblocks(n, kWalkThreads), st, P->y0, P->f0, u0, P->k, u1, g, *lp, begin, n,
                                                   (const double*)pc, out, err);
     UCP_LAUNCHED("k_lu0_finish");
     return UCP_OK;
@@ -980,7 +1115,7 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
   UCP_LAUNCHED("k_ex_fill");
   if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
-  k_ex0_eval<<<nblocks(total, 128), 128, 0, st>>>(P->y0, P->f0, u0, P->k, u1, g, counts + n,
+  UCP_WALK_LAUNCH(k_ex0_eval, total, nblocks(total, kWalkThreads), st, P->y0, P->f0, u0, P->k, u1, g, counts + n,
                                                   (const int32_t*)ppt, (const int32_t*)pj, (double*)pc);
   UCP_LAUNCHED("k_ex0_eval");
   k_ex_argmin<<<nblocks(n, 256), 256, 0, st>>>(u0, (const double*)pc, counts, (const int32_t*)pj, begin, n,
@@ -997,7 +1132,7 @@ int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const doub
   if (end == begin) return UCP_OK;
   if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
-  k_obj_terms<<<nblocks(end - begin, 128), 128, 0, as_stream(stream)>>>(P->y0, P->f0, u0, P->k, u1, g,
+  UCP_WALK_LAUNCH(k_obj_terms, end - begin, nblocks(end - begin, kWalkThreads), as_stream(stream), P->y0, P->f0, u0, P->k, u1, g,
                                                                           begin, end, terms, err);
   UCP_LAUNCHED("k_obj_terms");
   return UCP_OK;
