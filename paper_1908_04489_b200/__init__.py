@@ -34,6 +34,7 @@ from .solver import (
     partial_exhaustion_phase,
     run_block,
     solve,
+    solve_many,
 )
 from .witsenhausen import Witsenhausen
 
@@ -68,5 +69,5 @@ __all__ = [
     "Witsenhausen", "adaptive_allocation", "eval_controller", "eval_controller_many", "from_process_group",
     "init_identity", "local_update_phase", "make_grid", "make_problem", "max_workers", "nearest_index",
     "nearest_indices", "newton_or_gradient_step", "node_window_bounds", "partial_exhaustion_phase", "pdf",
-    "run_block", "set_workers", "solve", "trapezoid", "window_bounds", "window_indices", "__version__",
+    "run_block", "set_workers", "solve", "solve_many", "trapezoid", "window_bounds", "window_indices", "__version__",
 ]

@@ -675,25 +675,45 @@ k_mom_pairs(const double* __restrict__ yq, int64_t n, const double* __restrict__
 __global__ void __launch_bounds__(128)
 k_mom_accum(const double* __restrict__ pre, int64_t n, const double* __restrict__ x,
             const double* __restrict__ w, int64_t m, double* o0, double* o1, double* o2) {
+  // latency-bound by construction (one serial chain per query): keep 32
+  // pre-weight loads in flight per thread, x/w staged through shared memory
+  constexpr int kB = 32;
+  __shared__ double sx[256], sw[256];
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= n) return;
+  const bool active = q < n;
+  const double* col = pre + (active ? q : 0);
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-  const double* col = pre + q;
-#pragma unroll 8
-  for (int64_t i = 0; i < m; ++i) {
-    double wp = col[i * n];
-    if (wp != 0.0) {
-      const double xi = __ldg(x + i);
-      wp *= __ldg(w + i);
-      acc0 += wp;
-      const double wx = wp * xi;
-      acc1 += wx;
-      acc2 += wx * xi;
+  for (int64_t base = 0; base < m; base += 256) {
+    const int cnt = (int)(m - base < 256 ? m - base : 256);
+    __syncthreads();
+    for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
+      sx[r] = x[base + r];
+      sw[r] = w[base + r];
+    }
+    __syncthreads();
+    for (int r0 = 0; r0 < cnt; r0 += kB) {
+      double pv[kB];
+#pragma unroll
+      for (int k = 0; k < kB; ++k) pv[k] = (active && r0 + k < cnt) ? __ldcs(col + (base + r0 + k) * n) : 0.0;
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        double wp = pv[k];
+        if (wp != 0.0) {  // padding slots are 0.0: skipped like the reference's zeros
+          const double xi = sx[r0 + k];
+          wp *= sw[r0 + k];
+          acc0 += wp;
+          const double wx = wp * xi;
+          acc1 += wx;
+          acc2 += wx * xi;
+        }
+      }
     }
   }
-  o0[q] = acc0;
-  o1[q] = acc1;
-  o2[q] = acc2;
+  if (active) {
+    o0[q] = acc0;
+    o1[q] = acc1;
+    o2[q] = acc2;
+  }
 }
 
 // Stage-1 candidates: C1(u, y) = A u^2 - 2 B u + C (witsenhausen.py:73-78).

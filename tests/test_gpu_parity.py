@@ -253,3 +253,16 @@ def test_moments_direct_path_vs_oracle(P, oracle_mod, nq, m):
     want = oracle_mod.gauss_moments_points(y, x, w, a, h, m)
     for k in range(3):
         assert_bitwise(got[k], want[k], f"M{k}")
+
+
+def test_solve_many_matches_individual_solves(P):
+    """Concurrent instances (streams + threads) give each instance's solo result bitwise."""
+    pars = [(0.2, 5.0), (0.5, 3.0), (0.9, 7.0), (0.05, 5.0), (0.3, 3.0)]
+    grids = [(-25.0, 25.0, 301)] * 2
+    cfg = P.SolverConfig(max_rounds=4)
+    many = P.solve_many([P.Witsenhausen(k=k, sigma=s, grids=grids) for k, s in pars], cfg, concurrency=3)
+    for (k, s), r in zip(pars, many):
+        solo = P.solve(P.Witsenhausen(k=k, sigma=s, grids=grids), cfg)
+        assert r.final_objective == solo.final_objective
+        assert [x.objective for x in r.rounds] == [x.objective for x in solo.rounds]
+        np.testing.assert_array_equal(np.asarray(r.controllers.values(0)), np.asarray(solo.controllers.values(0)))
