@@ -1144,6 +1144,38 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
   return UCP_OK;
 }
 
+int ucp_wc_run_block(const ucp_wc_problem* P, int kind, int iters, double* u0, double* u1,
+                     const ucp_local_params* lp, const int64_t* win_lo0, const int64_t* win_hi0,
+                     const int64_t* win_lo1, const int64_t* win_hi1, double* scratch0, double* scratch1,
+                     int64_t* err, ucp_workspace* ws, void* stream) {
+  int rc = check_problem(P);
+  if (rc) return rc;
+  if (kind < 0 || kind > 1 || iters < 0) return arg_fail("run_block: bad kind/iters");
+  if (!u0 || !u1 || !scratch0 || !scratch1 || !err || !ws) return arg_fail("run_block: null argument");
+  if (kind == 0 && !lp) return arg_fail("run_block: local params missing");
+  if (kind == 1 && (!win_lo0 || !win_hi0 || !win_lo1 || !win_hi1)) return arg_fail("run_block: windows missing");
+  cudaStream_t st = as_stream(stream);
+  double* u[2] = {u0, u1};
+  double* scratch[2] = {scratch0, scratch1};
+  const int64_t d[2] = {P->d0, P->d1};
+  const int64_t* lo[2] = {win_lo0, win_lo1};
+  const int64_t* hi[2] = {win_hi0, win_hi1};
+  // solver.py:226-231: every phase reads the latest controllers; the new
+  // vector is written to scratch (the sweep reads the old one) and copied back
+  for (int it = 0; it < iters; ++it) {
+    for (int m = 0; m < 2; ++m) {
+      int64_t* e = err + 3 * (2 * (int64_t)it + m);
+      if (kind == 0)
+        rc = ucp_wc_local_update(P, m, u0, u1, lp + m, 0, d[m], scratch[m], e, ws, stream);
+      else
+        rc = ucp_wc_exhaustion(P, m, u0, u1, lo[m], hi[m], 0, d[m], scratch[m], e, ws, stream);
+      if (rc) return rc;
+      UCP_CHECK(cudaMemcpyAsync(u[m], scratch[m], sizeof(double) * (size_t)d[m], cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  return UCP_OK;
+}
+
 int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const double* u1, int64_t begin,
                            int64_t end, double* terms, int64_t* err, void* stream) {
   int rc = check_problem(P);

@@ -55,6 +55,17 @@ class _ErrorLog:
         self.meta.append((kind, stage))
         return row
 
+    def slots(self, metas: list, sharding: Sharding) -> torch.Tensor:
+        """Contiguous rows for a run of phases (one native block call)."""
+        need = len(metas)
+        if len(self.meta) + need > self.rows.shape[0]:
+            self.flush(sharding)
+            if need > self.rows.shape[0]:
+                self.rows = torch.full((need, 3), NO_ERROR, dtype=I64, device=self.device)
+        start = len(self.meta)
+        self.meta.extend(metas)
+        return self.rows[start:start + need]
+
     def flush(self, sharding: Sharding) -> None:
         n = len(self.meta)
         if n == 0:
@@ -227,6 +238,33 @@ class Witsenhausen(Problem):
                   ptr(buf), ptr(err), D.ws, D.stream)
         sharding.allgather_(buf)
         return buf[: g.d]
+
+    def device_run_block(self, kind: str, iters: int, U: ControllerSet, cfg) -> ControllerSet:
+        """`iters` iterations of one phase kind over both stages in ONE native
+        call (ucp_wc_run_block; solver.py:226-231), unsharded."""
+        from .grids import SampledController
+
+        if iters <= 0:
+            return U
+        D = self.device_context()
+        u0, u1 = self._uv(U)
+        out0, out1 = u0.clone(), u1.clone()
+        s0, s1 = torch.empty_like(out0), torch.empty_like(out1)
+        g0, g1 = self.grids
+        lp = (_lib.LocalParams * 2)(*[_lib.LocalParams(cfg.fd_step, cfg.curvature_min, cfg.grad_step,
+                                                       cfg.cap_for(g)) for g in (g0, g1)])
+        if kind == "local":
+            code, wins = 0, (None, None, None, None)
+        else:
+            code = 1
+            lo0, hi0 = D.window(self, 0, cfg.radius_for(g0))
+            lo1, hi1 = D.window(self, 1, cfg.radius_for(g1))
+            wins = (ptr(lo0), ptr(hi0), ptr(lo1), ptr(hi1))
+        err = D.errors.slots([(kind, m) for _ in range(iters) for m in (0, 1)], LOCAL)
+        _lib.call("ucp_wc_run_block", ctypes.byref(D.P), code, int(iters), ptr(out0), ptr(out1), lp, *wins,
+                  ptr(s0), ptr(s1), ptr(err), D.ws, D.stream)
+        return ControllerSet((SampledController(g0, out0, _trusted_device=True),
+                              SampledController(g1, out1, _trusted_device=True)))
 
     def device_objective(self, U: ControllerSet, sharding: Sharding = LOCAL) -> float:
         """problem.py:110-127: stage-0 integrand on device, then the serial trapezoid."""
