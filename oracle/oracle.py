@@ -64,6 +64,15 @@ def lib():
         L.orc_wc_stage1_cost.restype = None
         L.orc_wc_stage1_cost.argtypes = [
             _f64p, _i64p, _i64, _f64p, _f64p, _f64p, _i64, _dbl, _dbl, _i64, _f64p]
+        L.orc_unif_moments_grid.restype = None
+        L.orc_unif_moments_grid.argtypes = [_f64p, _i64, _f64p, _dbl, _dbl, _i64, _dbl, _f64p, _f64p, _f64p]
+        L.orc_unif_ball_sum.restype = None
+        L.orc_unif_ball_sum.argtypes = [_f64p, _i64, _f64p, _dbl, _dbl, _i64, _dbl, _f64p]
+        L.orc_unif_propagate.restype = None
+        L.orc_unif_propagate.argtypes = [_f64p, _f64p, _i64, _dbl, _dbl, _i64, _dbl, _f64p]
+        L.orc_unif_moments_points.restype = None
+        L.orc_unif_moments_points.argtypes = [_f64p, _i64, _f64p, _f64p, _f64p, _i64, _dbl, _dbl, _i64, _dbl,
+                                              _f64p, _f64p, _f64p]
         L.orc_phi_cdf.restype = _dbl
         L.orc_phi_cdf.argtypes = [_dbl]
         L.orc_num_threads.restype = ctypes.c_int
@@ -126,6 +135,35 @@ def phi_cdf(z):  # kernels.py:398-404
     return float(lib().orc_phi_cdf(float(z)))
 
 
+def unif_moments_grid(x, v, a, h, d, rad):  # kernels.py:488-525
+    x, v = _c(x), _c(v)
+    o = [np.empty(x.size) for _ in range(3)]
+    lib().orc_unif_moments_grid(x, x.size, v, float(a), float(h), int(d), float(rad), *o)
+    return tuple(o)
+
+
+def unif_ball_sum(x, g, a, h, d, rad):  # kernels.py:528-555
+    x, g = _c(x), _c(g)
+    out = np.empty(x.size)
+    lib().orc_unif_ball_sum(x, x.size, g, float(a), float(h), int(d), float(rad), out)
+    return out
+
+
+def unif_propagate(masses, centers, a, h, d, rad):  # kernels.py:558-577
+    masses, centers = _c(masses), _c(centers)
+    out = np.empty(int(d))
+    lib().orc_unif_propagate(masses, centers, centers.size, float(a), float(h), int(d), float(rad), out)
+    return out
+
+
+def unif_moments_points(y, centers, w, vals, a, h, d, rad):  # kernels.py:580-615
+    y, centers, w, vals = _c(y), _c(centers), _c(w), _c(vals)
+    o = [np.empty(y.size) for _ in range(3)]
+    lib().orc_unif_moments_points(y, y.size, centers, w, vals, centers.size, float(a), float(h), int(d),
+                                  float(rad), *o)
+    return tuple(o)
+
+
 # ------------------------------------------------------ grids / numerics glue
 
 
@@ -179,12 +217,26 @@ class OracleWitsenhausen:
         if self.f0 is None:
             self.f0 = gaussian_pdf(0.0, self.sigma, self.y0)
 
+    name = "witsenhausen"
+    M = 2
+
     def grid(self, m):
         return (self.y0, self.a0, self.h0, self.d0) if m == 0 else (self.y1, self.a1, self.h1, self.d1)
 
+    def span(self, m):
+        g = self.grid0 if m == 0 else self.grid1
+        return float(g[0]), float(g[1])
+
+    def h_floor(self, m):
+        return None
+
+    def project(self, m, v):
+        return v
+
     # witsenhausen.py:59-79.  y_centers are always stage grid points here
     # (indices `seg_idx`), whose f0 is the host-precomputed per-point value.
-    def cost_segmented(self, m, u_flat, offsets, seg_idx, u0, u1):
+    def cost_segmented(self, m, u_flat, offsets, seg_idx, Us_or_u0, u1=None):
+        u0, u1 = (Us_or_u0, u1) if u1 is not None else (Us_or_u0[0], Us_or_u0[1])
         u_flat, offsets = _c(u_flat), _c(offsets, np.int64)
         seg_idx = _c(seg_idx, np.int64)
         out = np.empty(u_flat.size)
@@ -202,14 +254,128 @@ class OracleWitsenhausen:
 
     def cost_batch(self, m, u, idx, u0, u1):  # problem.py:69-76
         u = _c(u)
-        return self.cost_segmented(m, u, np.arange(u.size + 1, dtype=np.int64), idx, u0, u1)
+        return self.cost_segmented(m, u, np.arange(u.size + 1, dtype=np.int64), idx, [u0, u1])
 
 
 class OracleNumericError(RuntimeError):
     """Mirror of problem.NumericError (problem.py:25-26)."""
 
 
-# --------------------------------------------------------------- solver.py
+def nearest_idx(points, a, h, d, y):  # grids.py:141-145
+    return np.clip(np.ceil((np.asarray(y, dtype=np.float64) - a) / h - 0.5).astype(np.int64), 0, d - 1)
+
+
+def _trap_weights(h, d):
+    w = np.full(d, h)
+    w[0] *= 0.5
+    w[-1] *= 0.5
+    return w
+
+
+class OracleZeroDelay:
+    """Restates problems/zero_delay.py:36-86 (uniform channel noise U(-1, 1))."""
+
+    name = "zero_delay"
+
+    def __init__(self, power_weight=2.0, grid0=(-5.0, 5.0, 2000), grid1=(-6.0, 6.0, 2000), f0=None, fw0=None):
+        self.pw = float(power_weight)
+        self.specs = [tuple(grid0), tuple(grid1)]
+        self.M = 2
+        self.pts = [linspace_grid(*g)[0] for g in self.specs]
+        self.hs = [linspace_grid(*g)[1] for g in self.specs]
+        self.f0 = gaussian_pdf(0.0, 1.0, self.pts[0]) if f0 is None else _c(f0)
+        self.fw0 = _trap_weights(self.hs[0], self.pts[0].size) * gaussian_pdf(0.0, 1.0, self.pts[0]) \
+            if fw0 is None else _c(fw0)
+
+    def grid(self, m):
+        return self.pts[m], float(self.specs[m][0]), self.hs[m], int(self.specs[m][2])
+
+    def span(self, m):
+        return float(self.specs[m][0]), float(self.specs[m][1])
+
+    def h_floor(self, m):  # zero_delay.py:56-65 (probe widened to one decoder cell)
+        return self.hs[1]
+
+    def project(self, m, v):
+        return v
+
+    def cost_segmented(self, m, u_flat, offsets, seg_idx, Us):
+        counts = np.diff(offsets)
+        _, a1, h1, d1 = self.grid(1)
+        if m == 0:  # zero_delay.py:69-76
+            y_flat = np.repeat(self.pts[0][seg_idx], counts)
+            s0, s1, s2 = unif_moments_grid(u_flat, Us[1], a1, h1, d1, 1.0)
+            distortion = s0 * y_flat * y_flat - 2.0 * s1 * y_flat + s2
+            f0 = np.repeat(self.f0[seg_idx], counts)
+            return f0 * (self.pw * u_flat * u_flat + distortion)
+        a, b, c = unif_moments_points(self.pts[1][seg_idx], Us[0], self.fw0, self.pts[0], a1, h1, d1, 1.0)
+        a, b, c = (np.repeat(t, counts) for t in (a, b, c))  # zero_delay.py:77-83
+        return a * u_flat * u_flat - 2.0 * b * u_flat + c
+
+
+class OracleInventory:
+    """Restates problems/inventory.py:31-150 (M stages, uniform demand, u >= 0)."""
+
+    name = "inventory"
+
+    def __init__(self, stages=2, order_cost=0.1, stage_cost="piecewise_linear", holding_rate=1.0,
+                 backlog_rate=1.0, grids=None):
+        self.M = int(stages)
+        self.oc = float(order_cost)
+        self.stage_cost = stage_cost
+        self.hr, self.br = float(holding_rate), float(backlog_rate)
+        self.specs = [tuple(g) for g in (grids or [(-3.0, 3.0, 601)] * self.M)]
+        self.pts = [linspace_grid(*g)[0] for g in self.specs]
+        self.hs = [linspace_grid(*g)[1] for g in self.specs]
+
+    def grid(self, m):
+        return self.pts[m], float(self.specs[m][0]), self.hs[m], int(self.specs[m][2])
+
+    def span(self, m):
+        return float(self.specs[m][0]), float(self.specs[m][1])
+
+    def gamma(self, x):  # inventory.py:61-69
+        if self.stage_cost == "quadratic":
+            return x * x
+        return self.hr * np.maximum(x, 0.0) + self.br * np.maximum(-x, 0.0)
+
+    def project(self, m, v):  # inventory.py:71-72
+        return np.maximum(v, 0.0)
+
+    def state(self, mm):  # inventory.py:74-76
+        return self.grid(min(mm, self.M - 1))
+
+    def h_floor(self, m):  # inventory.py:131-136
+        return self.state(m + 1)[2]
+
+    def downstream(self, Us):  # inventory.py:78-94
+        gs = [None] * (self.M + 1)
+        gs[self.M] = self.gamma(self.state(self.M)[0])
+        for mm in range(self.M - 1, 0, -1):
+            pts = self.pts[mm]
+            _, an, hn, dn = self.state(mm + 1)
+            expect = unif_ball_sum(pts + Us[mm], gs[mm + 1], an, hn, dn, 1.0)
+            gs[mm] = self.gamma(pts) + (self.oc * Us[mm] + expect)
+        return gs
+
+    def forward_density(self, m, Us):  # inventory.py:96-110
+        _, a0, h0, d0 = self.grid(0)
+        f = unif_propagate(np.array([1.0]), np.array([0.0]), a0, h0, d0, 1.0)
+        for mm in range(m):
+            _, an, hn, dn = self.grid(mm + 1)
+            f = unif_propagate(self.hs[mm] * f, self.pts[mm] + Us[mm], an, hn, dn, 1.0)
+        return f
+
+    def cost_segmented(self, m, u_flat, offsets, seg_idx, Us):  # inventory.py:138-150
+        counts = np.diff(offsets)
+        pts, a, h, d = self.grid(m)
+        y_flat = np.repeat(pts[seg_idx], counts)
+        f_m = self.forward_density(m, Us)
+        gs = self.downstream(Us)
+        _, an, hn, dn = self.state(m + 1)
+        expect = unif_ball_sum(y_flat + u_flat, gs[m + 1], an, hn, dn, 1.0)
+        weight = f_m[nearest_idx(pts, a, h, d, y_flat)]
+        return weight * (self.oc * u_flat + expect)
 
 
 @dataclass(frozen=True)
@@ -230,75 +396,72 @@ class OracleConfig:  # solver.py:47-97 (fields used on the hot path)
         return self.newton_cap if self.newton_cap is not None else (b - a) / 10.0
 
 
-def _grid_ab(p, m):
-    g = p.grid0 if m == 0 else p.grid1
-    return float(g[0]), float(g[1])
-
-
 def _bad(p, m, phase, i):
     y = p.grid(m)[0][int(i)]
     return OracleNumericError(
-        f"witsenhausen: non-finite marginal cost in {phase} phase at stage {m}, "
-        f"grid point {int(i)} (y={y!r})")
+        f"{p.name}: non-finite marginal cost in {phase} phase at stage {m}, grid point {int(i)} (y={y!r})")
 
 
-def local_update_phase(p: OracleWitsenhausen, m, u0, u1, cfg: OracleConfig, points=None):
-    """solver.py:179-203 with problem.py:88-102 and solver.py:146-149.
+def _cost_batch(p, m, u, idx, Us):
+    u = _c(u)
+    return p.cost_segmented(m, u, np.arange(u.size + 1, dtype=np.int64), idx, Us)
 
-    ``points`` restricts the sweep to a subset of grid indices (used for
-    bounded CPU-baseline samples); the default is the whole grid.
-    """
-    u_all = u0 if m == 0 else u1
+
+def local_update(p, m, Us, cfg: OracleConfig, points=None):
+    """solver.py:179-203 with problem.py:88-102 (and the problems' probe floors)."""
+    u_all = Us[m]
     idx = np.arange(u_all.size, dtype=np.int64) if points is None else _c(points, np.int64)
     u = u_all[idx]
     with np.errstate(over="ignore"):
         h = cfg.fd_step * (1.0 + np.abs(u))
-    up = p.cost_batch(m, u + h, idx, u0, u1)
-    mid = p.cost_batch(m, u, idx, u0, u1)
-    dn = p.cost_batch(m, u - h, idx, u0, u1)
+    floor = p.h_floor(m) if hasattr(p, "h_floor") else None
+    if floor is not None:
+        h = np.maximum(h, floor)
+    up = _cost_batch(p, m, u + h, idx, Us)
+    mid = _cost_batch(p, m, u, idx, Us)
+    dn = _cost_batch(p, m, u - h, idx, Us)
     with np.errstate(over="ignore", invalid="ignore"):
         c1 = (up - dn) / (2.0 * h)
         c2 = (up - 2.0 * mid + dn) / (h * h)
     bad = np.flatnonzero(~(np.isfinite(c1) & np.isfinite(c2)))
     if bad.size:
         raise _bad(p, m, "local-update", idx[bad[0]])
-    a, b = _grid_ab(p, m)
-    cap = cfg.cap(a, b)
+    cap = cfg.cap(*p.span(m))
     newton = c2 > cfg.curvature_min
     quot = np.divide(c1, c2, out=np.zeros_like(c1), where=newton)
-    stepped = np.where(newton, u - np.clip(quot, -cap, cap), u - cfg.grad_step * c1)
-    cost_old = p.cost_batch(m, u, idx, u0, u1)
-    cost_new = p.cost_batch(m, stepped, idx, u0, u1)
+    stepped = p.project(m, np.where(newton, u - np.clip(quot, -cap, cap), u - cfg.grad_step * c1))
+    cost_old = _cost_batch(p, m, u, idx, Us)
+    cost_new = _cost_batch(p, m, stepped, idx, Us)
     bad = np.flatnonzero(~(np.isfinite(cost_old) & np.isfinite(cost_new)))
     if bad.size:
         raise _bad(p, m, "local-update", idx[bad[0]])
     return np.where(cost_new <= cost_old, stepped, u)
 
 
-def partial_exhaustion_phase(p: OracleWitsenhausen, m, u0, u1, cfg: OracleConfig, points=None):
+def partial_exhaustion(p, m, Us, cfg: OracleConfig, points=None):
     """solver.py:206-223 with grids.py:180-195 and kernels.py:147-187."""
     y, a, h, d = p.grid(m)
-    u = u0 if m == 0 else u1
-    lo, hi = node_window_bounds(y, a, h, d, cfg.radius(*_grid_ab(p, m)))
+    lo, hi = node_window_bounds(y, a, h, d, cfg.radius(*p.span(m)))
     idx = np.arange(d, dtype=np.int64) if points is None else _c(points, np.int64)
-    cand, offsets = flatten_windows(u, lo[idx], hi[idx])
-    costs = p.cost_segmented(m, cand, offsets, idx, u0, u1)
+    cand, offsets = flatten_windows(Us[m], lo[idx], hi[idx])
+    costs = p.cost_segmented(m, cand, offsets, idx, Us)
     bad = np.flatnonzero(~np.isfinite(costs))
     if bad.size:
         seg = int(np.searchsorted(offsets, bad[0], side="right") - 1)
         raise _bad(p, m, "partial-exhaustion", idx[seg])
-    return cand[segmented_argmin(costs, offsets)]
+    return p.project(m, cand[segmented_argmin(costs, offsets)])
 
 
-def objective(p: OracleWitsenhausen, u0, u1):  # problem.py:110-127
-    costs = p.cost_batch(0, u0, np.arange(p.d0, dtype=np.int64), u0, u1)
+def objective_of(p, Us):  # problem.py:110-127
+    y, a, h, d = p.grid(0)
+    costs = _cost_batch(p, 0, Us[0], np.arange(d, dtype=np.int64), Us)
     bad = np.flatnonzero(~np.isfinite(costs))
     if bad.size:
         i = int(bad[0])
         raise OracleNumericError(
-            f"witsenhausen: non-finite objective integrand at stage 0, grid point {i} "
-            f"(y={p.y0[i]!r}, u={u0[i]!r})")
-    return trapezoid_sum(costs, p.h0)
+            f"{p.name}: non-finite objective integrand at stage 0, grid point {i} "
+            f"(y={y[i]!r}, u={Us[0][i]!r})")
+    return trapezoid_sum(costs, h)
 
 
 def adaptive_allocation(gl, ge, n):  # solver.py:152-167
@@ -310,24 +473,24 @@ def adaptive_allocation(gl, ge, n):  # solver.py:152-167
     return nl, n - nl
 
 
-def solve(p: OracleWitsenhausen, cfg: OracleConfig | None = None, u0=None, u1=None):
-    """solver.py:234-290 (adaptive local/exhaustion rounds)."""
+def solve_generic(p, cfg: OracleConfig | None = None, Us=None):
+    """solver.py:234-290 (adaptive local/exhaustion rounds) for any oracle problem."""
     cfg = cfg or OracleConfig()
-    u0 = p.y0.copy() if u0 is None else _c(u0).copy()
-    u1 = p.y1.copy() if u1 is None else _c(u1).copy()
+    Us = [p.grid(m)[0].copy() for m in range(p.M)] if Us is None else [_c(u).copy() for u in Us]
+    Us = [p.project(m, Us[m]) for m in range(p.M)]
     n = cfg.iters_per_round
     n_local = n // 2
-    current = objective(p, u0, u1)
+    current = objective_of(p, Us)
     rounds = []
     term = "max_rounds"
     for r in range(1, cfg.max_rounds + 1):
-        for phase, iters in ((local_update_phase, n_local), (partial_exhaustion_phase, n - n_local)):
+        for phase, iters in ((local_update, n_local), (partial_exhaustion, n - n_local)):
             for _ in range(iters):
-                u0 = phase(p, 0, u0, u1, cfg)
-                u1 = phase(p, 1, u0, u1, cfg)
-            if phase is local_update_phase:
-                after_local = objective(p, u0, u1)
-        after_exh = objective(p, u0, u1)
+                for m in range(p.M):
+                    Us[m] = phase(p, m, Us, cfg)
+            if phase is local_update:
+                after_local = objective_of(p, Us)
+        after_exh = objective_of(p, Us)
         gl, ge = abs(current - after_local), abs(after_local - after_exh)
         rounds.append((r, after_exh, gl, ge, n_local, n - n_local, after_local))
         current = after_exh
@@ -335,7 +498,25 @@ def solve(p: OracleWitsenhausen, cfg: OracleConfig | None = None, u0=None, u1=No
             term = "converged"
             break
         n_local, _ = adaptive_allocation(gl, ge, n)
-    return u0, u1, current, rounds, term
+    return Us, current, rounds, term
+
+
+# ---- Witsenhausen wrappers (two controllers passed explicitly) --------------
+def local_update_phase(p, m, u0, u1, cfg: OracleConfig, points=None):
+    return local_update(p, m, [u0, u1], cfg, points)
+
+
+def partial_exhaustion_phase(p, m, u0, u1, cfg: OracleConfig, points=None):
+    return partial_exhaustion(p, m, [u0, u1], cfg, points)
+
+
+def objective(p, u0, u1):
+    return objective_of(p, [u0, u1])
+
+
+def solve(p, cfg: OracleConfig | None = None, u0=None, u1=None):
+    Us, J, rounds, term = solve_generic(p, cfg, None if u0 is None else [u0, u1])
+    return Us[0], Us[1], J, rounds, term
 
 
 def host_cpu_description() -> dict:

@@ -220,6 +220,119 @@ void orc_wc_stage1_cost(const double* u_flat, const int64_t* offsets, int64_t ns
   free(mom);
 }
 
+/* ---------------------------------------------------------------------------
+ * Uniform-noise kernels (config 5: ZeroDelay, Inventory).  Cell j of a grid
+ * spans [a + h(j - 1/2), a + h(j + 1/2)], the end cells extend to -/+HUGE
+ * (kernels.py:302-309 _cell_edges; numba bodies kernels.py:488-615).
+ * ------------------------------------------------------------------------- */
+#define HUGE_EDGE 1.0e300
+
+static inline int64_t cell_index(double x, double a, double h, int64_t d) {
+  int64_t j = (int64_t)ceil((x - a) / h - 0.5);
+  if (j < 0) j = 0;
+  if (j > d - 1) j = d - 1;
+  return j;
+}
+
+static inline double cell_left(int64_t j, double a, double h) { return j > 0 ? a + h * ((double)j - 0.5) : -HUGE_EDGE; }
+static inline double cell_right(int64_t j, double a, double h, int64_t d) {
+  return j < d - 1 ? a + h * ((double)j + 0.5) : HUGE_EDGE;
+}
+
+/* kernels.py:488-525 (_unif_moments_grid_numba) */
+void orc_unif_moments_grid(const double* x, int64_t n, const double* v, double a, double h, int64_t d,
+                           double rad, double* s0, double* s1, double* s2) {
+  double inv = 1.0 / (2.0 * rad);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < n; ++t) {
+    double xlo = x[t] - rad, xhi = x[t] + rad;
+    int64_t jlo = cell_index(xlo, a, h, d), jhi = cell_index(xhi, a, h, d);
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    for (int64_t j = jlo; j <= jhi; ++j) {
+      double lj = cell_left(j, a, h), rj = cell_right(j, a, h, d);
+      double lo = xlo > lj ? xlo : lj;
+      double hi = xhi < rj ? xhi : rj;
+      double ov = hi - lo;
+      if (ov > 0.0) {
+        double vj = v[j];
+        acc0 += ov;
+        acc1 += ov * vj;
+        acc2 += (ov * vj) * vj;
+      }
+    }
+    s0[t] = acc0 * inv;
+    s1[t] = acc1 * inv;
+    s2[t] = acc2 * inv;
+  }
+}
+
+/* kernels.py:528-555 (_unif_ball_sum_numba) */
+void orc_unif_ball_sum(const double* x, int64_t n, const double* g, double a, double h, int64_t d, double rad,
+                       double* out) {
+  double inv = 1.0 / (2.0 * rad);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < n; ++t) {
+    double xlo = x[t] - rad, xhi = x[t] + rad;
+    int64_t jlo = cell_index(xlo, a, h, d), jhi = cell_index(xhi, a, h, d);
+    double acc = 0.0;
+    for (int64_t j = jlo; j <= jhi; ++j) {
+      double lj = cell_left(j, a, h), rj = cell_right(j, a, h, d);
+      double lo = xlo > lj ? xlo : lj;
+      double hi = xhi < rj ? xhi : rj;
+      double ov = hi - lo;
+      if (ov > 0.0) acc += ov * g[j];
+    }
+    out[t] = acc * inv;
+  }
+}
+
+/* kernels.py:558-577 (_unif_propagate_numba): out has d entries */
+void orc_unif_propagate(const double* masses, const double* centers, int64_t n, double a, double h, int64_t d,
+                        double rad, double* out) {
+  double inv = 1.0 / ((2.0 * rad) * h);
+#pragma omp parallel for schedule(static)
+  for (int64_t j = 0; j < d; ++j) {
+    double lj = cell_left(j, a, h), rj = cell_right(j, a, h, d);
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      double lo = centers[i] - rad, hi = centers[i] + rad;
+      if (lo < lj) lo = lj;
+      if (hi > rj) hi = rj;
+      double ov = hi - lo;
+      if (ov > 0.0) acc += masses[i] * ov;
+    }
+    out[j] = acc * inv;
+  }
+}
+
+/* kernels.py:580-615 (_unif_moments_points_numba) */
+void orc_unif_moments_points(const double* y, int64_t n, const double* centers, const double* w,
+                             const double* vals, int64_t m, double a, double h, int64_t d, double rad,
+                             double* m0, double* m1, double* m2) {
+  double inv = 1.0 / ((2.0 * rad) * h);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < n; ++t) {
+    int64_t j = cell_index(y[t], a, h, d);
+    double lj = cell_left(j, a, h), rj = cell_right(j, a, h, d);
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      double lo = centers[i] - rad, hi = centers[i] + rad;
+      if (lo < lj) lo = lj;
+      if (hi > rj) hi = rj;
+      double ov = hi - lo;
+      if (ov > 0.0) {
+        double wov = w[i] * ov, vi = vals[i];
+        acc0 += wov;
+        acc1 += wov * vi;
+        acc2 += (wov * vi) * vi;
+      }
+    }
+    m0[t] = acc0 * inv;
+    m1[t] = acc1 * inv;
+    m2[t] = acc2 * inv;
+  }
+}
+
 #ifdef _OPENMP
 #include <omp.h>
 int orc_num_threads(void) { return omp_get_max_threads(); }

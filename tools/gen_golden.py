@@ -29,7 +29,7 @@ import numpy as np  # noqa: E402
 from ucpsolve import kernels  # noqa: E402
 from ucpsolve.grids import ControllerSet, SampledController, nearest_indices  # noqa: E402
 from ucpsolve.numerics import pdf  # noqa: E402
-from ucpsolve.problems import Witsenhausen  # noqa: E402
+from ucpsolve.problems import Inventory, Witsenhausen, ZeroDelay  # noqa: E402
 from ucpsolve.solver import (  # noqa: E402
     SolverConfig,
     local_update_phase,
@@ -165,6 +165,68 @@ def fine_fixture(res2000, log2d=20, n_centres=384, n_queries=12):
                         q_idx=q_idx, m0=p[0], m1=p[1], m2=p[2])
 
 
+def generic_fixture(prob, tag, solve_too=True, extra=None):
+    """Phases, objective and (optionally) a full solve of a config-5 problem."""
+    cfg = SolverConfig()
+    out = {"specs": np.array([[g.a, g.b, g.d] for g in prob.grids])}
+    if extra:
+        out.update(extra)
+    sets = {"ident": prob.identity_controllers(), "pert0": perturbed(prob, 0, 0.3), "pert1": perturbed(prob, 1, 1.0)}
+    # the solver starts from projected controllers (solver.py:241-248)
+    for name, U in sets.items():
+        for m in range(prob.M):
+            U = U.replace(m, U[m].with_values(prob.project(m, U.values(m))))
+        for m in range(prob.M):
+            out[f"{name}_u{m}"] = U.values(m)
+        out[f"{name}_J"] = prob.objective(U)
+        for m in range(prob.M):
+            g = prob.grids[m]
+            out[f"{name}_c{m}"] = prob.marginal_cost_batch(m, U.values(m), g.points, U)
+            out[f"{name}_lu{m}"] = local_update_phase(prob, m, U, cfg)
+            out[f"{name}_ex{m}"] = partial_exhaustion_phase(prob, m, U, cfg)
+        V = U
+        for ph in (local_update_phase, partial_exhaustion_phase):
+            for m in range(prob.M):
+                V = V.replace(m, V[m].with_values(ph(prob, m, V, cfg)))
+        for m in range(prob.M):
+            out[f"{name}_it_u{m}"] = V.values(m)
+        out[f"{name}_it_J"] = prob.objective(V)
+    if solve_too:
+        t0 = time.perf_counter()
+        res = solve(prob, cfg)
+        out["solve_wall_s"] = time.perf_counter() - t0
+        out["solve_rounds"] = np.array([[r.round_index, r.objective, r.local_gain, r.exhaustion_gain,
+                                         r.local_iters, r.exhaustion_iters, r.objective_after_local]
+                                        for r in res.rounds])
+        out["solve_J"] = res.final_objective
+        out["solve_termination"] = res.termination
+        for m in range(prob.M):
+            out[f"solve_u{m}"] = res.controllers.values(m)
+    np.savez_compressed(OUT / f"{tag}.npz", **out)
+
+
+def config5_fixtures():
+    zd = ZeroDelay(grids=[(-5.0, 5.0, 201), (-6.0, 6.0, 241)])
+    generic_fixture(zd, "zd_small", extra={"f0": pdf(zd._source, zd.grids[0].points), "fw0": zd._fw0, "pw": 2.0})
+    zd2 = ZeroDelay(power_weight=0.7, grids=[(-5.0, 5.0, 400), (-6.0, 6.0, 333)])
+    generic_fixture(zd2, "zd_pw07", solve_too=True,
+                    extra={"f0": pdf(zd2._source, zd2.grids[0].points), "fw0": zd2._fw0, "pw": 0.7})
+    inv = Inventory(grids=[(-3.0, 3.0, 241)] * 2)
+    generic_fixture(inv, "inv_m2", extra={"stages": 2, "stage_cost": "piecewise_linear"})
+    inv3 = Inventory(stages=3, grids=[(-3.0, 3.0, 121)] * 3)
+    generic_fixture(inv3, "inv_m3", extra={"stages": 3, "stage_cost": "piecewise_linear"})
+    invq = Inventory(stages=3, stage_cost="quadratic", order_cost=0.3, grids=[(-3.0, 3.0, 97), (-2.5, 3.5, 131),
+                                                                               (-3.0, 2.0, 111)])
+    generic_fixture(invq, "inv_m3q", extra={"stages": 3, "stage_cost": "quadratic", "order_cost": 0.3})
+    inv1 = Inventory(stages=1, grids=[(-3.0, 3.0, 151)])
+    generic_fixture(inv1, "inv_m1", extra={"stages": 1, "stage_cost": "piecewise_linear"})
+    # default-grid solves (config 5 headline sizes)
+    zdd = ZeroDelay()
+    generic_fixture(zdd, "zd_default", extra={"f0": pdf(zdd._source, zdd.grids[0].points), "fw0": zdd._fw0,
+                                              "pw": 2.0})
+    generic_fixture(Inventory(), "inv_default", extra={"stages": 2, "stage_cost": "piecewise_linear"})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-big", action="store_true", help="skip the d=2000 solve and 2^20 samples")
@@ -175,6 +237,7 @@ def main():
 
     meta["numba"] = numba.__version__
     kernels_fixture()
+    config5_fixtures()
     wc_phase_fixture(201, "d201")
     wc_phase_fixture(2000, "d2000")
     _, w201 = wc_solve_fixture(201, "d201")
