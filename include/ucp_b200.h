@@ -143,6 +143,75 @@ int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const doub
                            int64_t begin, int64_t end, double* terms, int64_t* err,
                            void* stream);
 
+/* ---- config 5: uniform-noise kernels and the other UCP examples -----------
+ * kernels.py:488-615 (numba bodies); rad = noise half-width. */
+int ucp_unif_moments_grid(const double* x, int64_t n, const double* v, double a, double h, int64_t d,
+                          double rad, double* s0, double* s1, double* s2, void* stream);
+int ucp_unif_ball_sum(const double* x, int64_t n, const double* g, double a, double h, int64_t d,
+                      double rad, double* out, void* stream);
+/* out has d entries */
+int ucp_unif_propagate(const double* masses, const double* centers, int64_t n, double a, double h,
+                       int64_t d, double rad, double* out, void* stream);
+int ucp_unif_moments_points(const double* y, int64_t n, const double* centers, const double* w,
+                            const double* vals, int64_t m, double a, double h, int64_t d, double rad,
+                            double* m0, double* m1, double* m2, void* stream);
+
+/* Zero-delay source-channel coding (problems/zero_delay.py:36-86): encoder
+ * grid 0, decoder grid 1, f0 = pdf(N(0,1), y0) and fw0 from host NumPy. */
+typedef struct ucp_zd_problem {
+  double power_weight;
+  double a0, h0;
+  int64_t d0;
+  double a1, h1;
+  int64_t d1;
+  const double* y0;
+  const double* y1;
+  const double* f0;
+  const double* fw0;
+} ucp_zd_problem;
+/* marginal_cost_segmented (zero_delay.py:66-86): y_seg/f0_seg per segment */
+int ucp_zd_cost(const ucp_zd_problem* P, int stage, const double* u0, const double* u1,
+                const double* u_flat, int64_t n_cand, const int64_t* offsets, const double* y_seg,
+                const double* f0_seg, int64_t nseg, double* out, ucp_workspace* ws, void* stream);
+/* local update with the widened probe h = max(h, h1) (zero_delay.py:56-65) */
+int ucp_zd_local_update(const ucp_zd_problem* P, int stage, const double* u0, const double* u1,
+                        const ucp_local_params* lp, int64_t begin, int64_t end, double* out,
+                        int64_t* err, ucp_workspace* ws, void* stream);
+int ucp_zd_exhaustion(const ucp_zd_problem* P, int stage, const double* u0, const double* u1,
+                      const int64_t* win_lo, const int64_t* win_hi, int64_t begin, int64_t end,
+                      double* out, int64_t* err, ucp_workspace* ws, void* stream);
+int ucp_zd_objective_terms(const ucp_zd_problem* P, const double* u0, const double* u1,
+                           int64_t begin, int64_t end, double* terms, int64_t* err, void* stream);
+
+/* Multi-stage inventory control (problems/inventory.py:31-150), M <= 16
+ * stages, grid m = (a[m], h[m], d[m]) with device points pts[m]; controllers
+ * are passed as a host array of M device pointers.  Projection u >= 0. */
+#define UCP_INV_MAX_STAGES 16
+typedef struct ucp_inv_problem {
+  int32_t stages;
+  int32_t quadratic; /* stage_cost: 0 piecewise_linear, 1 quadratic */
+  double order_cost, holding_rate, backlog_rate;
+  double a[UCP_INV_MAX_STAGES];
+  double h[UCP_INV_MAX_STAGES];
+  int64_t d[UCP_INV_MAX_STAGES];
+  const double* pts[UCP_INV_MAX_STAGES];
+} ucp_inv_problem;
+int ucp_inv_cost(const ucp_inv_problem* P, int stage, const double* const* u, const double* u_flat,
+                 int64_t n_cand, const int64_t* offsets, const double* y_seg, int64_t nseg,
+                 double* out, ucp_workspace* ws, void* stream);
+int ucp_inv_local_update(const ucp_inv_problem* P, int stage, const double* const* u,
+                         const ucp_local_params* lp, int64_t begin, int64_t end, double* out,
+                         int64_t* err, ucp_workspace* ws, void* stream);
+int ucp_inv_exhaustion(const ucp_inv_problem* P, int stage, const double* const* u,
+                       const int64_t* win_lo, const int64_t* win_hi, int64_t begin, int64_t end,
+                       double* out, int64_t* err, ucp_workspace* ws, void* stream);
+int ucp_inv_objective_terms(const ucp_inv_problem* P, const double* const* u, int64_t begin,
+                            int64_t end, double* terms, int64_t* err, ucp_workspace* ws,
+                            void* stream);
+/* stock density at stage m (inventory.py:96-110), out[d[m]] */
+int ucp_inv_forward_density(const ucp_inv_problem* P, int stage, const double* const* u, double* out,
+                            ucp_workspace* ws, void* stream);
+
 /* ---- instrumentation ------------------------------------------------------
  * FP64 pipe throughput probe (no FMA: DMUL/DADD only, 8 independent chains
  * per thread).  Performs iters*16 DP ops per thread; sink must hold

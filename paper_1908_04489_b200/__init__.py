@@ -37,11 +37,12 @@ from .solver import (
     solve_many,
 )
 from .witsenhausen import Witsenhausen
+from .config5 import Inventory, ZeroDelay
 
 BACKEND = "b200"
 __version__ = "0.1.0"
 
-REGISTRY = {Witsenhausen.name: Witsenhausen}
+REGISTRY = {Witsenhausen.name: Witsenhausen, ZeroDelay.name: ZeroDelay, Inventory.name: Inventory}
 
 
 def make_problem(name: str, params: dict | None = None, grids=None):
@@ -66,7 +67,7 @@ def set_workers(n: int) -> int:
 __all__ = [
     "BACKEND", "ControllerSet", "Density", "Gaussian", "Grid", "LOCAL", "NumericError", "Problem",
     "REGISTRY", "RoundReport", "SampledController", "Sharding", "SolveResult", "SolverConfig", "Uniform",
-    "Witsenhausen", "adaptive_allocation", "eval_controller", "eval_controller_many", "from_process_group",
+    "Witsenhausen", "ZeroDelay", "Inventory", "adaptive_allocation", "eval_controller", "eval_controller_many", "from_process_group",
     "init_identity", "local_update_phase", "make_grid", "make_problem", "max_workers", "nearest_index",
     "nearest_indices", "newton_or_gradient_step", "node_window_bounds", "partial_exhaustion_phase", "pdf",
     "run_block", "set_workers", "solve", "solve_many", "trapezoid", "window_bounds", "window_indices", "__version__",

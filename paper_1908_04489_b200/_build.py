@@ -14,7 +14,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libucp_b200.so"
 SOURCES = [CSRC / "ucp_kernels.cu"]
-HEADERS = [CSRC / "ucp_libm.h", CSRC / "ucp_exp_data.h", PKG.parent / "include" / "ucp_b200.h"]
+HEADERS = [CSRC / "ucp_libm.h", CSRC / "ucp_exp_data.h", CSRC / "ucp_config5.cuh", PKG.parent / "include" / "ucp_b200.h"]
 
 NVCC_FLAGS = [
     "-O3",

@@ -1,0 +1,643 @@
+// Config 5 (PAPER.md's additional examples): the uniform-noise kernels and
+// the ZeroDelay / Inventory (M >= 1 stages) marginal costs, plus generic
+// device sweeps templated on a per-problem cost functor.  Included at the
+// end of ucp_kernels.cu (shares its workspace, error and launch plumbing).
+//
+// Same ref-order contract as the Witsenhausen path: every output is one
+// thread's serial loop in the reference's order with the reference's
+// association; parallelism spans independent outputs only.
+
+namespace {
+
+constexpr double kHugeEdge = 1.0e300;  // kernels.py:61 _HUGE
+
+// cell j spans [a + h(j - 1/2), a + h(j + 1/2)], end cells open (kernels.py:302-309)
+__device__ __forceinline__ long long cell_index(double x, double a, double h, int64_t d) {
+  long long j = (long long)ceil((x - a) / h - 0.5);
+  if (j < 0) j = 0;
+  if (j > d - 1) j = d - 1;
+  return j;
+}
+__device__ __forceinline__ double cell_left(long long j, double a, double h) {
+  return j > 0 ? a + h * ((double)j - 0.5) : -kHugeEdge;
+}
+__device__ __forceinline__ double cell_right(long long j, double a, double h, int64_t d) {
+  return j < d - 1 ? a + h * ((double)j + 0.5) : kHugeEdge;
+}
+
+// numpy.maximum(a, b) as this NumPy evaluates it (NaN in a wins, ties -> b)
+__device__ __forceinline__ double np_maximum(double a, double b) { return (a > b || a != a) ? a : b; }
+
+struct Mom3U {
+  double s0, s1, s2;
+};
+
+// kernels.py:495-525: overlap moments of v under U(x - rad, x + rad)
+__device__ __forceinline__ Mom3U unif_moments_at(double x, const double* __restrict__ v, double a, double h,
+                                                 int64_t d, double rad) {
+  const double xlo = x - rad, xhi = x + rad;
+  const long long jlo = cell_index(xlo, a, h, d), jhi = cell_index(xhi, a, h, d);
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  for (long long j = jlo; j <= jhi; ++j) {
+    const double lj = cell_left(j, a, h), rj = cell_right(j, a, h, d);
+    const double lo = xlo > lj ? xlo : lj;
+    const double hi = xhi < rj ? xhi : rj;
+    const double ov = hi - lo;
+    if (ov > 0.0) {
+      const double vj = __ldg(v + j);
+      acc0 += ov;
+      const double ovv = ov * vj;
+      acc1 += ovv;
+      acc2 += ovv * vj;
+    }
+  }
+  const double inv = 1.0 / (2.0 * rad);
+  Mom3U r;
+  r.s0 = acc0 * inv;
+  r.s1 = acc1 * inv;
+  r.s2 = acc2 * inv;
+  return r;
+}
+
+// kernels.py:532-555: E[g] under U(x - rad, x + rad)
+__device__ __forceinline__ double unif_ball_at(double x, const double* __restrict__ g, double a, double h, int64_t d,
+                                               double rad) {
+  const double xlo = x - rad, xhi = x + rad;
+  const long long jlo = cell_index(xlo, a, h, d), jhi = cell_index(xhi, a, h, d);
+  double acc = 0.0;
+  for (long long j = jlo; j <= jhi; ++j) {
+    const double lj = cell_left(j, a, h), rj = cell_right(j, a, h, d);
+    const double lo = xlo > lj ? xlo : lj;
+    const double hi = xhi < rj ? xhi : rj;
+    const double ov = hi - lo;
+    if (ov > 0.0) acc += ov * __ldg(g + j);
+  }
+  return acc * (1.0 / (2.0 * rad));
+}
+
+__global__ void k_unif_moments_grid(const double* __restrict__ x, int64_t n, const double* __restrict__ v, double a,
+                                    double h, int64_t d, double rad, double* s0, double* s1, double* s2) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  Mom3U r = unif_moments_at(x[t], v, a, h, d, rad);
+  s0[t] = r.s0;
+  s1[t] = r.s1;
+  s2[t] = r.s2;
+}
+
+__global__ void k_unif_ball_sum(const double* __restrict__ x, const double* __restrict__ xadd, int64_t n,
+                                const double* __restrict__ g, double a, double h, int64_t d, double rad,
+                                double* out) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const double xt = xadd ? x[t] + xadd[t] : x[t];
+  out[t] = unif_ball_at(xt, g, a, h, d, rad);
+}
+
+// kernels.py:558-577, one thread per output node j, centres in ascending i.
+// masses = mscale * f (the reference forms g.spacing * f as an array first:
+// the same single rounding per element), centres = cpts + cu (points + u).
+__global__ void k_unif_propagate(const double* __restrict__ f, double mscale, const double* __restrict__ cpts,
+                                 const double* __restrict__ cu, int64_t n, double a, double h, int64_t d,
+                                 double rad, double* out) {
+  __shared__ double sm[256], sc[256];
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const double lj = j < d ? cell_left(j, a, h) : 0.0, rj = j < d ? cell_right(j, a, h, d) : 0.0;
+  double acc = 0.0;
+  for (int64_t base = 0; base < n; base += 256) {
+    const int cnt = (int)(n - base < 256 ? n - base : 256);
+    __syncthreads();
+    for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
+      sm[r] = mscale == 1.0 ? f[base + r] : mscale * f[base + r];
+      sc[r] = cu ? cpts[base + r] + cu[base + r] : cpts[base + r];
+    }
+    __syncthreads();
+    if (j < d) {
+      for (int r = 0; r < cnt; ++r) {
+        double lo = sc[r] - rad, hi = sc[r] + rad;
+        if (lo < lj) lo = lj;
+        if (hi > rj) hi = rj;
+        const double ov = hi - lo;
+        if (ov > 0.0) acc += sm[r] * ov;
+      }
+    }
+  }
+  if (j < d) out[j] = acc * (1.0 / ((2.0 * rad) * h));
+}
+
+// kernels.py:580-615, one thread per query, support points in ascending i
+__global__ void k_unif_moments_points(const double* __restrict__ y, int64_t n, const double* __restrict__ centers,
+                                      const double* __restrict__ w, const double* __restrict__ vals, int64_t m,
+                                      double a, double h, int64_t d, double rad, double* m0, double* m1, double* m2) {
+  __shared__ double sc[256], sw[256], sv[256];
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = t < n;
+  const long long j = cell_index(active ? y[t] : 0.0, a, h, d);
+  const double lj = cell_left(j, a, h), rj = cell_right(j, a, h, d);
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  for (int64_t base = 0; base < m; base += 256) {
+    const int cnt = (int)(m - base < 256 ? m - base : 256);
+    __syncthreads();
+    for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
+      sc[r] = centers[base + r];
+      sw[r] = w[base + r];
+      sv[r] = vals[base + r];
+    }
+    __syncthreads();
+    if (active) {
+      for (int r = 0; r < cnt; ++r) {
+        double lo = sc[r] - rad, hi = sc[r] + rad;
+        if (lo < lj) lo = lj;
+        if (hi > rj) hi = rj;
+        const double ov = hi - lo;
+        if (ov > 0.0) {
+          const double wov = sw[r] * ov, vi = sv[r];
+          acc0 += wov;
+          const double wv = wov * vi;
+          acc1 += wv;
+          acc2 += wv * vi;
+        }
+      }
+    }
+  }
+  if (active) {
+    const double inv = 1.0 / ((2.0 * rad) * h);
+    m0[t] = acc0 * inv;
+    m1[t] = acc1 * inv;
+    m2[t] = acc2 * inv;
+  }
+}
+
+// ------------------------------------------------------- cost functors
+// zero_delay.py:69-76: C0(u, y_i) = f0_i (pw u^2 + E[(y - u1(x1))^2]), x1 = u + w
+struct ZdCost0 {
+  const double* y0;
+  const double* f0;
+  const double* v1;
+  double a1, h1, pw;
+  int64_t d1;
+  __device__ __forceinline__ double operator()(double u, int64_t i) const {
+    const Mom3U s = unif_moments_at(u, v1, a1, h1, d1, 1.0);
+    const double y = y0[i];
+    const double distortion = (((s.s0 * y) * y) - ((2.0 * s.s1) * y)) + s.s2;
+    return f0[i] * (((pw * u) * u) + distortion);
+  }
+};
+
+// any stage whose cost is quadratic in u with per-point moments (ZeroDelay m=1)
+struct QuadCost {
+  const double* A;
+  const double* B;
+  const double* C;
+  int64_t begin;
+  __device__ __forceinline__ double operator()(double u, int64_t i) const {
+    const int64_t k = i - begin;
+    return quad_in_u(A[k], B[k], C[k], u);
+  }
+};
+
+// inventory.py:138-150: f_m(nearest(y)) * (c u + E[g_{m+1}(y + u - w)])
+struct InvCost {
+  const double* ym;
+  const double* fm;
+  const double* gnext;
+  double am, hm, an, hn, oc;
+  int64_t dm, dn;
+  __device__ __forceinline__ double operator()(double u, int64_t i) const {
+    const double y = ym[i];
+    const double expect = unif_ball_at(y + u, gnext, an, hn, dn, 1.0);
+    const double weight = fm[cell_index(y, am, hm, dm)];
+    return weight * ((oc * u) + expect);
+  }
+};
+
+__device__ __forceinline__ double project_value(int kind, double v) { return kind == 1 ? np_maximum(v, 0.0) : v; }
+
+// solver.py:179-203 for any cost functor; h floor = the problem's widened
+// probe (zero_delay.py:56-65, inventory.py:131-136), project per problem.
+template <class Cost>
+__global__ void k_gen_local(Cost cost, const double* __restrict__ u, ucp_local_params lp, double h_floor,
+                            int project_kind, int64_t begin, int64_t n, double* out, int64_t* err) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t i = begin + t;
+  const double ui = u[i];
+  double hh = lp.fd_step * (1.0 + fabs(ui));
+  if (h_floor > 0.0) hh = np_maximum(hh, h_floor);
+  const double up = cost(ui + hh, i), mid = cost(ui, i), dn = cost(ui - hh, i);
+  const double c1 = (up - dn) / (2.0 * hh);
+  const double c2 = ((up - 2.0 * mid) + dn) / (hh * hh);
+  if (!(finite(c1) && finite(c2))) {
+    flag_min(err, i);
+    out[i] = ui;
+    return;
+  }
+  const double stepped = project_value(project_kind, newton_step(ui, c1, c2, lp));
+  const double cost_new = cost(stepped, i);
+  if (!(finite(mid) && finite(cost_new))) flag_min(err + 1, i);
+  const double r = cost_new <= mid ? stepped : ui;
+  if (!finite(r)) flag_min(err + 2, i);
+  out[i] = r;
+}
+
+// solver.py:206-223: first strict argmin over the window, kept in registers
+template <class Cost>
+__global__ void k_gen_exhaust(Cost cost, const double* __restrict__ u, const int64_t* __restrict__ lo,
+                              const int64_t* __restrict__ hi, int project_kind, int64_t begin, int64_t n,
+                              double* out, int64_t* err) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t i = begin + t;
+  double bu = u[lo[i]];
+  double bv = cost(bu, i);
+  bool ok = finite(bv);
+  for (int64_t j = lo[i] + 1; j <= hi[i]; ++j) {
+    const double uj = u[j];
+    const double c = cost(uj, i);
+    ok = ok && finite(c);
+    if (c < bv) {
+      bv = c;
+      bu = uj;
+    }
+  }
+  if (!ok) flag_min(err, i);
+  out[i] = project_value(project_kind, bu);
+}
+
+template <class Cost>
+__global__ void k_gen_terms(Cost cost, const double* __restrict__ u0, int64_t begin, int64_t end, double* terms,
+                            int64_t* err) {
+  const int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= end) return;
+  const double c = cost(u0[i], i);
+  if (!finite(c)) flag_min(err, i);
+  terms[i] = c;
+}
+
+// marginal_cost_segmented over a flat candidate list; the cost functor is
+// built on per-SEGMENT arrays (observation y, density) and indexed by segment
+template <class Cost>
+__global__ void k_gen_segmented(Cost cost, const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
+                                int64_t nseg, double* out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = offsets[nseg];
+  if (c >= n) return;
+  int64_t lo = 0, hi = nseg;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (offsets[mid] <= c) lo = mid; else hi = mid;
+  }
+  out[c] = cost(u_flat[c], lo);
+}
+
+// Inventory: gs[mm] = gamma(pts) + (c u + E[gs[mm+1](pts + u - w)]) (inventory.py:84-94);
+// gs[M] = gamma(terminal points) when gnext == nullptr.
+__global__ void k_inv_downstream(const double* __restrict__ pts, const double* __restrict__ u, int64_t n,
+                                 const double* __restrict__ gnext, double an, double hn, int64_t dn, double oc,
+                                 int quadratic, double hr, double br, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = pts[i];
+  const double gam = quadratic ? x * x : hr * np_maximum(x, 0.0) + br * np_maximum(-x, 0.0);
+  if (!gnext) {
+    out[i] = gam;
+    return;
+  }
+  const double ui = u[i];
+  const double expect = unif_ball_at(x + ui, gnext, an, hn, dn, 1.0);
+  out[i] = gam + ((oc * ui) + expect);
+}
+
+template <class Cost>
+int launch_gen_local(const Cost& c, const double* u, const ucp_local_params* lp, double h_floor, int project_kind,
+                     int64_t begin, int64_t n, double* out, int64_t* err, cudaStream_t st) {
+  k_gen_local<Cost><<<nblocks(n, 128), 128, 0, st>>>(c, u, *lp, h_floor, project_kind, begin, n, out, err);
+  UCP_LAUNCHED("k_gen_local");
+  return UCP_OK;
+}
+
+template <class Cost>
+int launch_gen_exhaust(const Cost& c, const double* u, const int64_t* lo, const int64_t* hi, int project_kind,
+                       int64_t begin, int64_t n, double* out, int64_t* err, cudaStream_t st) {
+  k_gen_exhaust<Cost><<<nblocks(n, 128), 128, 0, st>>>(c, u, lo, hi, project_kind, begin, n, out, err);
+  UCP_LAUNCHED("k_gen_exhaust");
+  return UCP_OK;
+}
+
+int check_zd(const ucp_zd_problem* P) {
+  if (!P || !P->y0 || !P->y1 || !P->f0 || !P->fw0) return arg_fail("null zero-delay problem pointer");
+  if (P->d0 < 2 || P->d1 < 2) return arg_fail("grid.d must be at least 2");
+  return UCP_OK;
+}
+
+ZdCost0 zd_cost0(const ucp_zd_problem* P, const double* u1) {
+  ZdCost0 c;
+  c.y0 = P->y0;
+  c.f0 = P->f0;
+  c.v1 = u1;
+  c.a1 = P->a1;
+  c.h1 = P->h1;
+  c.d1 = P->d1;
+  c.pw = P->power_weight;
+  return c;
+}
+
+// zero_delay.py:77-83: decoder moments at queries y (centres u0, weights fw0, values y0)
+int zd_moments(const ucp_zd_problem* P, const double* u0, const double* yq, int64_t nq, ucp_workspace* ws,
+               cudaStream_t st, QuadCost* q) {
+  void* pm;
+  int rc;
+  if ((rc = ws_get(ws, WS_MOM, sizeof(double) * 3 * (size_t)nq, &pm))) return rc;
+  double* m0 = (double*)pm;
+  k_unif_moments_points<<<nblocks(nq, 128), 128, 0, st>>>(yq, nq, u0, P->fw0, P->y0, P->d0, P->a1, P->h1, P->d1,
+                                                          1.0, m0, m0 + nq, m0 + 2 * nq);
+  UCP_LAUNCHED("k_unif_moments_points");
+  q->A = m0;
+  q->B = m0 + nq;
+  q->C = m0 + 2 * nq;
+  return UCP_OK;
+}
+
+// ----------------------------------------------------------- inventory
+int check_inv(const ucp_inv_problem* P, const double* const* u) {
+  if (!P || P->stages < 1 || P->stages > UCP_INV_MAX_STAGES) return arg_fail("inventory: bad stage count");
+  for (int m = 0; m < P->stages; ++m) {
+    if (!P->pts[m] || P->d[m] < 2) return arg_fail("inventory: bad grid");
+    if (u && !u[m]) return arg_fail("inventory: null controller");
+  }
+  return UCP_OK;
+}
+
+inline int inv_state(const ucp_inv_problem* P, int mm) { return mm < P->stages - 1 ? mm : P->stages - 1; }
+
+// Stock density at stage m (inventory.py:96-110) into *out (device, d[m]).
+int inv_forward_density(const ucp_inv_problem* P, int m, const double* const* u, ucp_workspace* ws,
+                        cudaStream_t st, const double** out) {
+  void *pa, *pb, *pone;
+  int rc;
+  int64_t dmax = 0;
+  for (int k = 0; k < P->stages; ++k) dmax = P->d[k] > dmax ? P->d[k] : dmax;
+  if ((rc = ws_get(ws, WS_C5_F0, sizeof(double) * (size_t)dmax, &pa))) return rc;
+  if ((rc = ws_get(ws, WS_C5_F1, sizeof(double) * (size_t)dmax, &pb))) return rc;
+  if ((rc = ws_get(ws, WS_C5_ONE, sizeof(double) * 2, &pone))) return rc;
+  static const double one_zero[2] = {1.0, 0.0};
+  UCP_CHECK(cudaMemcpyAsync(pone, one_zero, sizeof one_zero, cudaMemcpyHostToDevice, st));
+  double* bufs[2] = {(double*)pa, (double*)pb};
+  const double* one = (const double*)pone;
+  // f = unif_propagate([1.0], [0.0], grid 0)
+  k_unif_propagate<<<nblocks(P->d[0], 128), 128, 0, st>>>(one, 1.0, one + 1, nullptr, 1, P->a[0], P->h[0], P->d[0],
+                                                           1.0, bufs[0]);
+  UCP_LAUNCHED("k_unif_propagate");
+  int cur = 0;
+  for (int mm = 0; mm < m; ++mm) {
+    // f = unif_propagate(h_mm * f, pts_mm + u_mm, grid mm+1)
+    k_unif_propagate<<<nblocks(P->d[mm + 1], 128), 128, 0, st>>>(bufs[cur], P->h[mm], P->pts[mm], u[mm], P->d[mm],
+                                                                 P->a[mm + 1], P->h[mm + 1], P->d[mm + 1], 1.0,
+                                                                 bufs[cur ^ 1]);
+    UCP_LAUNCHED("k_unif_propagate");
+    cur ^= 1;
+  }
+  *out = bufs[cur];
+  return UCP_OK;
+}
+
+// g_{m+1} on the stage-(m+1) state grid (inventory.py:78-94), backwards from M.
+int inv_downstream(const ucp_inv_problem* P, int m, const double* const* u, ucp_workspace* ws, cudaStream_t st,
+                   const double** out) {
+  void *pa, *pb;
+  int rc;
+  int64_t dmax = 0;
+  for (int k = 0; k < P->stages; ++k) dmax = P->d[k] > dmax ? P->d[k] : dmax;
+  if ((rc = ws_get(ws, WS_C5_G0, sizeof(double) * (size_t)dmax, &pa))) return rc;
+  if ((rc = ws_get(ws, WS_C5_G1, sizeof(double) * (size_t)dmax, &pb))) return rc;
+  double* bufs[2] = {(double*)pa, (double*)pb};
+  const int M = P->stages;
+  const int term = inv_state(P, M);
+  int cur = 0;
+  k_inv_downstream<<<nblocks(P->d[term], 128), 128, 0, st>>>(P->pts[term], nullptr, P->d[term], nullptr, 0.0, 0.0, 0,
+                                                             0.0, P->quadratic, P->holding_rate, P->backlog_rate,
+                                                             bufs[cur]);
+  UCP_LAUNCHED("k_inv_downstream");
+  for (int mm = M - 1; mm >= m + 1; --mm) {
+    const int nx = inv_state(P, mm + 1);
+    k_inv_downstream<<<nblocks(P->d[mm], 128), 128, 0, st>>>(P->pts[mm], u[mm], P->d[mm], bufs[cur], P->a[nx],
+                                                             P->h[nx], P->d[nx], P->order_cost, P->quadratic,
+                                                             P->holding_rate, P->backlog_rate, bufs[cur ^ 1]);
+    UCP_LAUNCHED("k_inv_downstream");
+    cur ^= 1;
+  }
+  *out = bufs[cur];
+  return UCP_OK;
+}
+
+int inv_cost(const ucp_inv_problem* P, int m, const double* const* u, ucp_workspace* ws, cudaStream_t st,
+             InvCost* c) {
+  int rc;
+  const double *fm, *gn;
+  if ((rc = inv_forward_density(P, m, u, ws, st, &fm))) return rc;
+  if ((rc = inv_downstream(P, m, u, ws, st, &gn))) return rc;
+  const int nx = inv_state(P, m + 1);
+  c->ym = P->pts[m];
+  c->fm = fm;
+  c->gnext = gn;
+  c->am = P->a[m];
+  c->hm = P->h[m];
+  c->dm = P->d[m];
+  c->an = P->a[nx];
+  c->hn = P->h[nx];
+  c->dn = P->d[nx];
+  c->oc = P->order_cost;
+  return UCP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ucp_unif_moments_grid(const double* x, int64_t n, const double* v, double a, double h, int64_t d, double rad,
+                          double* s0, double* s1, double* s2, void* stream) {
+  if (n < 0 || d < 2) return arg_fail("unif_moments_grid: bad sizes");
+  if (n == 0) return UCP_OK;
+  k_unif_moments_grid<<<nblocks(n, 128), 128, 0, as_stream(stream)>>>(x, n, v, a, h, d, rad, s0, s1, s2);
+  UCP_LAUNCHED("k_unif_moments_grid");
+  return UCP_OK;
+}
+
+int ucp_unif_ball_sum(const double* x, int64_t n, const double* g, double a, double h, int64_t d, double rad,
+                      double* out, void* stream) {
+  if (n < 0 || d < 2) return arg_fail("unif_ball_sum: bad sizes");
+  if (n == 0) return UCP_OK;
+  k_unif_ball_sum<<<nblocks(n, 128), 128, 0, as_stream(stream)>>>(x, nullptr, n, g, a, h, d, rad, out);
+  UCP_LAUNCHED("k_unif_ball_sum");
+  return UCP_OK;
+}
+
+int ucp_unif_propagate(const double* masses, const double* centers, int64_t n, double a, double h, int64_t d,
+                       double rad, double* out, void* stream) {
+  if (n < 0 || d < 2) return arg_fail("unif_propagate: bad sizes");
+  k_unif_propagate<<<nblocks(d, 128), 128, 0, as_stream(stream)>>>(masses, 1.0, centers, nullptr, n, a, h, d, rad,
+                                                                   out);
+  UCP_LAUNCHED("k_unif_propagate");
+  return UCP_OK;
+}
+
+int ucp_unif_moments_points(const double* y, int64_t n, const double* centers, const double* w, const double* vals,
+                            int64_t m, double a, double h, int64_t d, double rad, double* m0, double* m1,
+                            double* m2, void* stream) {
+  if (n < 0 || m < 0 || d < 2) return arg_fail("unif_moments_points: bad sizes");
+  if (n == 0) return UCP_OK;
+  k_unif_moments_points<<<nblocks(n, 128), 128, 0, as_stream(stream)>>>(y, n, centers, w, vals, m, a, h, d, rad, m0,
+                                                                        m1, m2);
+  UCP_LAUNCHED("k_unif_moments_points");
+  return UCP_OK;
+}
+
+// ---------------------------------------------------------------- ZeroDelay
+int ucp_zd_cost(const ucp_zd_problem* P, int stage, const double* u0, const double* u1, const double* u_flat,
+                int64_t n_cand, const int64_t* offsets, const double* y_seg, const double* f0_seg, int64_t nseg,
+                double* out, ucp_workspace* ws, void* stream) {
+  int rc = check_zd(P);
+  if (rc) return rc;
+  if (stage < 0 || stage > 1) return arg_fail("stage index out of range for zero_delay");
+  if (nseg <= 0 || n_cand <= 0) return UCP_OK;
+  cudaStream_t st = as_stream(stream);
+  if (stage == 0) {
+    ZdCost0 c = zd_cost0(P, u1);
+    c.y0 = y_seg;  // per-segment observation and density
+    c.f0 = f0_seg;
+    k_gen_segmented<ZdCost0><<<nblocks(n_cand, 128), 128, 0, st>>>(c, u_flat, offsets, nseg, out);
+    UCP_LAUNCHED("k_gen_segmented");
+    return UCP_OK;
+  }
+  QuadCost q;
+  if ((rc = zd_moments(P, u0, y_seg, nseg, ws, st, &q))) return rc;
+  q.begin = 0;
+  k_gen_segmented<QuadCost><<<nblocks(n_cand, 128), 128, 0, st>>>(q, u_flat, offsets, nseg, out);
+  UCP_LAUNCHED("k_gen_segmented");
+  return UCP_OK;
+}
+
+int ucp_zd_local_update(const ucp_zd_problem* P, int stage, const double* u0, const double* u1,
+                        const ucp_local_params* lp, int64_t begin, int64_t end, double* out, int64_t* err,
+                        ucp_workspace* ws, void* stream) {
+  int rc = check_zd(P);
+  if (rc) return rc;
+  if (stage < 0 || stage > 1) return arg_fail("stage index out of range for zero_delay");
+  const int64_t d = stage == 0 ? P->d0 : P->d1;
+  if (!lp || !err || begin < 0 || end > d || begin > end) return arg_fail("zd_local_update: bad arguments");
+  const int64_t n = end - begin;
+  if (n == 0) return UCP_OK;
+  cudaStream_t st = as_stream(stream);
+  const double floor = P->h1;  // zero_delay.py:56-65: probe >= one decoder cell, both stages
+  if (stage == 0) return launch_gen_local(zd_cost0(P, u1), u0, lp, floor, 0, begin, n, out, err, st);
+  QuadCost q;
+  if ((rc = zd_moments(P, u0, P->y1 + begin, n, ws, st, &q))) return rc;
+  q.begin = begin;
+  return launch_gen_local(q, u1, lp, floor, 0, begin, n, out, err, st);
+}
+
+int ucp_zd_exhaustion(const ucp_zd_problem* P, int stage, const double* u0, const double* u1, const int64_t* win_lo,
+                      const int64_t* win_hi, int64_t begin, int64_t end, double* out, int64_t* err,
+                      ucp_workspace* ws, void* stream) {
+  int rc = check_zd(P);
+  if (rc) return rc;
+  if (stage < 0 || stage > 1) return arg_fail("stage index out of range for zero_delay");
+  const int64_t d = stage == 0 ? P->d0 : P->d1;
+  if (!err || !win_lo || !win_hi || begin < 0 || end > d || begin > end) return arg_fail("zd_exhaustion: bad arguments");
+  const int64_t n = end - begin;
+  if (n == 0) return UCP_OK;
+  cudaStream_t st = as_stream(stream);
+  if (stage == 0) return launch_gen_exhaust(zd_cost0(P, u1), u0, win_lo, win_hi, 0, begin, n, out, err, st);
+  QuadCost q;
+  if ((rc = zd_moments(P, u0, P->y1 + begin, n, ws, st, &q))) return rc;
+  q.begin = begin;
+  return launch_gen_exhaust(q, u1, win_lo, win_hi, 0, begin, n, out, err, st);
+}
+
+int ucp_zd_objective_terms(const ucp_zd_problem* P, const double* u0, const double* u1, int64_t begin, int64_t end,
+                           double* terms, int64_t* err, void* stream) {
+  int rc = check_zd(P);
+  if (rc) return rc;
+  if (begin < 0 || end > P->d0 || begin > end) return arg_fail("zd_objective_terms: bad shard");
+  if (end == begin) return UCP_OK;
+  k_gen_terms<ZdCost0><<<nblocks(end - begin, 128), 128, 0, as_stream(stream)>>>(zd_cost0(P, u1), u0, begin, end,
+                                                                                 terms, err);
+  UCP_LAUNCHED("k_gen_terms");
+  return UCP_OK;
+}
+
+// ---------------------------------------------------------------- Inventory
+int ucp_inv_cost(const ucp_inv_problem* P, int stage, const double* const* u, const double* u_flat, int64_t n_cand,
+                 const int64_t* offsets, const double* y_seg, int64_t nseg, double* out, ucp_workspace* ws,
+                 void* stream) {
+  int rc = check_inv(P, u);
+  if (rc) return rc;
+  if (stage < 0 || stage >= P->stages) return arg_fail("stage index out of range for inventory");
+  if (nseg <= 0 || n_cand <= 0) return UCP_OK;
+  cudaStream_t st = as_stream(stream);
+  InvCost c;
+  if ((rc = inv_cost(P, stage, u, ws, st, &c))) return rc;
+  c.ym = y_seg;  // per-segment observation; weight via its nearest grid cell
+  k_gen_segmented<InvCost><<<nblocks(n_cand, 128), 128, 0, st>>>(c, u_flat, offsets, nseg, out);
+  UCP_LAUNCHED("k_gen_segmented");
+  return UCP_OK;
+}
+
+int ucp_inv_local_update(const ucp_inv_problem* P, int stage, const double* const* u, const ucp_local_params* lp,
+                         int64_t begin, int64_t end, double* out, int64_t* err, ucp_workspace* ws, void* stream) {
+  int rc = check_inv(P, u);
+  if (rc) return rc;
+  if (stage < 0 || stage >= P->stages) return arg_fail("stage index out of range for inventory");
+  if (!lp || !err || begin < 0 || end > P->d[stage] || begin > end) return arg_fail("inv_local_update: bad arguments");
+  const int64_t n = end - begin;
+  if (n == 0) return UCP_OK;
+  cudaStream_t st = as_stream(stream);
+  InvCost c;
+  if ((rc = inv_cost(P, stage, u, ws, st, &c))) return rc;
+  const double floor = P->h[inv_state(P, stage + 1)];  // inventory.py:131-136
+  return launch_gen_local(c, u[stage], lp, floor, 1, begin, n, out, err, st);
+}
+
+int ucp_inv_exhaustion(const ucp_inv_problem* P, int stage, const double* const* u, const int64_t* win_lo,
+                       const int64_t* win_hi, int64_t begin, int64_t end, double* out, int64_t* err,
+                       ucp_workspace* ws, void* stream) {
+  int rc = check_inv(P, u);
+  if (rc) return rc;
+  if (stage < 0 || stage >= P->stages) return arg_fail("stage index out of range for inventory");
+  if (!err || !win_lo || !win_hi || begin < 0 || end > P->d[stage] || begin > end)
+    return arg_fail("inv_exhaustion: bad arguments");
+  const int64_t n = end - begin;
+  if (n == 0) return UCP_OK;
+  cudaStream_t st = as_stream(stream);
+  InvCost c;
+  if ((rc = inv_cost(P, stage, u, ws, st, &c))) return rc;
+  return launch_gen_exhaust(c, u[stage], win_lo, win_hi, 1, begin, n, out, err, st);
+}
+
+int ucp_inv_objective_terms(const ucp_inv_problem* P, const double* const* u, int64_t begin, int64_t end,
+                            double* terms, int64_t* err, ucp_workspace* ws, void* stream) {
+  int rc = check_inv(P, u);
+  if (rc) return rc;
+  if (begin < 0 || end > P->d[0] || begin > end) return arg_fail("inv_objective_terms: bad shard");
+  if (end == begin) return UCP_OK;
+  cudaStream_t st = as_stream(stream);
+  InvCost c;
+  if ((rc = inv_cost(P, 0, u, ws, st, &c))) return rc;
+  k_gen_terms<InvCost><<<nblocks(end - begin, 128), 128, 0, st>>>(c, u[0], begin, end, terms, err);
+  UCP_LAUNCHED("k_gen_terms");
+  return UCP_OK;
+}
+
+int ucp_inv_forward_density(const ucp_inv_problem* P, int stage, const double* const* u, double* out,
+                            ucp_workspace* ws, void* stream) {
+  int rc = check_inv(P, u);
+  if (rc) return rc;
+  if (stage < 0 || stage >= P->stages) return arg_fail("stage index out of range for inventory");
+  const double* f;
+  cudaStream_t st = as_stream(stream);
+  if ((rc = inv_forward_density(P, stage, u, ws, st, &f))) return rc;
+  UCP_CHECK(cudaMemcpyAsync(out, f, sizeof(double) * (size_t)P->d[stage], cudaMemcpyDeviceToDevice, st));
+  return UCP_OK;
+}
+
+}  // extern "C"

@@ -816,7 +816,11 @@ struct ucp_workspace {
 };
 
 namespace {
-enum { WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS, WS_PAIRS, WS_NSLOTS };
+enum {
+  WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS, WS_PAIRS,
+  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_NSLOTS
+};
+static_assert(WS_NSLOTS <= 16, "workspace slots");
 // two-phase moments when the query set cannot fill the GPU with the direct kernel
 constexpr int64_t kTwoPhaseMaxQueries = 8192;
 constexpr int64_t kTwoPhaseMaxPairs = (int64_t)1 << 25;  // 256 MiB of pre-weights
@@ -1198,3 +1202,5 @@ int ucp_fp64_probe(int blocks, int threads, int iters, double* sink, void* strea
 }
 
 }  // extern "C"
+
+#include "ucp_config5.cuh"

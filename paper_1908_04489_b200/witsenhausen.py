@@ -24,77 +24,10 @@ from ._device import F64, I64, ptr, require_cuda, stream_ptr, to_device_f64, to_
 from .distributed import LOCAL, Sharding
 from .grids import ControllerSet, node_window_bounds
 from .numerics import Gaussian, pdf
+from .device_problem import NO_ERROR, ErrorLog
 from .problem import NumericError, Problem
 
 __all__ = ["Witsenhausen"]
-
-NO_ERROR = _lib.NO_ERROR
-
-
-class _ErrorLog:
-    """Device-side failure slots, one row of 3 int64 per phase, read lazily.
-
-    A phase never stalls the stream to look for non-finite values: it
-    atomicMin's the first offending grid point into its row, and the host
-    reads all pending rows at the next synchronisation point (the objective,
-    or the end of the solve).  The first phase (in execution order) with a
-    failure raises exactly the exception the reference raises at that phase;
-    work issued after it is discarded with the exception.
-    """
-
-    def __init__(self, device, problem, capacity: int = 1024):
-        self.device = device
-        self.problem = problem
-        self.rows = torch.full((capacity, 3), NO_ERROR, dtype=I64, device=device)
-        self.meta: list[tuple] = []
-
-    def slot(self, kind: str, stage: int, sharding: Sharding) -> torch.Tensor:
-        if len(self.meta) == self.rows.shape[0]:
-            self.flush(sharding)
-        row = self.rows[len(self.meta)]
-        self.meta.append((kind, stage))
-        return row
-
-    def slots(self, metas: list, sharding: Sharding) -> torch.Tensor:
-        """Contiguous rows for a run of phases (one native block call)."""
-        need = len(metas)
-        if len(self.meta) + need > self.rows.shape[0]:
-            self.flush(sharding)
-            if need > self.rows.shape[0]:
-                self.rows = torch.full((need, 3), NO_ERROR, dtype=I64, device=self.device)
-        start = len(self.meta)
-        self.meta.extend(metas)
-        return self.rows[start:start + need]
-
-    def flush(self, sharding: Sharding) -> None:
-        n = len(self.meta)
-        if n == 0:
-            return
-        rows = self.rows[:n]
-        sharding.allreduce_min_(rows)
-        host = rows.cpu().numpy()
-        rows.fill_(NO_ERROR)
-        meta, self.meta = self.meta, []
-        for (kind, m), row in zip(meta, host):
-            if (row != NO_ERROR).any():
-                raise _phase_error(self.problem, kind, m, row)
-
-
-def _phase_error(problem, kind, m, row):
-    name = problem.name if problem is not None else "witsenhausen"
-    pts = problem.grids[m].points if problem is not None else None
-    phase = {"local": "local-update", "exhaustion": "partial-exhaustion"}[kind]
-    for slot in range(3 if kind == "local" else 1):
-        i = int(row[slot])
-        if i == NO_ERROR:
-            continue
-        if slot == 2:  # grids.py: SampledController rejects non-finite values
-            return ValueError(f"controller value at grid point {i} is not finite")
-        y = pts[i] if pts is not None else float("nan")
-        return NumericError(
-            f"{name}: non-finite marginal cost in {phase} phase at stage {m}, grid point {i} (y={y!r})")
-    raise AssertionError("no failure in row")
-
 
 class _WcDevice:
     """Device-resident constants, ABI structs and scratch of one Witsenhausen problem."""
@@ -112,7 +45,7 @@ class _WcDevice:
         ws = ctypes.c_void_p()
         _lib.call("ucp_workspace_create", ctypes.byref(ws))
         self.ws = ws
-        self.errors = _ErrorLog(self.device, prob)
+        self.errors = ErrorLog(self.device, prob)
         self.windows: dict = {}
 
     def __del__(self):

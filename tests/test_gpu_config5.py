@@ -1,0 +1,106 @@
+"""Config 5 on the device: ZeroDelay and Inventory (M = 1, 2, 3) vs the
+reference's goldens, and the uniform-noise kernels vs the oracle, bitwise."""
+import numpy as np
+import pytest
+import torch
+
+from parity_util import assert_bitwise
+from test_oracle_config5 import FIXTURES, oracle_problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1908_04489_b200 as P
+
+    assert torch.cuda.is_available()
+    return P
+
+
+def device_problem(P, g):
+    specs = [tuple(float(v) if k < 2 else int(v) for k, v in enumerate(row)) for row in g["specs"]]
+    if "pw" in g:
+        prob = P.ZeroDelay(power_weight=float(g["pw"]), grids=specs)
+        prob._override_host_constants(g["f0"], g["fw0"])
+        return prob
+    return P.Inventory(stages=int(g["stages"]), stage_cost=str(g["stage_cost"]),
+                       order_cost=float(g["order_cost"]) if "order_cost" in g else 0.1, grids=specs)
+
+
+def _U(P, prob, us):
+    return P.ControllerSet(tuple(P.SampledController(g, u) for g, u in zip(prob.grids, us)))
+
+
+@pytest.mark.parametrize("tag", FIXTURES)
+def test_config5_device_vs_golden(P, golden, tag):
+    g = golden(tag)
+    prob = device_problem(P, g)
+    cfg = P.SolverConfig()
+    for name in ("ident", "pert0", "pert1"):
+        U = _U(P, prob, [g[f"{name}_u{m}"] for m in range(prob.M)])
+        assert_bitwise(prob.objective(U), g[f"{name}_J"], f"{name} J")
+        for m in range(prob.M):
+            pts = prob.grids[m].points
+            assert_bitwise(prob.marginal_cost_batch(m, U.values(m), pts, U), g[f"{name}_c{m}"], f"{name} C{m}")
+            assert_bitwise(P.local_update_phase(prob, m, U, cfg), g[f"{name}_lu{m}"], f"{name} LU{m}")
+            assert_bitwise(P.partial_exhaustion_phase(prob, m, U, cfg), g[f"{name}_ex{m}"], f"{name} EX{m}")
+        V = P.run_block(prob, U, cfg, 1, "local")
+        V = P.run_block(prob, V, cfg, 1, "exhaustion")
+        for m in range(prob.M):
+            assert_bitwise(V.values(m), g[f"{name}_it_u{m}"], f"{name} it u{m}")
+        assert_bitwise(prob.objective(V), g[f"{name}_it_J"], f"{name} it J")
+    if "solve_J" in g:
+        res = P.solve(prob, cfg)
+        assert res.termination == str(g["solve_termination"])
+        assert_bitwise(np.array([r.objective for r in res.rounds]), g["solve_rounds"][:, 1], "per-round J")
+        assert_bitwise(res.final_objective, g["solve_J"], "J")
+        for m in range(prob.M):
+            assert_bitwise(res.controllers.values(m), g[f"solve_u{m}"], f"u{m}")
+
+
+def test_inventory_forward_density_vs_oracle(P, golden, oracle_mod):
+    g = golden("inv_m3")
+    prob = device_problem(P, g)
+    p = oracle_problem(oracle_mod, g)
+    us = [g[f"pert1_u{m}"] for m in range(3)]
+    U = _U(P, prob, us)
+    for m in range(3):
+        assert_bitwise(prob.forward_density(m, U), p.forward_density(m, us), f"f_{m}")
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_uniform_kernels_vs_oracle(P, oracle_mod, seed):
+    from paper_1908_04489_b200 import _lib, config5
+    from paper_1908_04489_b200._device import ptr, stream_ptr
+
+    config5._bind()
+    rng = np.random.default_rng(seed)
+    a, b, d = -4.0, 3.5, 257 + seed * 100
+    h = (b - a) / (d - 1)
+    v = rng.normal(0, 2, d)
+    x = np.concatenate([rng.uniform(a - 3, b + 3, 999), [a, b, a - 1.0, b + 1.0, 0.5 * (a + b)]])
+    dev = torch.device("cuda", 0)
+    T = lambda z: torch.from_numpy(np.ascontiguousarray(z, dtype=np.float64)).to(dev)  # noqa: E731
+    s = stream_ptr(dev)
+    for rad in (1.0, 0.37):
+        outs = [torch.empty(x.size, dtype=torch.float64, device=dev) for _ in range(3)]
+        _lib.call("ucp_unif_moments_grid", ptr(T(x)), x.size, ptr(T(v)), a, h, d, rad, *(ptr(o) for o in outs), s)
+        want = oracle_mod.unif_moments_grid(x, v, a, h, d, rad)
+        for k in range(3):
+            assert_bitwise(outs[k].cpu().numpy(), want[k], f"unif_moments_grid s{k}")
+        out = torch.empty(x.size, dtype=torch.float64, device=dev)
+        _lib.call("ucp_unif_ball_sum", ptr(T(x)), x.size, ptr(T(v)), a, h, d, rad, ptr(out), s)
+        assert_bitwise(out.cpu().numpy(), oracle_mod.unif_ball_sum(x, v, a, h, d, rad), "ball_sum")
+        masses = np.abs(rng.normal(0, 1, x.size))
+        out = torch.empty(d, dtype=torch.float64, device=dev)
+        _lib.call("ucp_unif_propagate", ptr(T(masses)), ptr(T(x)), x.size, a, h, d, rad, ptr(out), s)
+        assert_bitwise(out.cpu().numpy(), oracle_mod.unif_propagate(masses, x, a, h, d, rad), "propagate")
+        w, vals = np.abs(rng.normal(0, 1, x.size)), rng.normal(0, 3, x.size)
+        q = rng.uniform(a - 1, b + 1, 500)
+        outs = [torch.empty(q.size, dtype=torch.float64, device=dev) for _ in range(3)]
+        _lib.call("ucp_unif_moments_points", ptr(T(q)), q.size, ptr(T(x)), ptr(T(w)), ptr(T(vals)), x.size, a, h, d,
+                  rad, *(ptr(o) for o in outs), s)
+        want = oracle_mod.unif_moments_points(q, x, w, vals, a, h, d, rad)
+        for k in range(3):
+            assert_bitwise(outs[k].cpu().numpy(), want[k], f"unif_moments_points m{k}")
