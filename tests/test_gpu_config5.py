@@ -81,7 +81,13 @@ def test_uniform_kernels_vs_oracle(P, oracle_mod, seed):
     v = rng.normal(0, 2, d)
     x = np.concatenate([rng.uniform(a - 3, b + 3, 999), [a, b, a - 1.0, b + 1.0, 0.5 * (a + b)]])
     dev = torch.device("cuda", 0)
-    T = lambda z: torch.from_numpy(np.ascontiguousarray(z, dtype=np.float64)).to(dev)  # noqa: E731
+    keep = []  # device copies must outlive the (asynchronous) calls that read them
+
+    def T(z):
+        t = torch.from_numpy(np.ascontiguousarray(z, dtype=np.float64)).to(dev)
+        keep.append(t)
+        return t
+
     s = stream_ptr(dev)
     for rad in (1.0, 0.37):
         outs = [torch.empty(x.size, dtype=torch.float64, device=dev) for _ in range(3)]
