@@ -177,8 +177,10 @@ int ucp_zd_cost(const ucp_zd_problem* P, int stage, const double* u0, const doub
 int ucp_zd_local_update(const ucp_zd_problem* P, int stage, const double* u0, const double* u1,
                         const ucp_local_params* lp, int64_t begin, int64_t end, double* out,
                         int64_t* err, ucp_workspace* ws, void* stream);
+/* wmax = max window width (hi - lo + 1) over the sweep */
 int ucp_zd_exhaustion(const ucp_zd_problem* P, int stage, const double* u0, const double* u1,
-                      const int64_t* win_lo, const int64_t* win_hi, int64_t begin, int64_t end,
+                      const int64_t* win_lo, const int64_t* win_hi, int64_t wmax, int64_t begin,
+                      int64_t end,
                       double* out, int64_t* err, ucp_workspace* ws, void* stream);
 int ucp_zd_objective_terms(const ucp_zd_problem* P, const double* u0, const double* u1,
                            int64_t begin, int64_t end, double* terms, int64_t* err, void* stream);
@@ -203,7 +205,8 @@ int ucp_inv_local_update(const ucp_inv_problem* P, int stage, const double* cons
                          const ucp_local_params* lp, int64_t begin, int64_t end, double* out,
                          int64_t* err, ucp_workspace* ws, void* stream);
 int ucp_inv_exhaustion(const ucp_inv_problem* P, int stage, const double* const* u,
-                       const int64_t* win_lo, const int64_t* win_hi, int64_t begin, int64_t end,
+                       const int64_t* win_lo, const int64_t* win_hi, int64_t wmax, int64_t begin,
+                       int64_t end,
                        double* out, int64_t* err, ucp_workspace* ws, void* stream);
 int ucp_inv_objective_terms(const ucp_inv_problem* P, const double* const* u, int64_t begin,
                             int64_t end, double* terms, int64_t* err, ucp_workspace* ws,

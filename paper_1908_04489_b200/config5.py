@@ -56,15 +56,15 @@ _SIGS = {
                                    c_vp, c_vp, c_vp]),
     "ucp_zd_local_update": (ctypes.c_int, [_PP(ZdProblemC), ctypes.c_int, c_vp, c_vp, _PP(_lib.LocalParams), c_i64,
                                            c_i64, c_vp, c_vp, c_vp, c_vp]),
-    "ucp_zd_exhaustion": (ctypes.c_int, [_PP(ZdProblemC), ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp,
-                                         c_vp, c_vp, c_vp]),
+    "ucp_zd_exhaustion": (ctypes.c_int, [_PP(ZdProblemC), ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64,
+                                         c_vp, c_vp, c_vp, c_vp]),
     "ucp_zd_objective_terms": (ctypes.c_int, [_PP(ZdProblemC), c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "ucp_inv_cost": (ctypes.c_int, [_PP(InvProblemC), ctypes.c_int, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp,
                                     c_vp, c_vp]),
     "ucp_inv_local_update": (ctypes.c_int, [_PP(InvProblemC), ctypes.c_int, c_vp, _PP(_lib.LocalParams), c_i64,
                                             c_i64, c_vp, c_vp, c_vp, c_vp]),
-    "ucp_inv_exhaustion": (ctypes.c_int, [_PP(InvProblemC), ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp,
-                                          c_vp, c_vp, c_vp]),
+    "ucp_inv_exhaustion": (ctypes.c_int, [_PP(InvProblemC), ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64,
+                                          c_vp, c_vp, c_vp, c_vp]),
     "ucp_inv_objective_terms": (ctypes.c_int, [_PP(InvProblemC), c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "ucp_inv_forward_density": (ctypes.c_int, [_PP(InvProblemC), ctypes.c_int, c_vp, c_vp, c_vp, c_vp]),
 }
@@ -117,7 +117,7 @@ class _DeviceSweeps:
             self._abi_local(m, ts, lp, begin, end, buf, err)
         else:
             lo, hi = D.window(self, m, cfg.radius_for(g))
-            self._abi_exhaustion(m, ts, lo, hi, begin, end, buf, err)
+            self._abi_exhaustion(m, ts, lo, hi, D.window_width(self, m, cfg.radius_for(g)), begin, end, buf, err)
         sharding.allgather_(buf)
         return buf[: g.d]
 
@@ -210,10 +210,10 @@ class ZeroDelay(_DeviceSweeps, Problem):
         _lib.call("ucp_zd_local_update", ctypes.byref(self._P), m, ptr(ts[0]), ptr(ts[1]), ctypes.byref(lp), begin,
                   end, ptr(buf), ptr(err), D.ws, D.stream)
 
-    def _abi_exhaustion(self, m, ts, lo, hi, begin, end, buf, err):
+    def _abi_exhaustion(self, m, ts, lo, hi, wmax, begin, end, buf, err):
         D = self._dev
-        _lib.call("ucp_zd_exhaustion", ctypes.byref(self._P), m, ptr(ts[0]), ptr(ts[1]), ptr(lo), ptr(hi), begin,
-                  end, ptr(buf), ptr(err), D.ws, D.stream)
+        _lib.call("ucp_zd_exhaustion", ctypes.byref(self._P), m, ptr(ts[0]), ptr(ts[1]), ptr(lo), ptr(hi), wmax,
+                  begin, end, ptr(buf), ptr(err), D.ws, D.stream)
 
     def _abi_terms(self, ts, begin, end, terms, err):
         _lib.call("ucp_zd_objective_terms", ctypes.byref(self._P), ptr(ts[0]), ptr(ts[1]), begin, end, ptr(terms),
@@ -293,10 +293,10 @@ class Inventory(_DeviceSweeps, Problem):
         _lib.call("ucp_inv_local_update", ctypes.byref(self._P), m, ctypes.cast(self._uarray(ts), c_vp),
                   ctypes.byref(lp), begin, end, ptr(buf), ptr(err), D.ws, D.stream)
 
-    def _abi_exhaustion(self, m, ts, lo, hi, begin, end, buf, err):
+    def _abi_exhaustion(self, m, ts, lo, hi, wmax, begin, end, buf, err):
         D = self._dev
         _lib.call("ucp_inv_exhaustion", ctypes.byref(self._P), m, ctypes.cast(self._uarray(ts), c_vp), ptr(lo),
-                  ptr(hi), begin, end, ptr(buf), ptr(err), D.ws, D.stream)
+                  ptr(hi), wmax, begin, end, ptr(buf), ptr(err), D.ws, D.stream)
 
     def _abi_terms(self, ts, begin, end, terms, err):
         D = self._dev

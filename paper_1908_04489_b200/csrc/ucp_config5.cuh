@@ -213,18 +213,36 @@ struct InvCost {
 
 __device__ __forceinline__ double project_value(int kind, double v) { return kind == 1 ? np_maximum(v, 0.0) : v; }
 
-// solver.py:179-203 for any cost functor; h floor = the problem's widened
-// probe (zero_delay.py:56-65, inventory.py:131-136), project per problem.
+// solver.py:179-203 for any cost functor, in two launches so small grids
+// still fill the GPU: (1) the three FD probes u+h, u, u-h of every point in
+// parallel (probe-major), (2) per point: derivatives, safeguarded step,
+// projection, cost_new and the monotone guard.  The h floor is the
+// problem's widened probe (zero_delay.py:56-65, inventory.py:131-136).
 template <class Cost>
-__global__ void k_gen_local(Cost cost, const double* __restrict__ u, ucp_local_params lp, double h_floor,
-                            int project_kind, int64_t begin, int64_t n, double* out, int64_t* err) {
+__global__ void k_gen_probe(Cost cost, const double* __restrict__ u, double fd_step, double h_floor, int64_t begin,
+                            int64_t n, double* cost3) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 3 * n) return;
+  const int p = (int)(t / n);
+  const int64_t i = begin + (t - (int64_t)p * n);
+  const double ui = u[i];
+  double hh = fd_step * (1.0 + fabs(ui));
+  if (h_floor > 0.0) hh = np_maximum(hh, h_floor);
+  const double uu = p == 0 ? ui + hh : (p == 1 ? ui : ui - hh);
+  cost3[t] = cost(uu, i);
+}
+
+template <class Cost>
+__global__ void k_gen_finish(Cost cost, const double* __restrict__ u, ucp_local_params lp, double h_floor,
+                             int project_kind, int64_t begin, int64_t n, const double* __restrict__ cost3,
+                             double* out, int64_t* err) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int64_t i = begin + t;
   const double ui = u[i];
   double hh = lp.fd_step * (1.0 + fabs(ui));
   if (h_floor > 0.0) hh = np_maximum(hh, h_floor);
-  const double up = cost(ui + hh, i), mid = cost(ui, i), dn = cost(ui - hh, i);
+  const double up = cost3[t], mid = cost3[n + t], dn = cost3[2 * n + t];
   const double c1 = (up - dn) / (2.0 * hh);
   const double c2 = ((up - 2.0 * mid) + dn) / (hh * hh);
   if (!(finite(c1) && finite(c2))) {
@@ -240,28 +258,43 @@ __global__ void k_gen_local(Cost cost, const double* __restrict__ u, ucp_local_p
   out[i] = r;
 }
 
-// solver.py:206-223: first strict argmin over the window, kept in registers
+// solver.py:206-223 in two launches: (1) every (point, window slot) candidate
+// cost in parallel, slot-major per point (wmax = widest window); (2) per
+// point, the first strict minimum in window order (kernels.py:147-160), any
+// non-finite candidate flagging the point, then the projection.
 template <class Cost>
-__global__ void k_gen_exhaust(Cost cost, const double* __restrict__ u, const int64_t* __restrict__ lo,
-                              const int64_t* __restrict__ hi, int project_kind, int64_t begin, int64_t n,
-                              double* out, int64_t* err) {
+__global__ void k_gen_exh_eval(Cost cost, const double* __restrict__ u, const int64_t* __restrict__ lo,
+                               const int64_t* __restrict__ hi, int64_t begin, int64_t n, int64_t wmax,
+                               double* costs) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * wmax) return;
+  const int64_t k = t / n, p = t - k * n;
+  const int64_t i = begin + p;
+  const int64_t j = lo[i] + k;
+  if (j <= hi[i]) costs[p * wmax + k] = cost(u[j], i);
+}
+
+__global__ void k_gen_exh_pick(const double* __restrict__ u, const int64_t* __restrict__ lo,
+                               const int64_t* __restrict__ hi, int project_kind, int64_t begin, int64_t n,
+                               int64_t wmax, const double* __restrict__ costs, double* out, int64_t* err) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int64_t i = begin + t;
-  double bu = u[lo[i]];
-  double bv = cost(bu, i);
+  const double* c = costs + t * wmax;
+  const int64_t w = hi[i] - lo[i] + 1;
+  int64_t best = 0;
+  double bv = c[0];
   bool ok = finite(bv);
-  for (int64_t j = lo[i] + 1; j <= hi[i]; ++j) {
-    const double uj = u[j];
-    const double c = cost(uj, i);
-    ok = ok && finite(c);
-    if (c < bv) {
-      bv = c;
-      bu = uj;
+  for (int64_t k = 1; k < w; ++k) {
+    const double x = c[k];
+    ok = ok && finite(x);
+    if (x < bv) {
+      bv = x;
+      best = k;
     }
   }
   if (!ok) flag_min(err, i);
-  out[i] = project_value(project_kind, bu);
+  out[i] = project_value(project_kind, u[lo[i] + best]);
 }
 
 template <class Cost>
@@ -310,17 +343,31 @@ __global__ void k_inv_downstream(const double* __restrict__ pts, const double* _
 
 template <class Cost>
 int launch_gen_local(const Cost& c, const double* u, const ucp_local_params* lp, double h_floor, int project_kind,
-                     int64_t begin, int64_t n, double* out, int64_t* err, cudaStream_t st) {
-  k_gen_local<Cost><<<nblocks(n, 128), 128, 0, st>>>(c, u, *lp, h_floor, project_kind, begin, n, out, err);
-  UCP_LAUNCHED("k_gen_local");
+                     int64_t begin, int64_t n, double* out, int64_t* err, ucp_workspace* ws, cudaStream_t st) {
+  void* pc;
+  int rc;
+  if ((rc = ws_get(ws, WS_COST, sizeof(double) * 3 * (size_t)n, &pc))) return rc;
+  k_gen_probe<Cost><<<nblocks(3 * n, 128), 128, 0, st>>>(c, u, lp->fd_step, h_floor, begin, n, (double*)pc);
+  UCP_LAUNCHED("k_gen_probe");
+  k_gen_finish<Cost><<<nblocks(n, 128), 128, 0, st>>>(c, u, *lp, h_floor, project_kind, begin, n,
+                                                      (const double*)pc, out, err);
+  UCP_LAUNCHED("k_gen_finish");
   return UCP_OK;
 }
 
 template <class Cost>
-int launch_gen_exhaust(const Cost& c, const double* u, const int64_t* lo, const int64_t* hi, int project_kind,
-                       int64_t begin, int64_t n, double* out, int64_t* err, cudaStream_t st) {
-  k_gen_exhaust<Cost><<<nblocks(n, 128), 128, 0, st>>>(c, u, lo, hi, project_kind, begin, n, out, err);
-  UCP_LAUNCHED("k_gen_exhaust");
+int launch_gen_exhaust(const Cost& c, const double* u, const int64_t* lo, const int64_t* hi, int64_t wmax,
+                       int project_kind, int64_t begin, int64_t n, double* out, int64_t* err, ucp_workspace* ws,
+                       cudaStream_t st) {
+  if (wmax < 1) return arg_fail("exhaustion: window width must be >= 1");
+  void* pc;
+  int rc;
+  if ((rc = ws_get(ws, WS_COST, sizeof(double) * (size_t)(n * wmax), &pc))) return rc;
+  k_gen_exh_eval<Cost><<<nblocks(n * wmax, 128), 128, 0, st>>>(c, u, lo, hi, begin, n, wmax, (double*)pc);
+  UCP_LAUNCHED("k_gen_exh_eval");
+  k_gen_exh_pick<<<nblocks(n, 128), 128, 0, st>>>(u, lo, hi, project_kind, begin, n, wmax, (const double*)pc, out,
+                                                  err);
+  UCP_LAUNCHED("k_gen_exh_pick");
   return UCP_OK;
 }
 
@@ -529,15 +576,15 @@ int ucp_zd_local_update(const ucp_zd_problem* P, int stage, const double* u0, co
   if (n == 0) return UCP_OK;
   cudaStream_t st = as_stream(stream);
   const double floor = P->h1;  // zero_delay.py:56-65: probe >= one decoder cell, both stages
-  if (stage == 0) return launch_gen_local(zd_cost0(P, u1), u0, lp, floor, 0, begin, n, out, err, st);
+  if (stage == 0) return launch_gen_local(zd_cost0(P, u1), u0, lp, floor, 0, begin, n, out, err, ws, st);
   QuadCost q;
   if ((rc = zd_moments(P, u0, P->y1 + begin, n, ws, st, &q))) return rc;
   q.begin = begin;
-  return launch_gen_local(q, u1, lp, floor, 0, begin, n, out, err, st);
+  return launch_gen_local(q, u1, lp, floor, 0, begin, n, out, err, ws, st);
 }
 
 int ucp_zd_exhaustion(const ucp_zd_problem* P, int stage, const double* u0, const double* u1, const int64_t* win_lo,
-                      const int64_t* win_hi, int64_t begin, int64_t end, double* out, int64_t* err,
+                      const int64_t* win_hi, int64_t wmax, int64_t begin, int64_t end, double* out, int64_t* err,
                       ucp_workspace* ws, void* stream) {
   int rc = check_zd(P);
   if (rc) return rc;
@@ -547,11 +594,11 @@ int ucp_zd_exhaustion(const ucp_zd_problem* P, int stage, const double* u0, cons
   const int64_t n = end - begin;
   if (n == 0) return UCP_OK;
   cudaStream_t st = as_stream(stream);
-  if (stage == 0) return launch_gen_exhaust(zd_cost0(P, u1), u0, win_lo, win_hi, 0, begin, n, out, err, st);
+  if (stage == 0) return launch_gen_exhaust(zd_cost0(P, u1), u0, win_lo, win_hi, wmax, 0, begin, n, out, err, ws, st);
   QuadCost q;
   if ((rc = zd_moments(P, u0, P->y1 + begin, n, ws, st, &q))) return rc;
   q.begin = begin;
-  return launch_gen_exhaust(q, u1, win_lo, win_hi, 0, begin, n, out, err, st);
+  return launch_gen_exhaust(q, u1, win_lo, win_hi, wmax, 0, begin, n, out, err, ws, st);
 }
 
 int ucp_zd_objective_terms(const ucp_zd_problem* P, const double* u0, const double* u1, int64_t begin, int64_t end,
@@ -595,11 +642,11 @@ int ucp_inv_local_update(const ucp_inv_problem* P, int stage, const double* cons
   InvCost c;
   if ((rc = inv_cost(P, stage, u, ws, st, &c))) return rc;
   const double floor = P->h[inv_state(P, stage + 1)];  // inventory.py:131-136
-  return launch_gen_local(c, u[stage], lp, floor, 1, begin, n, out, err, st);
+  return launch_gen_local(c, u[stage], lp, floor, 1, begin, n, out, err, ws, st);
 }
 
 int ucp_inv_exhaustion(const ucp_inv_problem* P, int stage, const double* const* u, const int64_t* win_lo,
-                       const int64_t* win_hi, int64_t begin, int64_t end, double* out, int64_t* err,
+                       const int64_t* win_hi, int64_t wmax, int64_t begin, int64_t end, double* out, int64_t* err,
                        ucp_workspace* ws, void* stream) {
   int rc = check_inv(P, u);
   if (rc) return rc;
@@ -611,7 +658,7 @@ int ucp_inv_exhaustion(const ucp_inv_problem* P, int stage, const double* const*
   cudaStream_t st = as_stream(stream);
   InvCost c;
   if ((rc = inv_cost(P, stage, u, ws, st, &c))) return rc;
-  return launch_gen_exhaust(c, u[stage], win_lo, win_hi, 1, begin, n, out, err, st);
+  return launch_gen_exhaust(c, u[stage], win_lo, win_hi, wmax, 1, begin, n, out, err, ws, st);
 }
 
 int ucp_inv_objective_terms(const ucp_inv_problem* P, const double* const* u, int64_t begin, int64_t end,

@@ -113,5 +113,10 @@ class DeviceContext:
         key = (m, float(r))
         if key not in self.windows:
             lo, hi = node_window_bounds(prob.grids[m], r)
-            self.windows[key] = (to_device_i64(lo, self.device), to_device_i64(hi, self.device))
-        return self.windows[key]
+            self.windows[key] = (to_device_i64(lo, self.device), to_device_i64(hi, self.device),
+                                 int((hi - lo).max()) + 1)
+        return self.windows[key][:2]
+
+    def window_width(self, prob, m: int, r: float) -> int:
+        self.window(prob, m, r)
+        return self.windows[(m, float(r))][2]
