@@ -24,7 +24,7 @@ def test_run_config_merging(tmp_path):
     cfgf.write_text(json.dumps({"problem": "zero_delay", "params": {"power_weight": 3.0},
                                 "solver": {"max_rounds": 7}}))
     args = cli.build_parser().parse_args(["solve", "--config", str(cfgf), "--param", "power_weight=1.5",
-                                          "--grid", "1:-6,6,301", "--solver", "precision=1e-8",
+                                          "--grid=1:-6,6,301", "--solver", "precision=1e-8",
                                           "--out", str(tmp_path / "o")])
     rc = cli.load_run_config(args)
     assert rc.problem == "zero_delay" and rc.params == {"power_weight": 1.5}
@@ -38,7 +38,7 @@ def test_run_config_merging(tmp_path):
 def test_solve_exports_bitwise_csv_and_report(tmp_path, golden):
     g = golden("wc_solve_d201")
     out = tmp_path / "run"
-    assert cli.main(["solve", "--grid", "-25,25,201", "--out", str(out)]) == 0
+    assert cli.main(["solve", "--grid=-25,25,201", "--out", str(out)]) == 0
     rep = json.loads((out / "report.json").read_text())
     assert rep["termination"] == "converged" and rep["backend"] == "b200"
     assert rep["total_rounds"] == len(g["rounds"])
@@ -62,4 +62,4 @@ def test_numeric_failure_exit_2(tmp_path, monkeypatch):
         raise NumericError("witsenhausen: non-finite marginal cost in local-update phase at stage 0, grid point 3")
 
     monkeypatch.setattr(cli, "solve", boom)
-    assert cli.main(["solve", "--grid", "-25,25,101", "--out", str(tmp_path)]) == 2
+    assert cli.main(["solve", "--grid=-25,25,101", "--out", str(tmp_path)]) == 2
