@@ -78,12 +78,12 @@ int main() {
   lat<<<1, 32>>>(n, 1.0, out, cyc); cudaDeviceSynchronize();
   lat<<<1, 32>>>(n, 1.0, out, cyc); cudaDeviceSynchronize();
   printf("latency cycles: DMUL %.2f  DADD %.2f  DFMA %.2f\n", cyc[0] / (double)n, cyc[1] / (double)n, cyc[2] / (double)n);
-  for (int warps = 1; warps <= 16; warps *= 2) {
+  for (int warps = 1; warps <= 32; warps *= 2) {
     walk<<<1, 32 * warps>>>(n, v, out, cyc); cudaDeviceSynchronize();
     walk<<<1, 32 * warps>>>(n, v, out, cyc); cudaDeviceSynchronize();
     printf("walk: %2d warps/CTA (1 SM): %.2f cycles per node per warp\n", warps, cyc[3] / (double)n);
   }
-  for (int warps = 1; warps <= 16; warps *= 2) {
+  for (int warps = 1; warps <= 32; warps *= 2) {
     walk_sp<<<1, 32 * warps>>>(n, v, out, cyc); cudaDeviceSynchronize();
     walk_sp<<<1, 32 * warps>>>(n, v, out, cyc); cudaDeviceSynchronize();
     walk2<<<1, 32 * warps>>>(n, v, out, cyc); cudaDeviceSynchronize();
