@@ -30,7 +30,10 @@ constexpr double kGaussCut = 12.0;  // kernels.py:55 GAUSS_CUT
 // least 12 resident per SM (<= 42 registers) so 12 warps per scheduler hide
 // the L1 latency of the v1 stream behind the FP64 pipe.
 constexpr int kWalkThreads = 128;
-constexpr int kWalkMinBlocks = 12;
+#ifndef UCP_WALK_MIN_BLOCKS
+#define UCP_WALK_MIN_BLOCKS 12
+#endif
+constexpr int kWalkMinBlocks = UCP_WALK_MIN_BLOCKS;
 
 __device__ const uint64_t g_exp_tab[256] = UCP_EXP_TAB_INIT;
 const uint64_t h_exp_tab[256] = UCP_EXP_TAB_INIT;

@@ -42,6 +42,53 @@ class Sharding:
         """A float64 buffer sized chunk*world so the all-gather is in place."""
         return torch.empty(self.chunk(d) * self.world, dtype=torch.float64, device=device)
 
+    # -- work-balanced partitions -------------------------------------------
+    def plan(self, d: int, weights: torch.Tensor | None = None) -> tuple:
+        """Shard boundaries (world+1 ints).  With ``weights`` (int64 per-point
+        work estimates, identical on every rank because they derive from the
+        same snapshot) the cumulative work is split evenly; otherwise equal
+        point counts.  Boundaries never change a result bit."""
+        d = int(d)
+        if self.world == 1:
+            return (0, d)
+        if weights is None:
+            c = self.chunk(d)
+            return tuple(min(r * c, d) for r in range(self.world)) + (d,)
+        cum = torch.cumsum(weights.to(torch.int64), 0)
+        targets = (cum[-1] * torch.arange(1, self.world, device=cum.device, dtype=torch.int64)) // self.world
+        cuts = torch.searchsorted(cum, targets, right=True).cpu().tolist()
+        out = [0]
+        for c in cuts:
+            out.append(min(max(int(c), out[-1]), d))
+        out.append(d)
+        return tuple(out)
+
+    def shard(self, bounds: tuple) -> tuple[int, int]:
+        return bounds[self.rank], bounds[self.rank + 1]
+
+    @staticmethod
+    def cmax(bounds: tuple) -> int:
+        return max(1, max(bounds[r + 1] - bounds[r] for r in range(len(bounds) - 1)))
+
+    def padded_buffer(self, bounds: tuple, device) -> torch.Tensor:
+        """world slots of cmax doubles; rank r's points land in slot r."""
+        return torch.empty(self.cmax(bounds) * self.world, dtype=torch.float64, device=device)
+
+    def rank_ptr(self, buf: torch.Tensor, bounds: tuple) -> int:
+        """Base pointer such that base[i] (i in this rank's shard) is its slot entry."""
+        return buf.data_ptr() + 8 * (self.rank * self.cmax(bounds) - bounds[self.rank])
+
+    def gather(self, buf: torch.Tensor, bounds: tuple, d: int) -> torch.Tensor:
+        """All-gather the slots and return the contiguous length-d vector."""
+        if self.world == 1:
+            return buf[:d]
+        self.allgather_(buf)
+        c = self.cmax(bounds)
+        if all(bounds[r] == r * c for r in range(self.world)):
+            return buf[:d]  # equal split: slots are already contiguous
+        slots = buf.view(self.world, c)
+        return torch.cat([slots[r, : bounds[r + 1] - bounds[r]] for r in range(self.world)])
+
     # -- collectives -------------------------------------------------------
     def allgather_(self, buf: torch.Tensor) -> None:
         """In-place all-gather of each rank's chunk of ``buf`` (no-op for one rank)."""

@@ -15,6 +15,7 @@ the window bounds are computed on the host, once per problem.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -28,6 +29,9 @@ from .device_problem import NO_ERROR, ErrorLog
 from .problem import NumericError, Problem
 
 __all__ = ["Witsenhausen"]
+
+# below this many points shards are equal-sized (balancing would cost more than it saves)
+BALANCE_MIN_POINTS = int(os.environ.get("UCP_BALANCE_MIN_POINTS", 1 << 14))
 
 class _WcDevice:
     """Device-resident constants, ABI structs and scratch of one Witsenhausen problem."""
@@ -144,19 +148,43 @@ class Witsenhausen(Problem):
         return out[:n].cpu().numpy()
 
     # ------------------------------------------------ solver sweeps (device)
+    # ---- work-balanced shards (multi-GPU) --------------------------------
+    def _plan(self, m: int, U: ControllerSet, sharding: Sharding, stage0_scale=None) -> tuple:
+        """Shard boundaries for a stage-m phase: split the estimated work
+        (walk nodes for stage 0, in-range support points for stage 1) evenly
+        across ranks.  Estimates come from the shared snapshot, so every rank
+        computes the same boundaries; results do not depend on them."""
+        d = self.grids[m].d
+        if sharding.world == 1 or d < BALANCE_MIN_POINTS:
+            return sharding.plan(d)
+        D = self.device_context()
+        u0, _ = self._uv(U)
+        g1 = self.grids[1]
+        if m == 0:
+            s = D.y0 + u0
+            span = torch.clamp(torch.minimum(s + 12.0, torch.full_like(s, g1.b))
+                               - torch.maximum(s - 12.0, torch.full_like(s, g1.a)), min=0.0)
+            w = (span / g1.spacing).to(torch.int64) + 1
+            if stage0_scale is not None:
+                w = w * stage0_scale
+        else:
+            xs = torch.sort(D.y0 + u0).values
+            w = (torch.searchsorted(xs, D.y1 + 12.0, right=True) - torch.searchsorted(xs, D.y1 - 12.0)) + 1
+        return sharding.plan(d, w)
+
     def device_local_update(self, m: int, U: ControllerSet, cfg, sharding: Sharding = LOCAL):
         """One local-update sweep of stage m (solver.py:179-203); returns a CUDA tensor."""
         D = self.device_context()
         g = self.grids[m]
         u0, u1 = self._uv(U)
         lp = _lib.LocalParams(cfg.fd_step, cfg.curvature_min, cfg.grad_step, cfg.cap_for(g))
-        begin, end = sharding.bounds(g.d)
-        buf = sharding.out_buffer(g.d, D.device)
+        bounds = self._plan(m, U, sharding)
+        begin, end = sharding.shard(bounds)
+        buf = sharding.padded_buffer(bounds, D.device)
         err = D.errors.slot("local", m, sharding)
         _lib.call("ucp_wc_local_update", ctypes.byref(D.P), m, ptr(u0), ptr(u1), ctypes.byref(lp), begin, end,
-                  ptr(buf), ptr(err), D.ws, D.stream)
-        sharding.allgather_(buf)
-        return buf[: g.d]
+                  sharding.rank_ptr(buf, bounds), ptr(err), D.ws, D.stream)
+        return sharding.gather(buf, bounds, g.d)
 
     def device_exhaustion(self, m: int, U: ControllerSet, cfg, sharding: Sharding = LOCAL):
         """One partial-exhaustion sweep of stage m (solver.py:206-223)."""
@@ -164,13 +192,13 @@ class Witsenhausen(Problem):
         g = self.grids[m]
         u0, u1 = self._uv(U)
         lo, hi = D.window(self, m, cfg.radius_for(g))
-        begin, end = sharding.bounds(g.d)
-        buf = sharding.out_buffer(g.d, D.device)
+        bounds = self._plan(m, U, sharding, stage0_scale=(hi - lo + 1) if m == 0 else None)
+        begin, end = sharding.shard(bounds)
+        buf = sharding.padded_buffer(bounds, D.device)
         err = D.errors.slot("exhaustion", m, sharding)
         _lib.call("ucp_wc_exhaustion", ctypes.byref(D.P), m, ptr(u0), ptr(u1), ptr(lo), ptr(hi), begin, end,
-                  ptr(buf), ptr(err), D.ws, D.stream)
-        sharding.allgather_(buf)
-        return buf[: g.d]
+                  sharding.rank_ptr(buf, bounds), ptr(err), D.ws, D.stream)
+        return sharding.gather(buf, bounds, g.d)
 
     def device_run_block(self, kind: str, iters: int, U: ControllerSet, cfg) -> ControllerSet:
         """`iters` iterations of one phase kind over both stages in ONE native
@@ -206,12 +234,13 @@ class Witsenhausen(Problem):
         D.errors.flush(sharding)  # earlier phases fail first, in order
         g = self.grids[0]
         u0, u1 = self._uv(U)
-        begin, end = sharding.bounds(g.d)
-        terms = sharding.out_buffer(g.d, D.device)
+        bounds = self._plan(0, U, sharding)
+        begin, end = sharding.shard(bounds)
+        buf = sharding.padded_buffer(bounds, D.device)
         res = torch.full((2,), NO_ERROR, dtype=I64, device=D.device)  # [J bits, first bad point]
-        _lib.call("ucp_wc_objective_terms", ctypes.byref(D.P), ptr(u0), ptr(u1), begin, end, ptr(terms),
-                  res[1:].data_ptr(), D.stream)
-        sharding.allgather_(terms)
+        _lib.call("ucp_wc_objective_terms", ctypes.byref(D.P), ptr(u0), ptr(u1), begin, end,
+                  sharding.rank_ptr(buf, bounds), res[1:].data_ptr(), D.stream)
+        terms = sharding.gather(buf, bounds, g.d)
         sharding.allreduce_min_(res[1:])
         _lib.call("ucp_trapezoid_sum", ptr(terms), g.d, g.spacing, res[:1].data_ptr(), None, D.stream)
         host = res.cpu().numpy()

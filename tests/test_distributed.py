@@ -6,6 +6,7 @@ GPU (gloo, 2 processes on one GPU): the real device sweeps sharded over two
 ranks, bitwise identical to the single-process result.  (NCCL is the
 production backend; its collectives are the same two calls.)
 """
+import ctypes
 import os
 import socket
 import sys
@@ -62,6 +63,17 @@ def _prim_worker(rank, world, port, q):
         buf[b:e] = torch.arange(b, e, dtype=torch.float64)
         sh.allgather_(buf)
         res[d] = (b, e, buf[:d].numpy().copy())
+    # work-balanced, uneven shards: padded slots + compaction
+    d = 1000
+    w = torch.ones(d, dtype=torch.int64)
+    w[:100] = 50  # heavy head
+    bounds = sh.plan(d, w)
+    b, e = sh.shard(bounds)
+    buf = sh.padded_buffer(bounds, "cpu")
+    base = sh.rank_ptr(buf, bounds)
+    view = torch.from_numpy(np.ctypeslib.as_array((ctypes.c_double * (e - b)).from_address(base + 8 * b)))
+    view[:] = torch.arange(b, e, dtype=torch.float64)
+    res["balanced"] = (bounds, sh.gather(buf, bounds, d).numpy().copy())
     t = torch.tensor([10 + rank, 5 - rank, (1 << 63) - 1], dtype=torch.int64)
     sh.allreduce_min_(t)
     res["min"] = t.numpy().copy()
@@ -77,6 +89,10 @@ def test_sharding_primitives_world2():
         np.testing.assert_array_equal(g0, np.arange(d, dtype=np.float64))
         np.testing.assert_array_equal(g1, g0)
     np.testing.assert_array_equal(out[0]["min"], [10, 4, (1 << 63) - 1])
+    for r in (0, 1):
+        bounds, full = out[r]["balanced"]
+        assert bounds[0] == 0 and bounds[-1] == 1000 and 0 < bounds[1] < 500  # the heavy head shrinks shard 0
+        np.testing.assert_array_equal(full, np.arange(1000, dtype=np.float64))
 
 
 # ------------------------------------- solver block loop over an oracle fake
@@ -161,10 +177,13 @@ def _gpu_solve_worker(rank, world, port, q, d):
 
 
 @pytest.mark.gpu
-def test_sharded_device_solve_bitwise_world2():
+@pytest.mark.parametrize("balanced", [False, True])
+def test_sharded_device_solve_bitwise_world2(balanced, monkeypatch):
     import paper_1908_04489_b200 as P
 
     d = 301
+    # work-balanced (uneven) shards are used above UCP_BALANCE_MIN_POINTS points
+    monkeypatch.setenv("UCP_BALANCE_MIN_POINTS", "16" if balanced else str(1 << 20))
     out = _spawn(_gpu_solve_worker, 2, d)
     prob = P.Witsenhausen(grids=[(-25.0, 25.0, d)] * 2)
     ref = P.solve(prob, P.SolverConfig(max_rounds=3))
