@@ -122,10 +122,13 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
                         int64_t* err, ucp_workspace* ws, void* stream);
 /* solver.py:206-223 partial_exhaustion_phase; win_lo/win_hi from
  * grids.node_window_bounds (grids.py:180-195).  err[0] <- first point with a
- * non-finite candidate cost.  Synchronises `stream` once (candidate count). */
+ * non-finite candidate cost.  cand_bound = sum of window widths over the
+ * shard (host-known): when given (> 0) and within budget the call never
+ * synchronises; with 0 it reads the candidate count back (one stream sync). */
 int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, const double* u1,
-                      const int64_t* win_lo, const int64_t* win_hi, int64_t begin, int64_t end,
-                      double* out, int64_t* err, ucp_workspace* ws, void* stream);
+                      const int64_t* win_lo, const int64_t* win_hi, int64_t cand_bound,
+                      int64_t begin, int64_t end, double* out, int64_t* err, ucp_workspace* ws,
+                      void* stream);
 /* solver.py:226-231 _run_block, unsharded: `iters` iterations over both
  * stages of one phase kind (0 = local update with lp[0..1], 1 = partial
  * exhaustion with the two stages' windows), each phase reading the latest
@@ -134,8 +137,9 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
  * per block: no per-phase host round trip beyond the exhaustion count. */
 int ucp_wc_run_block(const ucp_wc_problem* P, int kind, int iters, double* u0, double* u1,
                      const ucp_local_params* lp, const int64_t* win_lo0, const int64_t* win_hi0,
-                     const int64_t* win_lo1, const int64_t* win_hi1, double* scratch0,
-                     double* scratch1, int64_t* err, ucp_workspace* ws, void* stream);
+                     const int64_t* win_lo1, const int64_t* win_hi1, int64_t cand_bound0,
+                     double* scratch0, double* scratch1, int64_t* err, ucp_workspace* ws,
+                     void* stream);
 /* problem.py:110-127 objective, per-point part: terms[i] = C0(u0[i], y0[i])
  * for i in [begin, end); err[0] <- first non-finite term.  The serial
  * trapezoid over all terms is ucp_trapezoid_sum. */

@@ -827,6 +827,8 @@ static_assert(WS_NSLOTS <= 16, "workspace slots");
 // two-phase moments when the query set cannot fill the GPU with the direct kernel
 constexpr int64_t kTwoPhaseMaxQueries = 8192;
 constexpr int64_t kTwoPhaseMaxPairs = (int64_t)1 << 25;  // 256 MiB of pre-weights
+// sync-free exhaustion when the candidate upper bound fits (16 B per candidate)
+constexpr int64_t kSyncFreeMaxCand = (int64_t)1 << 27;
 
 int ws_get(ucp_workspace* ws, int slot, size_t bytes, void** out) {
   if (ws->cap[slot] < bytes) {
@@ -1091,8 +1093,8 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
 }
 
 int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, const double* u1,
-                      const int64_t* win_lo, const int64_t* win_hi, int64_t begin, int64_t end,
-                      double* out, int64_t* err, ucp_workspace* ws, void* stream) {
+                      const int64_t* win_lo, const int64_t* win_hi, int64_t cand_bound, int64_t begin,
+                      int64_t end, double* out, int64_t* err, ucp_workspace* ws, void* stream) {
   int rc = check_problem(P);
   if (rc) return rc;
   if (!ws || !err || !win_lo || !win_hi) return arg_fail("exhaustion: null argument");
@@ -1130,9 +1132,19 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
   UCP_CHECK(cudaMemsetAsync(counts + n, 0, sizeof(int64_t), st));
   UCP_CHECK(cub::DeviceScan::ExclusiveSum(ws->scan_tmp, tmp_bytes, counts, counts, n + 1, st));
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  UCP_CHECK(cudaMemcpyAsync(ws->h_total, counts + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  UCP_CHECK(cudaStreamSynchronize(st));
-  int64_t total = *ws->h_total;
+  // The candidate count lives on the device.  With a host-known upper bound
+  // (sum of window widths) that fits the budget, size everything for the
+  // bound and let the kernels read the true count: no host round trip, so a
+  // whole block of phases stays queued on the stream.  Otherwise read it back.
+  int64_t total;
+  if (cand_bound > 0 && cand_bound <= kSyncFreeMaxCand) {
+    total = cand_bound;
+  } else {
+    UCP_CHECK(cudaMemcpyAsync(ws->h_total, counts + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    UCP_CHECK(cudaStreamSynchronize(st));
+    total = *ws->h_total;
+  }
+  if (total <= 0) total = 1;
   void *ppt, *pj, *pc;
   if ((rc = ws_get(ws, WS_CAND_PT, sizeof(int32_t) * (size_t)total, &ppt))) return rc;
   if ((rc = ws_get(ws, WS_CAND_J, sizeof(int32_t) * (size_t)total, &pj))) return rc;
@@ -1153,8 +1165,8 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
 
 int ucp_wc_run_block(const ucp_wc_problem* P, int kind, int iters, double* u0, double* u1,
                      const ucp_local_params* lp, const int64_t* win_lo0, const int64_t* win_hi0,
-                     const int64_t* win_lo1, const int64_t* win_hi1, double* scratch0, double* scratch1,
-                     int64_t* err, ucp_workspace* ws, void* stream) {
+                     const int64_t* win_lo1, const int64_t* win_hi1, int64_t cand_bound0, double* scratch0,
+                     double* scratch1, int64_t* err, ucp_workspace* ws, void* stream) {
   int rc = check_problem(P);
   if (rc) return rc;
   if (kind < 0 || kind > 1 || iters < 0) return arg_fail("run_block: bad kind/iters");
@@ -1175,7 +1187,8 @@ int ucp_wc_run_block(const ucp_wc_problem* P, int kind, int iters, double* u0, d
       if (kind == 0)
         rc = ucp_wc_local_update(P, m, u0, u1, lp + m, 0, d[m], scratch[m], e, ws, stream);
       else
-        rc = ucp_wc_exhaustion(P, m, u0, u1, lo[m], hi[m], 0, d[m], scratch[m], e, ws, stream);
+        rc = ucp_wc_exhaustion(P, m, u0, u1, lo[m], hi[m], m == 0 ? cand_bound0 : 0, 0, d[m], scratch[m], e, ws,
+                               stream);
       if (rc) return rc;
       UCP_CHECK(cudaMemcpyAsync(u[m], scratch[m], sizeof(double) * (size_t)d[m], cudaMemcpyDeviceToDevice, st));
     }

@@ -113,9 +113,16 @@ class DeviceContext:
         key = (m, float(r))
         if key not in self.windows:
             lo, hi = node_window_bounds(prob.grids[m], r)
+            widths = np.concatenate([[0], np.cumsum(hi - lo + 1)])
             self.windows[key] = (to_device_i64(lo, self.device), to_device_i64(hi, self.device),
-                                 int((hi - lo).max()) + 1)
+                                 int((hi - lo).max()) + 1, widths)
         return self.windows[key][:2]
+
+    def candidate_bound(self, prob, m: int, r: float, begin: int, end: int) -> int:
+        """Sum of window widths over [begin, end): an upper bound on the deduped candidates."""
+        self.window(prob, m, r)
+        widths = self.windows[(m, float(r))][3]
+        return int(widths[end] - widths[begin])
 
     def window_width(self, prob, m: int, r: float) -> int:
         self.window(prob, m, r)

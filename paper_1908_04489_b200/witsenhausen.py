@@ -196,7 +196,8 @@ class Witsenhausen(Problem):
         begin, end = sharding.shard(bounds)
         buf = sharding.padded_buffer(bounds, D.device)
         err = D.errors.slot("exhaustion", m, sharding)
-        _lib.call("ucp_wc_exhaustion", ctypes.byref(D.P), m, ptr(u0), ptr(u1), ptr(lo), ptr(hi), begin, end,
+        bound = D.candidate_bound(self, m, cfg.radius_for(g), begin, end) if m == 0 else 0
+        _lib.call("ucp_wc_exhaustion", ctypes.byref(D.P), m, ptr(u0), ptr(u1), ptr(lo), ptr(hi), bound, begin, end,
                   sharding.rank_ptr(buf, bounds), ptr(err), D.ws, D.stream)
         return sharding.gather(buf, bounds, g.d)
 
@@ -215,14 +216,15 @@ class Witsenhausen(Problem):
         lp = (_lib.LocalParams * 2)(*[_lib.LocalParams(cfg.fd_step, cfg.curvature_min, cfg.grad_step,
                                                        cfg.cap_for(g)) for g in (g0, g1)])
         if kind == "local":
-            code, wins = 0, (None, None, None, None)
+            code, wins, bound = 0, (None, None, None, None), 0
         else:
             code = 1
             lo0, hi0 = D.window(self, 0, cfg.radius_for(g0))
             lo1, hi1 = D.window(self, 1, cfg.radius_for(g1))
             wins = (ptr(lo0), ptr(hi0), ptr(lo1), ptr(hi1))
+            bound = D.candidate_bound(self, 0, cfg.radius_for(g0), 0, g0.d)
         err = D.errors.slots([(kind, m) for _ in range(iters) for m in (0, 1)], LOCAL)
-        _lib.call("ucp_wc_run_block", ctypes.byref(D.P), code, int(iters), ptr(out0), ptr(out1), lp, *wins,
+        _lib.call("ucp_wc_run_block", ctypes.byref(D.P), code, int(iters), ptr(out0), ptr(out1), lp, *wins, bound,
                   ptr(s0), ptr(s1), ptr(err), D.ws, D.stream)
         return ControllerSet((SampledController(g0, out0, _trusted_device=True),
                               SampledController(g1, out1, _trusted_device=True)))

@@ -266,3 +266,21 @@ def test_solve_many_matches_individual_solves(P):
         assert r.final_objective == solo.final_objective
         assert [x.objective for x in r.rounds] == [x.objective for x in solo.rounds]
         np.testing.assert_array_equal(np.asarray(r.controllers.values(0)), np.asarray(solo.controllers.values(0)))
+
+
+def test_exhaustion_sync_and_syncfree_paths_agree(P, golden, monkeypatch):
+    """ucp_wc_exhaustion with a host candidate bound (no stream sync) and
+    without one (count read back) give the reference's result."""
+    from paper_1908_04489_b200.device_problem import DeviceContext
+
+    g = golden("wc_d201")
+    cfg = P.SolverConfig()
+    for bound_off in (False, True):
+        prob = _wc(P, g)
+        if bound_off:
+            monkeypatch.setattr(DeviceContext, "candidate_bound", lambda *a, **k: 0)
+        U = _U(P, prob, g["pert1_u0"], g["pert1_u1"])
+        assert_bitwise(P.partial_exhaustion_phase(prob, 0, U, cfg), g["pert1_ex0"], f"EX0 bound_off={bound_off}")
+        V = P.run_block(prob, U, cfg, 1, "local")
+        V = P.run_block(prob, V, cfg, 1, "exhaustion")
+        assert_bitwise(V.values(0), g["pert1_it_u0"], "it u0")
