@@ -21,11 +21,11 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import F64, I64, ptr, require_cuda, stream_ptr, to_device_f64, to_device_i64
+from ._device import F64, I64, ptr, to_device_f64, to_device_i64
 from .distributed import LOCAL, Sharding
-from .grids import ControllerSet, node_window_bounds
+from .grids import ControllerSet
 from .numerics import Gaussian, pdf
-from .device_problem import NO_ERROR, ErrorLog
+from .device_problem import NO_ERROR, DeviceContext
 from .problem import NumericError, Problem
 
 __all__ = ["Witsenhausen"]
@@ -33,12 +33,12 @@ __all__ = ["Witsenhausen"]
 # below this many points shards are equal-sized (balancing would cost more than it saves)
 BALANCE_MIN_POINTS = int(os.environ.get("UCP_BALANCE_MIN_POINTS", 1 << 14))
 
-class _WcDevice:
-    """Device-resident constants, ABI structs and scratch of one Witsenhausen problem."""
+class _WcDevice(DeviceContext):
+    """Device-resident constants and ABI struct of one Witsenhausen problem
+    (plus the shared workspace / error log / window cache)."""
 
     def __init__(self, prob: "Witsenhausen", device=None):
-        self.lib = _lib.load()
-        self.device = require_cuda(device)
+        super().__init__(prob, device)
         g0, g1 = prob.grids
         self.y0 = to_device_f64(g0.points, self.device)
         self.y1 = to_device_f64(g1.points, self.device)
@@ -46,30 +46,6 @@ class _WcDevice:
         self.fw0 = to_device_f64(prob._fw0, self.device)
         self.P = _lib.WcProblem(prob.k, g0.a, g0.spacing, g0.d, g1.a, g1.spacing, g1.d,
                                 ptr(self.y0), ptr(self.y1), ptr(self.f0), ptr(self.fw0))
-        ws = ctypes.c_void_p()
-        _lib.call("ucp_workspace_create", ctypes.byref(ws))
-        self.ws = ws
-        self.errors = ErrorLog(self.device, prob)
-        self.windows: dict = {}
-
-    def __del__(self):
-        try:
-            if self.ws:
-                torch.cuda.synchronize(self.device)
-                self.lib.ucp_workspace_destroy(self.ws)
-        except Exception:  # interpreter shutdown
-            pass
-
-    @property
-    def stream(self) -> int:
-        return stream_ptr(self.device)
-
-    def window(self, prob, m: int, r: float):
-        key = (m, float(r))
-        if key not in self.windows:
-            lo, hi = node_window_bounds(prob.grids[m], r)
-            self.windows[key] = (to_device_i64(lo, self.device), to_device_i64(hi, self.device))
-        return self.windows[key]
 
 
 class Witsenhausen(Problem):
