@@ -14,6 +14,8 @@
 #include <string.h>
 
 #include <atomic>
+#include <mutex>
+#include <unordered_set>
 #include <cub/device/device_scan.cuh>
 
 #include "../../include/ucp_b200.h"
@@ -103,8 +105,23 @@ __device__ __forceinline__ double phi_cdf(double z) { return ucp_phi_cdf_tab(z, 
 // issues each group's loads one group ahead, so a lone warp per scheduler is
 // bound by its DMUL chain instead of L2 latency.  Throughput mode (large d)
 // keeps the register footprint at 40 so 12 CTAs/SM hide the latency instead.
-template <bool kLat>
+// kMode: 0 = throughput (global __ldg, 12 CTAs/SM), 1 = latency (L1
+// prefetch + loads one group ahead), 2 = latency with v1 staged whole in
+// shared memory (small grids, d <= kSmemWalkMax).
+template <int kMode>
+__device__ __forceinline__ double walk_ld(const double* v, int j) {
+  if (kMode == 2) return v[j];
+  return __ldg(v + j);
+}
+template <int kMode>
+__device__ __forceinline__ double2 walk_ld2(const double* v, int j) {
+  if (kMode == 2) return *reinterpret_cast<const double2*>(v + j);
+  return __ldg(reinterpret_cast<const double2*>(v + j));
+}
+
+template <int kMode>
 __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__ v, const WalkGrid g) {
+  constexpr bool kLat = kMode != 0;
   long long jlo = (long long)ceil(((st - kGaussCut) - g.a) / g.h);
   long long jhi = (long long)floor(((st + kGaussCut) - g.a) / g.h);
   if (jlo < 0) jlo = 0;
@@ -129,12 +146,12 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
     pdf *= ratio;                   \
     ratio *= q;                     \
   }
-#define UCP_WALK_STEP(W)            \
-  {                                 \
-    const double vj_ = __ldg(v + j); \
-    UCP_WALK_STEP_V(W, vj_);        \
+#define UCP_WALK_STEP(W)                      \
+  {                                           \
+    const double vj_ = walk_ld<kMode>(v, j);  \
+    UCP_WALK_STEP_V(W, vj_);                  \
   }
-    if (kLat) {
+    if (kMode == 1) {
       for (int p = j & ~15; p <= je; p += 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(v + p));
     }
     const double hh = 0.5 * h;
@@ -151,11 +168,11 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
     }
     if (kLat) {
       if (j + 3 <= jint) {
-        double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
-        double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
+        double2 p0 = walk_ld2<kMode>(v, j);
+        double2 p1 = walk_ld2<kMode>(v, j + 2);
         for (; j + 7 <= jint; j += 4) {
-          const double2 n0 = __ldg(reinterpret_cast<const double2*>(v + j + 4));
-          const double2 n1 = __ldg(reinterpret_cast<const double2*>(v + j + 6));
+          const double2 n0 = walk_ld2<kMode>(v, j + 4);
+          const double2 n1 = walk_ld2<kMode>(v, j + 6);
           UCP_WALK_STEP_V(h, p0.x);
           UCP_WALK_STEP_V(h, p0.y);
           UCP_WALK_STEP_V(h, p1.x);
@@ -186,7 +203,7 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
   }
   double lo = phi_cdf(g.a - st);
   double hi = phi_cdf(st - g.b);
-  const double v0 = __ldg(v), vl = __ldg(v + g.d - 1);
+  const double v0 = walk_ld<kMode>(v, 0), vl = walk_ld<kMode>(v, (int)(g.d - 1));
   Mom3 r;
   r.t0 = (acc0 + lo) + hi;
   r.t1 = (acc1 + lo * v0) + hi * vl;
@@ -200,11 +217,11 @@ __device__ __forceinline__ double quad_in_u(double a, double b, double c, double
 }
 
 // witsenhausen.py:64-70: C0(u, y) = f0(y) * (k^2 u^2 + E[(s - u1(y1))^2]), s = y+u
-template <bool kLat>
+template <int kMode>
 __device__ __forceinline__ double stage0_cost(double u, double y, double f0, double k,
                                               const double* __restrict__ v1, const WalkGrid g) {
   double s = y + u;
-  Mom3 t = gauss_walk<kLat>(s, v1, g);
+  Mom3 t = gauss_walk<kMode>(s, v1, g);
   double inner = quad_in_u(t.t0, t.t1, t.t2, s);
   return f0 * ((((k * k) * u) * u) + inner);
 }
@@ -216,13 +233,24 @@ __device__ __forceinline__ void flag_min(int64_t* slot, int64_t i) {
 }
 
 // ---------------------------------------------------------------- kernels
+// Mode-2 walk kernels stage the whole v1 (d <= kSmemWalkMax) in shared memory
+// before any thread returns; V becomes the shared copy.
+#define UCP_WALK_STAGE(V, D)                                        \
+  if (kMode == 2) {                                                 \
+    extern __shared__ __align__(16) double ucp_sv_[];               \
+    for (int r_ = threadIdx.x; r_ < (int)(D); r_ += blockDim.x)    \
+      ucp_sv_[r_] = V[r_];                                          \
+    __syncthreads();                                                \
+    V = ucp_sv_;                                                    \
+  }
 
-template <bool kLat>
-__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_gauss_grid(const double* __restrict__ s, int64_t n, const double* __restrict__ v,
+template <int kMode>
+__global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_gauss_grid(const double* __restrict__ s, int64_t n, const double* __restrict__ v,
                              WalkGrid g, double* t0, double* t1, double* t2) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  UCP_WALK_STAGE(v, g.d);
   if (t >= n) return;
-  Mom3 r = gauss_walk<kLat>(s[t], v, g);
+  Mom3 r = gauss_walk<kMode>(s[t], v, g);
   t0[t] = r.t0;
   t1[t] = r.t1;
   t2[t] = r.t2;
@@ -230,37 +258,39 @@ __global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_gau
 
 // marginal_cost_segmented m=0 over a flat candidate list; the segment of
 // candidate c is found by binary search in `offsets` (segments are short).
-template <bool kLat>
-__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_stage0_segmented(const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
+template <int kMode>
+__global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_stage0_segmented(const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
                                    int64_t nseg, const double* __restrict__ y_seg,
                                    const double* __restrict__ f0_seg, double k,
                                    const double* __restrict__ v1, WalkGrid g, double* out) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t n = offsets[nseg];
+  UCP_WALK_STAGE(v1, g.d);
   if (c >= n) return;
   int64_t lo = 0, hi = nseg;  // find s with offsets[s] <= c < offsets[s+1]
   while (hi - lo > 1) {
     int64_t mid = (lo + hi) >> 1;
     if (offsets[mid] <= c) lo = mid; else hi = mid;
   }
-  out[c] = stage0_cost<kLat>(u_flat[c], y_seg[lo], f0_seg[lo], k, v1, g);
+  out[c] = stage0_cost<kMode>(u_flat[c], y_seg[lo], f0_seg[lo], k, v1, g);
 }
 
 // Local update, stage 0, part 1 (problem.py:95-97): the three FD probes
 // u+h, u, u-h of every point.  probe-major layout so a warp walks adjacent
 // centres (coalesced v1 reads).
-template <bool kLat>
-__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_lu0_probe(const double* __restrict__ y0, const double* __restrict__ f0,
+template <int kMode>
+__global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_lu0_probe(const double* __restrict__ y0, const double* __restrict__ f0,
                             const double* __restrict__ u0, double k, const double* __restrict__ v1,
                             WalkGrid g, double fd_step, int64_t begin, int64_t n, double* cost3) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  UCP_WALK_STAGE(v1, g.d);
   if (t >= 3 * n) return;
   int p = (int)(t / n);
   int64_t i = begin + (t - (int64_t)p * n);
   double u = u0[i];
   double hh = fd_step * (1.0 + fabs(u));  // solver.py:192
   double uu = p == 0 ? u + hh : (p == 1 ? u : u - hh);
-  cost3[t] = stage0_cost<kLat>(uu, y0[i], f0[i], k, v1, g);
+  cost3[t] = stage0_cost<kMode>(uu, y0[i], f0[i], k, v1, g);
 }
 
 // Newton-or-gradient step shared by both stages (solver.py:130-149).
@@ -278,12 +308,13 @@ __device__ __forceinline__ double newton_step(double u, double c1, double c2,
 // Local update, stage 0, part 2: derivatives (problem.py:99-101), step,
 // cost_new and the monotone guard (solver.py:193-203).  cost_old is the
 // bitwise-identical `mid` probe.
-template <bool kLat>
-__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_lu0_finish(const double* __restrict__ y0, const double* __restrict__ f0,
+template <int kMode>
+__global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_lu0_finish(const double* __restrict__ y0, const double* __restrict__ f0,
                              const double* __restrict__ u0, double k, const double* __restrict__ v1,
                              WalkGrid g, ucp_local_params lp, int64_t begin, int64_t n,
                              const double* __restrict__ cost3, double* out, int64_t* err) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  UCP_WALK_STAGE(v1, g.d);
   if (t >= n) return;
   int64_t i = begin + t;
   double u = u0[i];
@@ -297,7 +328,7 @@ __global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_lu0
     return;
   }
   double stepped = newton_step(u, c1, c2, lp);  // project() is the identity
-  double cost_new = stage0_cost<kLat>(stepped, y0[i], f0[i], k, v1, g);
+  double cost_new = stage0_cost<kMode>(stepped, y0[i], f0[i], k, v1, g);
   if (!(finite(mid) && finite(cost_new))) flag_min(err + 1, i);
   double r = cost_new <= mid ? stepped : u;
   if (!finite(r)) flag_min(err + 2, i);
@@ -305,13 +336,14 @@ __global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_lu0
 }
 
 // Objective integrand (problem.py:116-127): c_i = C0(u0_i, y0_i).
-template <bool kLat>
-__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_obj_terms(const double* __restrict__ y0, const double* __restrict__ f0,
+template <int kMode>
+__global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_obj_terms(const double* __restrict__ y0, const double* __restrict__ f0,
                             const double* __restrict__ u0, double k, const double* __restrict__ v1,
                             WalkGrid g, int64_t begin, int64_t end, double* terms, int64_t* err) {
   int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  UCP_WALK_STAGE(v1, g.d);
   if (i >= end) return;
-  double c = stage0_cost<kLat>(u0[i], y0[i], f0[i], k, v1, g);
+  double c = stage0_cost<kMode>(u0[i], y0[i], f0[i], k, v1, g);
   if (!finite(c)) flag_min(err, i);
   terms[i] = c;
 }
@@ -423,16 +455,17 @@ __global__ void k_ex_fill(const double* __restrict__ u, const int64_t* __restric
   }
 }
 
-template <bool kLat>
-__global__ void __launch_bounds__(kWalkThreads, kLat ? 1 : kWalkMinBlocks) k_ex0_eval(const double* __restrict__ y0, const double* __restrict__ f0,
+template <int kMode>
+__global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ex0_eval(const double* __restrict__ y0, const double* __restrict__ f0,
                            const double* __restrict__ u0, double k, const double* __restrict__ v1,
                            WalkGrid g, const int64_t* __restrict__ total,
                            const int32_t* __restrict__ cand_pt, const int32_t* __restrict__ cand_j,
                            double* costs) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  UCP_WALK_STAGE(v1, g.d);
   if (c >= *total) return;
   int32_t i = cand_pt[c];
-  costs[c] = stage0_cost<kLat>(u0[cand_j[c]], y0[i], f0[i], k, v1, g);
+  costs[c] = stage0_cost<kMode>(u0[cand_j[c]], y0[i], f0[i], k, v1, g);
 }
 
 // First strict minimum per point (kernels.py:147-160), kept in registers;
@@ -645,7 +678,7 @@ k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x
 //      reference does (`if wp != 0: wp *= w[i]; acc += ...`).
 // Same operations in the same order per pair and per accumulator: bitwise
 // equal to the direct kernel.
-constexpr int kPairChunk = 64;
+constexpr int kPairChunk = 16;
 __global__ void __launch_bounds__(128)
 k_mom_pairs(const double* __restrict__ yq, int64_t n, const double* __restrict__ x,
             const double2* __restrict__ tails, int64_t m, double a, double h, int64_t d, double* pre) {
@@ -700,15 +733,18 @@ k_mom_accum(const double* __restrict__ pre, int64_t n, const double* __restrict_
       for (int k = 0; k < kB; ++k) pv[k] = (active && r0 + k < cnt) ? __ldcs(col + (base + r0 + k) * n) : 0.0;
 #pragma unroll
       for (int k = 0; k < kB; ++k) {
-        double wp = pv[k];
-        if (wp != 0.0) {  // padding slots are 0.0: skipped like the reference's zeros
-          const double xi = sx[r0 + k];
-          wp *= sw[r0 + k];
-          acc0 += wp;
-          const double wx = wp * xi;
-          acc1 += wx;
-          acc2 += wx * xi;
-        }
+        // Branch-free form of `if (wp != 0) { wp *= w; acc += ... }`: a
+        // skipped pair contributes exact zeros (operands selected to 0.0,
+        // so no NaN from w or x), and acc + (+-0) == acc because an
+        // accumulator that starts at +0.0 can never become -0.0 under
+        // round-to-nearest.  Lets the compiler overlap consecutive pairs.
+        const bool live = pv[k] != 0.0;  // padding slots are 0.0
+        const double wp = live ? pv[k] * sw[r0 + k] : 0.0;
+        const double xi = live ? sx[r0 + k] : 0.0;
+        acc0 += wp;
+        const double wx = wp * xi;
+        acc1 += wx;
+        acc2 += wx * xi;
       }
     }
   }
@@ -896,12 +932,29 @@ bool walk_latency_mode(int64_t n_walks) {
   return n_walks < (int64_t)sms * kWalkMinBlocks * kWalkThreads;
 }
 
-#define UCP_WALK_LAUNCH(kernel, n_walks, grid, stream, ...)                              \
-  do {                                                                                  \
-    if (walk_latency_mode(n_walks))                                                     \
-      kernel<true><<<(grid), kWalkThreads, 0, (stream)>>>(__VA_ARGS__);                 \
-    else                                                                                \
-      kernel<false><<<(grid), kWalkThreads, 0, (stream)>>>(__VA_ARGS__);                \
+// kSmemWalkMax doubles of v1 fit the opt-in shared memory of one CTA
+constexpr int64_t kSmemWalkMax = 12288;
+
+std::mutex g_smem_mu;
+std::unordered_set<const void*> g_smem_ok;
+
+template <class K>
+void allow_smem(K* kernel) {  // opt in to >48 KiB dynamic shared memory, once per kernel
+  std::lock_guard<std::mutex> lock(g_smem_mu);
+  if (g_smem_ok.insert(reinterpret_cast<const void*>(kernel)).second)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemWalkMax * sizeof(double)));
+}
+
+#define UCP_WALK_LAUNCH(kernel, n_walks, grid, stream, d_v1, ...)                                   \
+  do {                                                                                            \
+    if (!walk_latency_mode(n_walks)) {                                                            \
+      kernel<0><<<(grid), kWalkThreads, 0, (stream)>>>(__VA_ARGS__);                              \
+    } else if ((d_v1) <= kSmemWalkMax) {                                                          \
+      allow_smem(kernel<2>);                                                                      \
+      kernel<2><<<(grid), kWalkThreads, (size_t)(d_v1) * sizeof(double), (stream)>>>(__VA_ARGS__); \
+    } else {                                                                                      \
+      kernel<1><<<(grid), kWalkThreads, 0, (stream)>>>(__VA_ARGS__);                              \
+    }                                                                                             \
   } while (0)
 
 int check_aligned(const void* v) {
@@ -975,7 +1028,7 @@ int ucp_gauss_moments_grid(const double* s, int64_t n, const double* v, double a
   if (n == 0) return UCP_OK;
   if (int rc_ = check_aligned(v)) return rc_;
   WalkGrid g = make_walk_grid(a, h, d);
-  UCP_WALK_LAUNCH(k_gauss_grid, n, nblocks(n, kWalkThreads), as_stream(stream), s, n, v, g, t0, t1, t2);
+  UCP_WALK_LAUNCH(k_gauss_grid, n, nblocks(n, kWalkThreads), as_stream(stream), d, s, n, v, g, t0, t1, t2);
   UCP_LAUNCHED("k_gauss_grid");
   return UCP_OK;
 }
@@ -1029,7 +1082,7 @@ int ucp_wc_stage0_cost(const ucp_wc_problem* P, const double* v1, const double* 
   const int64_t n_host = n_cand;
   if (int rc_ = check_aligned(v1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
-  UCP_WALK_LAUNCH(k_stage0_segmented, n_host, nblocks(n_host, kWalkThreads), as_stream(stream), u_flat, offsets, nseg, y_seg,
+  UCP_WALK_LAUNCH(k_stage0_segmented, n_host, nblocks(n_host, kWalkThreads), as_stream(stream), P->d1, u_flat, offsets, nseg, y_seg,
                                                                            f0_seg, P->k, v1, g, out);
   UCP_LAUNCHED("k_stage0_segmented");
   return UCP_OK;
@@ -1073,10 +1126,10 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
     if ((rc = ws_get(ws, WS_COST, sizeof(double) * 3 * (size_t)n, &pc))) return rc;
     if (int rc_ = check_aligned(u1)) return rc_;
     WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
-    UCP_WALK_LAUNCH(k_lu0_probe, 3 * n, nblocks(3 * n, kWalkThreads), st, P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
+    UCP_WALK_LAUNCH(k_lu0_probe, 3 * n, nblocks(3 * n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
                                                      (double*)pc);
     UCP_LAUNCHED("k_lu0_probe");
-    UCP_WALK_LAUNCH(k_lu0_finish, n, nblocks(n, kWalkThreads), st, P->y0, P->f0, u0, P->k, u1, g, *lp, begin, n,
+    UCP_WALK_LAUNCH(k_lu0_finish, n, nblocks(n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, *lp, begin, n,
                                                   (const double*)pc, out, err);
     UCP_LAUNCHED("k_lu0_finish");
     return UCP_OK;
@@ -1154,7 +1207,7 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
   UCP_LAUNCHED("k_ex_fill");
   if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
-  UCP_WALK_LAUNCH(k_ex0_eval, total, nblocks(total, kWalkThreads), st, P->y0, P->f0, u0, P->k, u1, g, counts + n,
+  UCP_WALK_LAUNCH(k_ex0_eval, total, nblocks(total, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, counts + n,
                                                   (const int32_t*)ppt, (const int32_t*)pj, (double*)pc);
   UCP_LAUNCHED("k_ex0_eval");
   k_ex_argmin<<<nblocks(n, 256), 256, 0, st>>>(u0, (const double*)pc, counts, (const int32_t*)pj, begin, n,
@@ -1204,7 +1257,7 @@ int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const doub
   if (end == begin) return UCP_OK;
   if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
-  UCP_WALK_LAUNCH(k_obj_terms, end - begin, nblocks(end - begin, kWalkThreads), as_stream(stream), P->y0, P->f0, u0, P->k, u1, g,
+  UCP_WALK_LAUNCH(k_obj_terms, end - begin, nblocks(end - begin, kWalkThreads), as_stream(stream), P->d1, P->y0, P->f0, u0, P->k, u1, g,
                                                                           begin, end, terms, err);
   UCP_LAUNCHED("k_obj_terms");
   return UCP_OK;
