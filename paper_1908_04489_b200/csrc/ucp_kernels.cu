@@ -686,7 +686,7 @@ k_mom_pairs(const double* __restrict__ yq, int64_t n, const double* __restrict__
   for (int r = threadIdx.x; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
   __syncthreads();
   const ucp_exp_entry* stab2 = reinterpret_cast<const ucp_exp_entry*>(stab);
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t q = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const double yt = yq[q];
   long long j = (long long)ceil((yt - a) / h - 0.5);
@@ -695,7 +695,7 @@ k_mom_pairs(const double* __restrict__ yq, int64_t n, const double* __restrict__
   const bool at_left = j == 0, at_right = j == d - 1;
   const double factor = (at_left || at_right) ? 0.5 : 1.0;
   const double INV = inv_sqrt_2pi();
-  const int64_t i0 = (int64_t)blockIdx.y * kPairChunk;
+  const int64_t i0 = (int64_t)blockIdx.x * kPairChunk;
   const int64_t i1 = i0 + kPairChunk < m ? i0 + kPairChunk : m;
   for (int64_t i = i0; i < i1; ++i) {
     const double xi = x[i];
@@ -733,18 +733,15 @@ k_mom_accum(const double* __restrict__ pre, int64_t n, const double* __restrict_
       for (int k = 0; k < kB; ++k) pv[k] = (active && r0 + k < cnt) ? __ldcs(col + (base + r0 + k) * n) : 0.0;
 #pragma unroll
       for (int k = 0; k < kB; ++k) {
-        // Branch-free form of `if (wp != 0) { wp *= w; acc += ... }`: a
-        // skipped pair contributes exact zeros (operands selected to 0.0,
-        // so no NaN from w or x), and acc + (+-0) == acc because an
-        // accumulator that starts at +0.0 can never become -0.0 under
-        // round-to-nearest.  Lets the compiler overlap consecutive pairs.
-        const bool live = pv[k] != 0.0;  // padding slots are 0.0
-        const double wp = live ? pv[k] * sw[r0 + k] : 0.0;
-        const double xi = live ? sx[r0 + k] : 0.0;
-        acc0 += wp;
-        const double wx = wp * xi;
-        acc1 += wx;
-        acc2 += wx * xi;
+        double wp = pv[k];
+        if (wp != 0.0) {  // kernels.py:481 (padding slots are 0.0)
+          const double xi = sx[r0 + k];
+          wp *= sw[r0 + k];
+          acc0 += wp;
+          const double wx = wp * xi;
+          acc1 += wx;
+          acc2 += wx * xi;
+        }
       }
     }
   }
@@ -898,7 +895,7 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   if (nq <= kTwoPhaseMaxQueries && nq * m <= kTwoPhaseMaxPairs) {
     void* ppre;
     if ((rc = ws_get(ws, WS_PAIRS, sizeof(double) * (size_t)(nq * m), &ppre))) return rc;
-    dim3 grid_a(nblocks(nq, 128), (unsigned)((m + kPairChunk - 1) / kPairChunk));
+    dim3 grid_a((unsigned)((m + kPairChunk - 1) / kPairChunk), nblocks(nq, 128));
     k_mom_pairs<<<grid_a, 128, 0, st>>>(yq, nq, (const double*)px1, (const double2*)ptails, m, a, h, d,
                                         (double*)ppre);
     UCP_LAUNCHED("k_mom_pairs");
