@@ -22,7 +22,7 @@ from .grids import (
     window_bounds,
     window_indices,
 )
-from .numerics import Density, Gaussian, Uniform, pdf, trapezoid
+from .numerics import Density, Gaussian, Uniform, fd_first, fd_second, pdf, trapezoid
 from .problem import NumericError, Problem
 from .solver import (
     RoundReport,
@@ -36,6 +36,7 @@ from .solver import (
     solve,
     solve_many,
 )
+from .verify import OracleConfig, exhaustive_argmin, windowed_argmin
 from .witsenhausen import Witsenhausen
 from .config5 import Inventory, ZeroDelay
 
@@ -68,7 +69,8 @@ __all__ = [
     "BACKEND", "ControllerSet", "Density", "Gaussian", "Grid", "LOCAL", "NumericError", "Problem",
     "REGISTRY", "RoundReport", "SampledController", "Sharding", "SolveResult", "SolverConfig", "Uniform",
     "Witsenhausen", "ZeroDelay", "Inventory", "adaptive_allocation", "eval_controller", "eval_controller_many", "from_process_group",
-    "init_identity", "local_update_phase", "make_grid", "make_problem", "max_workers", "nearest_index",
+    "init_identity", "local_update_phase", "fd_first", "fd_second", "OracleConfig", "exhaustive_argmin",
+    "windowed_argmin", "make_grid", "make_problem", "max_workers", "nearest_index",
     "nearest_indices", "newton_or_gradient_step", "node_window_bounds", "partial_exhaustion_phase", "pdf",
     "run_block", "set_workers", "solve", "solve_many", "trapezoid", "window_bounds", "window_indices", "__version__",
 ]
