@@ -192,6 +192,11 @@ class ZeroDelay(_DeviceSweeps, Problem):
     def default_grid_specs(self):
         return [(-5.0, 5.0, 2000), (-6.0, 6.0, 2000)]
 
+    def derivatives_batch(self, m, u, y, U, h):
+        # zero_delay.py:56-65: probe at least one decoder cell wide (the device
+        # local update applies the same floor)
+        return super().derivatives_batch(m, u, y, U, np.maximum(h, self.grids[1].spacing))
+
     def _override_host_constants(self, f0, fw0):
         if self._dev is not None:
             raise RuntimeError("device context already created")
@@ -257,6 +262,13 @@ class Inventory(_DeviceSweeps, Problem):
 
     def default_grid_specs(self):
         return [(-3.0, 3.0, 601)] * self.stages
+
+    def _state_grid(self, mm):  # inventory.py:74-76
+        return self.grids[min(mm, self.stages - 1)]
+
+    def derivatives_batch(self, m, u, y, U, h):
+        # inventory.py:131-136: probe at least one next-stage state cell wide
+        return super().derivatives_batch(m, u, y, U, np.maximum(h, self._state_grid(m + 1).spacing))
 
     def gamma(self, x):
         x = np.asarray(x, dtype=np.float64)
