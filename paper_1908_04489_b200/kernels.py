@@ -8,6 +8,7 @@ libucp_b200 kernel -- there is no NumPy or CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 import torch
@@ -29,7 +30,7 @@ __all__ = [
 
 BACKEND = "b200"
 GAUSS_CUT = 12.0
-_WS = {}
+_TLS = threading.local()  # one scratch workspace per (host thread, device)
 
 
 def max_workers() -> int:
@@ -51,12 +52,14 @@ def _device_of(*xs):
 
 
 def _workspace(device):
-    key = device.index
-    if key not in _WS:
+    cache = getattr(_TLS, "ws", None)
+    if cache is None:
+        cache = _TLS.ws = {}
+    if device.index not in cache:
         ws = ctypes.c_void_p()
         _lib.call("ucp_workspace_create", ctypes.byref(ws))
-        _WS[key] = ws
-    return _WS[key]
+        cache[device.index] = ws
+    return cache[device.index]
 
 
 def _out(t, keep):
