@@ -297,6 +297,17 @@ def run_ours(args):
     c1 = {"config": f"d={C1_D} default SolverConfig, identity init", "wall_s": time.perf_counter() - t,
           "rounds": res.total_rounds, "J": res.final_objective, "termination": res.termination}
     u0h, u1h = resample(res.controllers.values(0), d), resample(res.controllers.values(1), d)
+    # the paper's grid size (d=14000): the reference needs 1,437 s on 8 cores
+    pp = P.Witsenhausen(k=K_WC, sigma=SIGMA, grids=[(*SPAN, 14000), (*SPAN, 14000)])
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    rp = P.solve(pp, P.SolverConfig(), sharding=sh)
+    torch.cuda.synchronize()
+    paper = {"config": "d=14000 (paper size) default SolverConfig, identity init",
+             "wall_s": time.perf_counter() - t, "rounds": rp.total_rounds, "J": rp.final_objective,
+             "termination": rp.termination, "reference_cpu_s": 1437.4,
+             "reference_cpu": "numba reference, 8-core Xeon (SURVEY.md Appendix B)"}
+    del pp, rp
 
     prob = P.Witsenhausen(k=K_WC, sigma=SIGMA, grids=[(*SPAN, d), (*SPAN, d)])
     h = prob.grids[0].spacing
@@ -444,7 +455,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(args, d, counts),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "phase_ms": dict(zip(["local0", "local1", "exh0", "exh1", "objective"], phase_ms.round(3).tolist())),
-            "time_to_converge": c1, "gpu": torch.cuda.get_device_name(dev),
+            "time_to_converge": c1, "time_to_converge_paper_size": paper, "gpu": torch.cuda.get_device_name(dev),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
