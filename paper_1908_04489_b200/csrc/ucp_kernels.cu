@@ -499,8 +499,9 @@ constexpr int kTile = 256;  // support points per shared-memory tile
 // serial loop: same operands, same bits), and per-tile min/max of x1 for
 // tile skipping (a tile holding a NaN is never skipped: NaN contributes to
 // the tail-weighted edge queries).
-__global__ void k_x1_prepare(const double* __restrict__ y0, const double* __restrict__ u0, int64_t d0,
-                             double a, double h, double b, double* x1, double2* tails, double2* tile_mm) {
+__global__ void k_x1_prepare(const double* __restrict__ y0, const double* __restrict__ u0,
+                             const double* __restrict__ w, int64_t d0, double a, double h, double b, double* x1,
+                             double2* xw, double2* tails, double2* tile_mm) {
   __shared__ double smin[kTile], smax[kTile];
   __shared__ int snan;
   if (threadIdx.x == 0) snan = 0;
@@ -511,8 +512,11 @@ __global__ void k_x1_prepare(const double* __restrict__ y0, const double* __rest
     x = y0 ? y0[i] + u0[i] : u0[i];
     x1[i] = x;
     tails[i] = make_double2(phi_cdf(a - x) / h, phi_cdf(x - b) / h);
+    xw[i] = make_double2(x, w[i]);
     if (isnan(x)) snan = 1;
     else mn = mx = x;
+  } else {
+    xw[i] = make_double2(INFINITY, 0.0);  // tile padding: out of range for every query
   }
   smin[threadIdx.x] = mn;
   smax[threadIdx.x] = mx;
@@ -526,6 +530,40 @@ __global__ void k_x1_prepare(const double* __restrict__ y0, const double* __rest
   }
   if (threadIdx.x == 0)
     tile_mm[blockIdx.x] = snan ? make_double2(-INFINITY, INFINITY) : make_double2(smin[0], smax[0]);
+}
+
+// ---- bulk async copy (TMA engine, cp.async.bulk) + mbarrier helpers ------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "UCP_MBAR_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra UCP_MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing on `bar` (bytes % 16 == 0, 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // One thread per query y; the CTA streams (x_i, w_i) tiles through shared
@@ -549,11 +587,13 @@ __global__ void k_x1_prepare(const double* __restrict__ y0, const double* __rest
 constexpr int kMomThreads = 128;
 constexpr int kMomUnroll = 4;
 __global__ void __launch_bounds__(kMomThreads, 6)
-k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x,
-          const double* __restrict__ w, const double2* __restrict__ tails, int64_t m,
-          const double2* __restrict__ tile_mm, double a, double h, int64_t d, double* o0, double* o1,
-          double* o2, int* work_counter) {
-  __shared__ double2 sxw[kTile];
+k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ xw,
+          const double2* __restrict__ tails, int64_t m, const double2* __restrict__ tile_mm, double a, double h,
+          int64_t d, double* o0, double* o1, double* o2, int* work_counter) {
+  // interior CTAs: (x, w) tiles arrive by bulk async copy (TMA engine) into a
+  // double buffer, the next non-skipped tile in flight while this one is used
+  __shared__ __align__(128) double2 sbuf[2][kTile];
+  __shared__ __align__(8) uint64_t sbar[2];
   __shared__ double2 slr[kTile];
   __shared__ __align__(16) uint64_t stab[256];
   __shared__ double s_ymin[kMomThreads / 32], s_ymax[kMomThreads / 32];
@@ -565,8 +605,14 @@ k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x
   const double b = a + h * (double)(d - 1);
   const double INV = inv_sqrt_2pi();
   const int64_t ntiles = (m + kTile - 1) / kTile;
-  if (threadIdx.x == 0) s_work = blockIdx.x;
+  if (threadIdx.x == 0) {
+    s_work = blockIdx.x;
+    mbar_init(&sbar[0], 1);
+    mbar_init(&sbar[1], 1);
+    mbar_init_fence();
+  }
   __syncthreads();
+  uint32_t phase0 = 0, phase1 = 0;  // completions seen per barrier (parity), CTA-uniform
   for (;;) {
     const int64_t k = s_work;
     if (k >= nqb) break;
@@ -602,23 +648,45 @@ k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x
     const bool has_left = s_left != 0, has_right = s_right != 0;
     const bool general = has_left || has_right;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-    for (int64_t tile = 0; tile < ntiles; ++tile) {
-      const double2 mm = tile_mm[tile];
-      const bool gauss_out = ymin - mm.y > kGaussCut || ymax - mm.x < -kGaussCut;
-      const bool left_out = !has_left || a - mm.x <= -kGaussCut;
-      const bool right_out = !has_right || mm.y - b <= -kGaussCut;
-      if (gauss_out && left_out && right_out) continue;  // CTA-uniform
-      const int64_t base = tile * kTile;
-      const int cnt = (int)(m - base < kTile ? m - base : kTile);
-      __syncthreads();
-      for (int r = threadIdx.x; r < kTile; r += kMomThreads) {
-        // padding slots are +inf: out of range for every query, never accumulated
-        sxw[r] = r < cnt ? make_double2(x[base + r], w[base + r]) : make_double2(INFINITY, 0.0);
-        if (general) slr[r] = r < cnt ? tails[base + r] : make_double2(0.0, 0.0);
+    // first tile >= t0 with a nonzero contribution to some query of the CTA
+    auto next_tile = [&](int64_t t0) -> int64_t {
+      for (int64_t tile = t0; tile < ntiles; ++tile) {
+        const double2 mm = tile_mm[tile];
+        const bool gauss_out = ymin - mm.y > kGaussCut || ymax - mm.x < -kGaussCut;
+        const bool left_out = !has_left || a - mm.x <= -kGaussCut;
+        const bool right_out = !has_right || mm.y - b <= -kGaussCut;
+        if (!(gauss_out && left_out && right_out)) return tile;
       }
-      __syncthreads();
-      if (!general) {
-        for (int r = 0; r < cnt; r += kMomUnroll) {
+      return ntiles;
+    };
+    constexpr uint32_t kTileBytes = kTile * sizeof(double2);
+    if (!general) {
+      int64_t tile = next_tile(0);
+      int cur = 0;
+      if (threadIdx.x == 0 && tile < ntiles) {
+        fence_proxy_async_smem();  // earlier generic reads of sbuf before the async refill
+        mbar_arrive_expect_tx(&sbar[0], kTileBytes);
+        bulk_g2s(sbuf[0], xw + tile * kTile, kTileBytes, &sbar[0]);
+      }
+      while (tile < ntiles) {
+        const int64_t nxt = next_tile(tile + 1);
+        if (cur == 0) {
+          mbar_wait(&sbar[0], phase0);
+          phase0 ^= 1u;
+        } else {
+          mbar_wait(&sbar[1], phase1);
+          phase1 ^= 1u;
+        }
+        if (threadIdx.x == 0 && nxt < ntiles) {
+          // every thread finished reading sbuf[cur ^ 1] (barrier at the end of
+          // the previous iteration); order those generic reads before the
+          // async-proxy writes of the refill
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&sbar[cur ^ 1], kTileBytes);
+          bulk_g2s(sbuf[cur ^ 1], xw + nxt * kTile, kTileBytes, &sbar[cur ^ 1]);
+        }
+        const double2* sxw = sbuf[cur];
+        for (int r = 0; r < kTile; r += kMomUnroll) {  // padding is (+inf, 0): never accumulated
           double e[kMomUnroll];
           bool in[kMomUnroll];
 #pragma unroll
@@ -630,16 +698,30 @@ k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x
 #pragma unroll
           for (int q = 0; q < kMomUnroll; ++q) {
             if (in[q]) {
-              const double2 xw = sxw[r + q];
-              const double wp = (e[q] * INV) * xw.y;
+              const double2 xwq = sxw[r + q];
+              const double wp = (e[q] * INV) * xwq.y;
               acc0 += wp;
-              const double wx = wp * xw.x;
+              const double wx = wp * xwq.x;
               acc1 += wx;
-              acc2 += wx * xw.x;
+              acc2 += wx * xwq.x;
             }
           }
         }
-      } else {
+        __syncthreads();
+        cur ^= 1;
+        tile = nxt;
+      }
+    } else {
+      double2* sxw = sbuf[0];
+      for (int64_t tile = next_tile(0); tile < ntiles; tile = next_tile(tile + 1)) {
+        const int64_t base = tile * kTile;
+        const int cnt = (int)(m - base < kTile ? m - base : kTile);
+        __syncthreads();
+        for (int r = threadIdx.x; r < kTile; r += kMomThreads) {
+          sxw[r] = xw[base + r];
+          slr[r] = r < cnt ? tails[base + r] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();
         for (int r = 0; r < cnt; ++r) {
           const double xi = sxw[r].x;
           const double diff = yt - xi;
@@ -657,6 +739,8 @@ k_moments(const double* __restrict__ yq, int64_t n, const double* __restrict__ x
           }
         }
       }
+      __syncthreads();
+      fence_proxy_async_smem();  // generic writes to sbuf[0] before later bulk copies into it
     }
     if (active) {
       o0[t] = acc0;
@@ -854,7 +938,7 @@ struct ucp_workspace {
 namespace {
 enum {
   WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS, WS_PAIRS,
-  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_NSLOTS
+  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_NSLOTS
 };
 static_assert(WS_NSLOTS <= 16, "workspace slots");
 // two-phase moments when the query set cannot fill the GPU with the direct kernel
@@ -883,14 +967,16 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   if (nq <= 0) return UCP_OK;
   void *px1, *ptile, *pctr, *ptails;
   int rc;
+  int64_t ntiles = (m + kTile - 1) / kTile;
+  void* pxw;
   if ((rc = ws_get(ws, WS_X1, sizeof(double) * (size_t)m, &px1))) return rc;
   if ((rc = ws_get(ws, WS_TAILS, sizeof(double2) * (size_t)m, &ptails))) return rc;
-  int64_t ntiles = (m + kTile - 1) / kTile;
+  if ((rc = ws_get(ws, WS_XW, sizeof(double2) * (size_t)(ntiles * kTile), &pxw))) return rc;
   if ((rc = ws_get(ws, WS_TILE, sizeof(double2) * (size_t)ntiles, &ptile))) return rc;
   if ((rc = ws_get(ws, WS_TOTAL, sizeof(int64_t) * 2, &pctr))) return rc;
   const double b = a + h * (double)(d - 1);
-  k_x1_prepare<<<(unsigned)ntiles, kTile, 0, st>>>(y0, u0, m, a, h, b, (double*)px1, (double2*)ptails,
-                                                   (double2*)ptile);
+  k_x1_prepare<<<(unsigned)ntiles, kTile, 0, st>>>(y0, u0, w, m, a, h, b, (double*)px1, (double2*)pxw,
+                                                   (double2*)ptails, (double2*)ptile);
   UCP_LAUNCHED("k_x1_prepare");
   if (nq <= kTwoPhaseMaxQueries && nq * m <= kTwoPhaseMaxPairs) {
     void* ppre;
@@ -912,7 +998,7 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   int64_t nqb = (nq + kMomThreads - 1) / kMomThreads;
   int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > nqb) grid = nqb;
-  k_moments<<<(unsigned)grid, kMomThreads, 0, st>>>(yq, nq, (const double*)px1, w, (const double2*)ptails, m,
+  k_moments<<<(unsigned)grid, kMomThreads, 0, st>>>(yq, nq, (const double2*)pxw, (const double2*)ptails, m,
                                                       (const double2*)ptile, a, h, d, o0, o1, o2, counter);
   UCP_LAUNCHED("k_moments");
   return UCP_OK;
