@@ -140,6 +140,16 @@ int ucp_wc_run_block(const ucp_wc_problem* P, int kind, int iters, double* u0, d
                      const int64_t* win_lo1, const int64_t* win_hi1, int64_t cand_bound0,
                      double* scratch0, double* scratch1, int64_t* err, ucp_workspace* ws,
                      void* stream);
+/* Same block as ucp_wc_run_block, with the iterations after the first
+ * replayed from a CUDA graph (captured once per block signature on a private
+ * stream, launched on `stream`).  err6 = 3 slots per stage, the minimum over
+ * all iterations (the host re-runs the block eagerly to name the first
+ * failing phase).  Exhaustion blocks need cand_bound0 > 0 to be graphed. */
+int ucp_wc_run_block_graph(const ucp_wc_problem* P, int kind, int iters, double* u0, double* u1,
+                           const ucp_local_params* lp, const int64_t* win_lo0,
+                           const int64_t* win_hi0, const int64_t* win_lo1,
+                           const int64_t* win_hi1, int64_t cand_bound0, double* scratch0,
+                           double* scratch1, int64_t* err6, ucp_workspace* ws, void* stream);
 /* problem.py:110-127 objective, per-point part: terms[i] = C0(u0[i], y0[i])
  * for i in [begin, end); err[0] <- first non-finite term.  The serial
  * trapezoid over all terms is ucp_trapezoid_sum. */

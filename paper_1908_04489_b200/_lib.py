@@ -67,6 +67,9 @@ SIGNATURES = {
                                   c_vp, c_vp, c_vp, c_vp]),
     "ucp_wc_run_block": (c_int, [ctypes.POINTER(WcProblem), c_int, c_int, c_vp, c_vp, ctypes.POINTER(LocalParams),
                                  c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ucp_wc_run_block_graph": (c_int, [ctypes.POINTER(WcProblem), c_int, c_int, c_vp, c_vp,
+                                       ctypes.POINTER(LocalParams), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
+                                       c_vp, c_vp]),
     "ucp_wc_objective_terms": (c_int, [ctypes.POINTER(WcProblem), c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
                                        c_vp]),
     "ucp_fp64_probe": (c_int, [c_int, c_int, c_int, c_vp, c_vp]),

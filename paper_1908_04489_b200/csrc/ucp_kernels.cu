@@ -13,7 +13,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <array>
 #include <atomic>
+#include <vector>
 #include <mutex>
 #include <unordered_set>
 #include <cub/device/device_scan.cuh>
@@ -927,12 +929,19 @@ __global__ void k_fp64_probe(int iters, double* sink) {
 }  // namespace
 
 // ============================================================ workspace
+struct ucp_graph_entry {
+  std::array<uint64_t, 20> key;
+  cudaGraphExec_t exec;
+};
+
 struct ucp_workspace {
   void* buf[16] = {nullptr};
   size_t cap[16] = {0};
   void* scan_tmp = nullptr;
   size_t scan_cap = 0;
-  int64_t* h_total = nullptr;  // pinned
+  int64_t* h_total = nullptr;           // pinned
+  cudaStream_t cap_stream = nullptr;    // private stream for CUDA-graph capture
+  std::vector<ucp_graph_entry> graphs;  // one instantiated graph per block signature
 };
 
 namespace {
@@ -1084,6 +1093,8 @@ int ucp_workspace_destroy(ucp_workspace* ws) {
     if (ws->buf[i]) cudaFree(ws->buf[i]);
   if (ws->scan_tmp) cudaFree(ws->scan_tmp);
   if (ws->h_total) cudaFreeHost(ws->h_total);
+  for (auto& g : ws->graphs) cudaGraphExecDestroy(g.exec);
+  if (ws->cap_stream) cudaStreamDestroy(ws->cap_stream);
   delete ws;
   return UCP_OK;
 }
@@ -1328,6 +1339,96 @@ int ucp_wc_run_block(const ucp_wc_problem* P, int kind, int iters, double* u0, d
       if (rc) return rc;
       UCP_CHECK(cudaMemcpyAsync(u[m], scratch[m], sizeof(double) * (size_t)d[m], cudaMemcpyDeviceToDevice, st));
     }
+  }
+  return UCP_OK;
+}
+
+// One block iteration (both stages) on stream st; err6 = 3 slots per stage,
+// shared by every iteration (minimum over the block).
+static int block_iteration(const ucp_wc_problem* P, int kind, double* u0, double* u1, const ucp_local_params* lp,
+                           const int64_t* const lo[2], const int64_t* const hi[2], int64_t cand_bound0,
+                           double* const scratch[2], int64_t* err6, ucp_workspace* ws, cudaStream_t st) {
+  double* u[2] = {u0, u1};
+  const int64_t d[2] = {P->d0, P->d1};
+  for (int m = 0; m < 2; ++m) {
+    int rc;
+    if (kind == 0)
+      rc = ucp_wc_local_update(P, m, u0, u1, lp + m, 0, d[m], scratch[m], err6 + 3 * m, ws, st);
+    else
+      rc = ucp_wc_exhaustion(P, m, u0, u1, lo[m], hi[m], m == 0 ? cand_bound0 : 0, 0, d[m], scratch[m], err6 + 3 * m,
+                             ws, st);
+    if (rc) return rc;
+    UCP_CHECK(cudaMemcpyAsync(u[m], scratch[m], sizeof(double) * (size_t)d[m], cudaMemcpyDeviceToDevice, st));
+  }
+  return UCP_OK;
+}
+
+int ucp_wc_run_block_graph(const ucp_wc_problem* P, int kind, int iters, double* u0, double* u1,
+                           const ucp_local_params* lp, const int64_t* win_lo0, const int64_t* win_hi0,
+                           const int64_t* win_lo1, const int64_t* win_hi1, int64_t cand_bound0, double* scratch0,
+                           double* scratch1, int64_t* err6, ucp_workspace* ws, void* stream) {
+  int rc = check_problem(P);
+  if (rc) return rc;
+  if (kind < 0 || kind > 1 || iters < 0) return arg_fail("run_block_graph: bad kind/iters");
+  if (!u0 || !u1 || !scratch0 || !scratch1 || !err6 || !ws) return arg_fail("run_block_graph: null argument");
+  if (kind == 0 && !lp) return arg_fail("run_block_graph: local params missing");
+  if (kind == 1 && (!win_lo0 || !win_hi0 || !win_lo1 || !win_hi1))
+    return arg_fail("run_block_graph: windows missing");
+  if (iters == 0) return UCP_OK;
+  cudaStream_t st = as_stream(stream);
+  const int64_t* lo[2] = {win_lo0, win_lo1};
+  const int64_t* hi[2] = {win_hi0, win_hi1};
+  double* scratch[2] = {scratch0, scratch1};
+  // the first iteration runs eagerly: it sizes every workspace buffer, so the
+  // captured iteration never allocates (and proves the launch sequence)
+  if ((rc = block_iteration(P, kind, u0, u1, lp, lo, hi, cand_bound0, scratch, err6, ws, st))) return rc;
+  if (iters == 1) return UCP_OK;
+  const bool graphable = kind == 0 || (cand_bound0 > 0 && cand_bound0 <= kSyncFreeMaxCand);
+  if (!graphable) {  // exhaustion that must read its candidate count back: stay eager
+    for (int it = 1; it < iters; ++it)
+      if ((rc = block_iteration(P, kind, u0, u1, lp, lo, hi, cand_bound0, scratch, err6, ws, st))) return rc;
+    return UCP_OK;
+  }
+  std::array<uint64_t, 20> key{};
+  key[0] = (uint64_t)kind;
+  key[1] = (uint64_t)(uintptr_t)P;
+  key[2] = (uint64_t)(uintptr_t)u0;
+  key[3] = (uint64_t)(uintptr_t)u1;
+  key[4] = (uint64_t)(uintptr_t)scratch0;
+  key[5] = (uint64_t)(uintptr_t)scratch1;
+  key[6] = (uint64_t)(uintptr_t)err6;
+  key[7] = (uint64_t)(uintptr_t)win_lo0;
+  key[8] = (uint64_t)(uintptr_t)win_hi0;
+  key[9] = (uint64_t)(uintptr_t)win_lo1;
+  key[10] = (uint64_t)(uintptr_t)win_hi1;
+  key[11] = (uint64_t)cand_bound0;
+  if (lp) {
+    const double* lv = reinterpret_cast<const double*>(lp);
+    for (int k = 0; k < 8; ++k) key[12 + k] = ucp_asu64(lv[k]);
+  }
+  cudaGraphExec_t exec = nullptr;
+  for (auto& g : ws->graphs)
+    if (g.key == key) exec = g.exec;
+  if (!exec) {
+    if (!ws->cap_stream) UCP_CHECK(cudaStreamCreateWithFlags(&ws->cap_stream, cudaStreamNonBlocking));
+    UCP_CHECK(cudaStreamBeginCapture(ws->cap_stream, cudaStreamCaptureModeThreadLocal));
+    rc = block_iteration(P, kind, u0, u1, lp, lo, hi, cand_bound0, scratch, err6, ws, ws->cap_stream);
+    cudaGraph_t graph = nullptr;
+    cudaError_t ec = cudaStreamEndCapture(ws->cap_stream, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (ec != cudaSuccess) return cuda_fail(ec, "cudaStreamEndCapture");
+    ec = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ec != cudaSuccess) return cuda_fail(ec, "cudaGraphInstantiate");
+    ws->graphs.push_back({key, exec});
+  }
+  // kernel launches of one iteration == the graph's nodes (for the counter)
+  for (int it = 1; it < iters; ++it) {
+    UCP_CHECK(cudaGraphLaunch(exec, st));
+    g_launches.fetch_add(kind == 0 ? 6 : 10, std::memory_order_relaxed);
   }
   return UCP_OK;
 }

@@ -62,9 +62,17 @@ class ErrorLog:
         host = rows.cpu().numpy()
         rows.fill_(NO_ERROR)
         meta, self.meta = self.meta, []
-        for (kind, m), row in zip(meta, host):
-            if (row != NO_ERROR).any():
-                raise _phase_error(self.problem, kind, m, row)
+        for entry, row in zip(meta, host):
+            kind, m = entry[0], entry[1]
+            if not (row != NO_ERROR).any():
+                continue
+            if kind == "block":
+                # a graph-replayed block only records the minimum over its
+                # iterations: re-run it eagerly from its input snapshot so the
+                # first failing phase raises exactly the reference's error
+                self.problem._replay_block_error(entry[2], sharding)
+                raise AssertionError("block failure did not reproduce")
+            raise _phase_error(self.problem, kind, m, row)
 
 
 def _phase_error(problem, kind, m, row):

@@ -32,13 +32,38 @@ __all__ = ["Witsenhausen"]
 
 # below this many points shards are equal-sized (balancing would cost more than it saves)
 BALANCE_MIN_POINTS = int(os.environ.get("UCP_BALANCE_MIN_POINTS", 1 << 14))
+# replay block iterations from CUDA graphs (UCP_GRAPHS=0 disables)
+GRAPH_BLOCKS = os.environ.get("UCP_GRAPHS", "1") != "0"
 
 class _WcDevice(DeviceContext):
     """Device-resident constants and ABI struct of one Witsenhausen problem
     (plus the shared workspace / error log / window cache)."""
 
+    def graph_state(self) -> dict:
+        """Fixed-address buffers of the graph-replayed block executor."""
+        if self._graph_state is None:
+            d0, d1 = int(self.y0.numel()), int(self.y1.numel())
+            self._graph_state = {
+                "u0": torch.empty(d0, dtype=F64, device=self.device),
+                "u1": torch.empty(d1, dtype=F64, device=self.device),
+                "s0": torch.empty(d0, dtype=F64, device=self.device),
+                "s1": torch.empty(d1, dtype=F64, device=self.device),
+                "err": torch.full((6,), NO_ERROR, dtype=I64, device=self.device),
+            }
+        return self._graph_state
+
+    def block_params(self, cfg, g0, g1):
+        """ucp_local_params[2] for both stages, cached per config (stable address and bits)."""
+        key = (cfg.fd_step, cfg.curvature_min, cfg.grad_step, cfg.cap_for(g0), cfg.cap_for(g1))
+        if key not in self._lp_cache:
+            self._lp_cache[key] = (_lib.LocalParams * 2)(
+                *[_lib.LocalParams(cfg.fd_step, cfg.curvature_min, cfg.grad_step, cfg.cap_for(g)) for g in (g0, g1)])
+        return self._lp_cache[key]
+
     def __init__(self, prob: "Witsenhausen", device=None):
         super().__init__(prob, device)
+        self._graph_state = None
+        self._lp_cache: dict = {}
         g0, g1 = prob.grids
         self.y0 = to_device_f64(g0.points, self.device)
         self.y1 = to_device_f64(g1.points, self.device)
@@ -177,20 +202,20 @@ class Witsenhausen(Problem):
                   sharding.rank_ptr(buf, bounds), ptr(err), D.ws, D.stream)
         return sharding.gather(buf, bounds, g.d)
 
-    def device_run_block(self, kind: str, iters: int, U: ControllerSet, cfg) -> ControllerSet:
+    def device_run_block(self, kind: str, iters: int, U: ControllerSet, cfg, graphs: bool = True) -> ControllerSet:
         """`iters` iterations of one phase kind over both stages in ONE native
-        call (ucp_wc_run_block; solver.py:226-231), unsharded."""
+        call (solver.py:226-231), unsharded.  With ``graphs`` the iterations
+        after the first replay a CUDA graph captured once per block signature
+        (fixed per-problem state buffers), which removes the per-kernel launch
+        cost that dominates small grids."""
         from .grids import SampledController
 
         if iters <= 0:
             return U
         D = self.device_context()
         u0, u1 = self._uv(U)
-        out0, out1 = u0.clone(), u1.clone()
-        s0, s1 = torch.empty_like(out0), torch.empty_like(out1)
         g0, g1 = self.grids
-        lp = (_lib.LocalParams * 2)(*[_lib.LocalParams(cfg.fd_step, cfg.curvature_min, cfg.grad_step,
-                                                       cfg.cap_for(g)) for g in (g0, g1)])
+        lp = D.block_params(cfg, g0, g1)
         if kind == "local":
             code, wins, bound = 0, (None, None, None, None), 0
         else:
@@ -199,11 +224,30 @@ class Witsenhausen(Problem):
             lo1, hi1 = D.window(self, 1, cfg.radius_for(g1))
             wins = (ptr(lo0), ptr(hi0), ptr(lo1), ptr(hi1))
             bound = D.candidate_bound(self, 0, cfg.radius_for(g0), 0, g0.d)
-        err = D.errors.slots([(kind, m) for _ in range(iters) for m in (0, 1)], LOCAL)
-        _lib.call("ucp_wc_run_block", ctypes.byref(D.P), code, int(iters), ptr(out0), ptr(out1), lp, *wins, bound,
-                  ptr(s0), ptr(s1), ptr(err), D.ws, D.stream)
+        if graphs and iters > 1 and GRAPH_BLOCKS:
+            st = D.graph_state()
+            st["u0"].copy_(u0)
+            st["u1"].copy_(u1)
+            _lib.call("ucp_wc_run_block_graph", ctypes.byref(D.P), code, int(iters), ptr(st["u0"]), ptr(st["u1"]), lp,
+                      *wins, bound, ptr(st["s0"]), ptr(st["s1"]), ptr(st["err"]), D.ws, D.stream)
+            rows = D.errors.slots([("block", 0, (kind, iters, U, cfg)), ("block", 1, (kind, iters, U, cfg))], LOCAL)
+            rows.view(-1).copy_(st["err"])
+            st["err"].fill_(NO_ERROR)
+            out0, out1 = st["u0"].clone(), st["u1"].clone()
+        else:
+            out0, out1 = u0.clone(), u1.clone()
+            s0, s1 = torch.empty_like(out0), torch.empty_like(out1)
+            err = D.errors.slots([(kind, m) for _ in range(iters) for m in (0, 1)], LOCAL)
+            _lib.call("ucp_wc_run_block", ctypes.byref(D.P), code, int(iters), ptr(out0), ptr(out1), lp, *wins,
+                      bound, ptr(s0), ptr(s1), ptr(err), D.ws, D.stream)
         return ControllerSet((SampledController(g0, out0, _trusted_device=True),
                               SampledController(g1, out1, _trusted_device=True)))
+
+    def _replay_block_error(self, payload, sharding) -> None:
+        """Re-run a graph-replayed block eagerly (per-phase error slots) and raise its first failure."""
+        kind, iters, U, cfg = payload
+        self.device_run_block(kind, iters, U, cfg, graphs=False)
+        self.device_context().errors.flush(sharding)
 
     def device_objective(self, U: ControllerSet, sharding: Sharding = LOCAL) -> float:
         """problem.py:110-127: stage-0 integrand on device, then the serial trapezoid."""

@@ -284,3 +284,30 @@ def test_exhaustion_sync_and_syncfree_paths_agree(P, golden, monkeypatch):
         V = P.run_block(prob, U, cfg, 1, "local")
         V = P.run_block(prob, V, cfg, 1, "exhaustion")
         assert_bitwise(V.values(0), g["pert1_it_u0"], "it u0")
+
+
+@pytest.mark.parametrize("kind", ["local", "exhaustion"])
+def test_graph_replayed_blocks_bitwise_and_errors(P, golden, kind):
+    """Blocks replayed from CUDA graphs give the eager result bit for bit, and a
+    failure inside one raises exactly the eager (reference) error."""
+    g = golden("wc_d201")
+    prob = _wc(P, g)
+    cfg = P.SolverConfig()
+    U = _U(P, prob, g["pert1_u0"], g["pert1_u1"])
+    a = prob.device_run_block(kind, 4, U, cfg, graphs=True)
+    b = prob.device_run_block(kind, 4, U, cfg, graphs=False)
+    a2 = prob.device_run_block(kind, 3, a, cfg, graphs=True)  # graph reuse with new inputs
+    b2 = prob.device_run_block(kind, 3, b, cfg, graphs=False)
+    for m in (0, 1):
+        assert_bitwise(a2.values(m), b2.values(m), f"{kind} u{m}")
+    prob.flush_errors()
+    u1 = g["pert0_u1"].copy()
+    u1[150] = 1e200
+    bad = _U(P, prob, g["pert0_u0"], u1)
+    msgs = []
+    for graphs in (True, False):
+        prob.device_run_block(kind, 3, bad, cfg, graphs=graphs)
+        with pytest.raises(P.NumericError) as e:
+            prob.flush_errors()
+        msgs.append(str(e.value))
+    assert msgs[0] == msgs[1]
