@@ -958,6 +958,14 @@ constexpr int64_t kSyncFreeMaxCand = (int64_t)1 << 27;
 
 int ws_get(ucp_workspace* ws, int slot, size_t bytes, void** out) {
   if (ws->cap[slot] < bytes) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (ws->cap_stream && cudaStreamIsCapturing(ws->cap_stream, &cs) == cudaSuccess &&
+        cs != cudaStreamCaptureStatusNone)
+      return arg_fail("workspace growth during graph capture");
+    // captured graphs hold workspace addresses: growing a buffer retires them
+    // (an in-flight graph exec is freed asynchronously on completion)
+    for (auto& g : ws->graphs) cudaGraphExecDestroy(g.exec);
+    ws->graphs.clear();
     if (ws->buf[slot]) UCP_CHECK(cudaFree(ws->buf[slot]));
     ws->buf[slot] = nullptr;
     ws->cap[slot] = 0;
