@@ -59,6 +59,9 @@ def parse():
                     help="target CPU seconds of the cpu_baseline sample (ours) / per step (reference)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--backend", default="nccl", help="process-group backend for N>1 (gloo: plumbing tests only)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="all ranks on cuda:0 (multi-rank plumbing test on a one-GPU box, gloo only)")
     return ap.parse_args()
 
 
@@ -275,11 +278,14 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    local_rank = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
     import paper_1908_04489_b200 as P
     from paper_1908_04489_b200 import _lib
     from paper_1908_04489_b200._device import ptr
