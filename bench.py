@@ -227,6 +227,7 @@ def run_reference(args):
     from oracle import oracle as orc
 
     orc.build()
+    orc.set_threads(os.cpu_count() or 1)  # torchrun exports OMP_NUM_THREADS=1; use every host core
     d = 1 << args.log2d
     u0c, u1c, c1 = c1_oracle_solve(orc)
     u0, u1 = resample(u0c, d), resample(u1c, d)
@@ -448,6 +449,7 @@ def run_ours(args):
             from oracle import oracle as orc
 
             orc.build()
+            orc.set_threads(os.cpu_count() or 1)
             p = orc.OracleWitsenhausen(k=K_WC, sigma=SIGMA, grid0=(*SPAN, d), grid1=(*SPAN, d),
                                        f0=prob._f0, fw0=prob._fw0)
             sec, times, thr, sample = cpu_step_seconds(orc, p, u0h, u1h, d, cfg.radius_for(prob.grids[0]),
