@@ -1033,7 +1033,7 @@ bool walk_latency_mode(int64_t n_walks) {
 }
 
 // kSmemWalkMax doubles of v1 fit the opt-in shared memory of one CTA
-constexpr int64_t kSmemWalkMax = 12288;
+constexpr int64_t kSmemWalkMax = 27648;  // 216 KiB of the 227 KiB opt-in per CTA
 
 std::mutex g_smem_mu;
 std::unordered_set<const void*> g_smem_ok;
