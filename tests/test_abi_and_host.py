@@ -94,6 +94,14 @@ def test_solver_config_validation_and_allocation():
     assert P.adaptive_allocation(1.0, 0.0, 20) == (19, 1)
     assert P.adaptive_allocation(0.0, 1.0, 20) == (1, 19)
     assert P.adaptive_allocation(3.0, 1.0, 20) == (15, 5)
+    assert P.adaptive_allocation(1, 1, 20) == (10, 10) and P.adaptive_allocation(0, 5, 20) == (1, 19)
+    rng = np.random.default_rng(10)  # acceptance criterion 10: invariants over 10^4 triples
+    for _ in range(10_000):
+        n = int(rng.integers(2, 100))
+        gl = float(rng.uniform(0, 1e4)) * (rng.random() > 0.05)
+        gp = float(rng.uniform(0, 1e4)) * (rng.random() > 0.05)
+        nl, npp = P.adaptive_allocation(gl, gp, n)
+        assert nl + npp == n and 1 <= nl <= n - 1
     g = P.make_grid(-25, 25, 2000)
     assert P.SolverConfig().radius_for(g) == 0.5 and P.SolverConfig().cap_for(g) == 5.0
 
