@@ -229,6 +229,48 @@ int ucp_inv_objective_terms(const ucp_inv_problem* P, const double* const* u, in
 int ucp_inv_forward_density(const ucp_inv_problem* P, int stage, const double* const* u, double* out,
                             ucp_workspace* ws, void* stream);
 
+/* ---- Monte-Carlo objective ------------------------------
+ * Replaces oracle.monte_carlo_objective (oracle.py:98-105) over the problems'
+ * simulate_cost (witsenhausen.py:81-89, zero_delay.py:88-94,
+ * inventory.py:152-166).  Draw streams, in the order simulate_cost consumes
+ * the generator: witsenhausen (x0 ~ N(0, sigma), w ~ N(0, 1)); zero_delay
+ * (x0 ~ N(0, 1), w ~ U(-1, 1)); inventory (x ~ U(-1, 1), then w_m ~ U(-1, 1)
+ * for m < stages). */
+#define UCP_MC_WITSENHAUSEN 0
+#define UCP_MC_ZERO_DELAY 1
+#define UCP_MC_INVENTORY 2
+#define UCP_MC_CHUNK 4096 /* samples per partial sum (fixes the reduction order) */
+typedef struct ucp_mc_problem {
+  int32_t kind;   /* UCP_MC_* */
+  int32_t stages; /* inventory stage count (2 otherwise) */
+  double k, sigma;      /* witsenhausen */
+  double power_weight;  /* zero_delay */
+  int32_t quadratic;    /* inventory stage_cost: 0 piecewise_linear, 1 quadratic */
+  int32_t reserved;
+  double order_cost, holding_rate, backlog_rate;
+  double a[UCP_INV_MAX_STAGES]; /* stage grids: a, spacing, d */
+  double h[UCP_INV_MAX_STAGES];
+  int64_t d[UCP_INV_MAX_STAGES];
+  const double* pts[UCP_INV_MAX_STAGES]; /* device grid points (inventory state snapping) */
+  const double* u[UCP_INV_MAX_STAGES];   /* device controller values */
+} ucp_mc_problem;
+/* number of draw streams S per sample (or -1 on a bad problem) */
+int ucp_mc_streams(const ucp_mc_problem* P);
+/* per-sample costs from caller-supplied draws laid out [S][n] (e.g. drawn on
+ * the host by the reference's NumPy generator): bitwise simulate_cost */
+int ucp_mc_costs(const ucp_mc_problem* P, const double* draws, int64_t n, double* costs, void* stream);
+/* the device generator's draws for samples [begin, end), laid out [S][end-begin]
+ * (Philox4x32-10, counter (i, stream), key = seed; Box-Muller for normals) */
+int ucp_mc_philox_draws(const ucp_mc_problem* P, uint64_t seed, int64_t begin, int64_t end, double* draws,
+                        void* stream);
+/* fixed-order partial sums over chunks [chunk_begin, chunk_end) of n samples:
+ * total == NULL -> sum of costs; else sum of (cost - *total / n)^2.
+ * partials[c - chunk_begin] per chunk. */
+int ucp_mc_partials(const ucp_mc_problem* P, uint64_t seed, int64_t n, int64_t chunk_begin, int64_t chunk_end,
+                    const double* total, double* partials, void* stream);
+/* fixed-order sum of n partials into *out (device) */
+int ucp_mc_reduce(const double* partials, int64_t n, double* out, void* stream);
+
 /* ---- instrumentation ------------------------------------------------------
  * FP64 pipe throughput probe (no FMA: DMUL/DADD only, 8 independent chains
  * per thread).  Performs iters*16 DP ops per thread; sink must hold

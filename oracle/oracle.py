@@ -519,6 +519,158 @@ def solve(p, cfg: OracleConfig | None = None, u0=None, u1=None):
     return Us[0], Us[1], J, rounds, term
 
 
+# ---- Monte-Carlo objective (oracle.py:98-105) -------------------------------
+
+
+def simulate_cost(p, Us, draws):
+    """Per-sample simulated cost from pre-drawn variates ``draws[s][i]``, the
+    generator outputs in the order the reference's ``simulate_cost`` consumes
+    them; the expressions are the reference's, NumPy elementwise."""
+    draws = [np.asarray(d, dtype=np.float64) for d in draws]
+    if p.name == "witsenhausen":  # problems/witsenhausen.py:81-89
+        _, a0, h0, d0 = p.grid(0)
+        _, a1, h1, d1 = p.grid(1)
+        x0 = draws[0]
+        u0 = np.asarray(Us[0])[nearest_idx(None, a0, h0, d0, x0)]
+        x1 = x0 + u0
+        w = draws[1]
+        u1 = np.asarray(Us[1])[nearest_idx(None, a1, h1, d1, x1 + w)]
+        x2 = x1 - u1
+        return p.k * p.k * u0 * u0 + x2 * x2
+    if p.name == "zero_delay":  # problems/zero_delay.py:88-94
+        _, a0, h0, d0 = p.grid(0)
+        _, a1, h1, d1 = p.grid(1)
+        x0 = draws[0]
+        u0 = np.asarray(Us[0])[nearest_idx(None, a0, h0, d0, x0)]
+        w = draws[1]
+        u1 = np.asarray(Us[1])[nearest_idx(None, a1, h1, d1, u0 + w)]
+        err = u1 - x0
+        return p.pw * u0 * u0 + err * err
+    # problems/inventory.py:152-166 (stock snapped to the state grid each stage)
+    g0 = p.state(0)
+    x = g0[0][nearest_idx(None, g0[1], g0[2], g0[3], draws[0])]
+    total = np.zeros(x.size)
+    for mm in range(p.M):
+        gm = p.grid(mm)
+        u = np.asarray(Us[mm])[nearest_idx(None, gm[1], gm[2], gm[3], x)]
+        w = draws[1 + mm]
+        gn = p.state(mm + 1)
+        x = gn[0][nearest_idx(None, gn[1], gn[2], gn[3], x + u - w)]
+        total += p.oc * u + p.gamma(x)
+    return total
+
+
+# Philox4x32-10 (Salmon et al., SC'11 "Parallel random numbers: as easy as
+# 1, 2, 3"), the device generator of device_monte_carlo_objective: restated
+# here so its stream is checked bit for bit.  No reference analogue -- the
+# reference draws with NumPy's PCG64, which the bitwise estimator uses.
+_PH_M0, _PH_M1, _PH_W0, _PH_W1, _U32 = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85, 0xFFFFFFFF
+
+
+def philox4x32_10(c0, c1, c2, c3, k0, k1):
+    c = [np.asarray(v, dtype=np.uint64) & _U32 for v in (c0, c1, c2, c3)]
+    k0, k1 = np.uint64(k0 & _U32), np.uint64(k1 & _U32)
+    for _ in range(10):
+        p0 = np.uint64(_PH_M0) * c[0]
+        p1 = np.uint64(_PH_M1) * c[2]
+        c = [(p1 >> np.uint64(32)) ^ c[1] ^ k0, p1 & np.uint64(_U32), (p0 >> np.uint64(32)) ^ c[3] ^ k1,
+             p0 & np.uint64(_U32)]
+        k0 = np.uint64((int(k0) + _PH_W0) & _U32)
+        k1 = np.uint64((int(k1) + _PH_W1) & _U32)
+    return [v.astype(np.uint32) for v in c]
+
+
+def _u01(hi, lo):  # 53 bits -> (x + 0.5) * 2^-53, in (0, 1)
+    x = ((hi.astype(np.uint64) << np.uint64(32)) | lo.astype(np.uint64)) >> np.uint64(11)
+    return (x.astype(np.float64) + 0.5) * 2.0 ** -53
+
+
+def philox_uniform01(seed, idx, stream):
+    """The two unit uniforms of counter (idx, stream), key = seed."""
+    idx = np.asarray(idx, dtype=np.uint64)
+    w = philox4x32_10(idx & np.uint64(_U32), idx >> np.uint64(32), np.full(idx.shape, stream, np.uint64), 0,
+                      seed & _U32, (seed >> 32) & _U32)
+    return _u01(w[0], w[1]), _u01(w[2], w[3])
+
+
+def philox_draws(p, seed, begin, end):
+    """Device draw streams for samples [begin, end): uniforms lo + (hi - lo) u
+    (bitwise), normals loc + scale * sqrt(-2 ln u1) cos(2 pi u2) (Box-Muller;
+    the device's log/cospi round differently from NumPy's, so normals agree
+    to a few ulp, not bitwise)."""
+    idx = np.arange(begin, end, dtype=np.uint64)
+    seed = int(seed) & ((1 << 64) - 1)
+
+    def normal(s, loc, scale):
+        u1, u2 = philox_uniform01(seed, idx, s)
+        return loc + scale * (np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2))
+
+    def uniform(s, lo, hi):
+        return lo + (hi - lo) * philox_uniform01(seed, idx, s)[0]
+
+    if p.name == "witsenhausen":
+        return np.stack([normal(0, 0.0, p.sigma), normal(1, 0.0, 1.0)])
+    if p.name == "zero_delay":
+        return np.stack([normal(0, 0.0, 1.0), uniform(1, -1.0, 1.0)])
+    return np.stack([uniform(s, -1.0, 1.0) for s in range(p.M + 1)])
+
+
+def _shuffle_tree(a):
+    """Lane 0 of a 32-lane __shfl_down tree (offsets 16..1) over the last axis."""
+    a = a.copy()
+    for off in (16, 8, 4, 2, 1):
+        a[..., :off] = a[..., :off] + a[..., off:2 * off]
+    return a[..., 0]
+
+
+def mc_chunk_partials(values, chunk=4096, threads=256):
+    """The device's fixed-order partial sum per chunk of ``values``: thread t
+    sums elements t, t+threads, ... serially, lanes fold by shuffle tree,
+    warps in order (csrc/ucp_mc.cuh: k_mc_partials)."""
+    values = np.asarray(values, dtype=np.float64)
+    nch = -(-values.size // chunk)
+    v = np.zeros(nch * chunk)
+    v[: values.size] = values
+    v = v.reshape(nch, chunk // threads, threads)
+    acc = np.zeros((nch, threads))
+    for j in range(chunk // threads):
+        acc = acc + v[:, j, :]
+    warps = _shuffle_tree(acc.reshape(nch, threads // 32, 32))
+    s = warps[:, 0]
+    for w in range(1, threads // 32):
+        s = s + warps[:, w]
+    return s
+
+
+def mc_reduce(partials, threads=1024):
+    """k_mc_reduce's fixed-order sum of the chunk partials."""
+    partials = np.asarray(partials, dtype=np.float64)
+    rows = -(-partials.size // threads)
+    v = np.zeros(max(rows, 1) * threads)
+    v[: partials.size] = partials
+    v = v.reshape(-1, threads)
+    acc = np.zeros(threads)
+    for r in range(v.shape[0]):
+        acc = acc + v[r]
+    warps = _shuffle_tree(acc.reshape(threads // 32, 32))
+    s = warps[0]
+    for w in range(1, threads // 32):
+        s = s + warps[w]
+    return float(s)
+
+
+def mc_estimate(costs):
+    """Estimate and stderr of the device estimator from per-sample costs,
+    with the device's reduction order and two-pass variance."""
+    costs = np.asarray(costs, dtype=np.float64)
+    n = costs.size
+    total = mc_reduce(mc_chunk_partials(costs))
+    mean = total / n
+    dev = costs - mean
+    sq = mc_reduce(mc_chunk_partials(dev * dev))
+    return total / n, math.sqrt(sq / (n - 1)) / math.sqrt(n)
+
+
 def host_cpu_description() -> dict:
     model = "unknown"
     try:

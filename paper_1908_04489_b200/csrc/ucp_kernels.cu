@@ -1465,3 +1465,4 @@ int ucp_fp64_probe(int blocks, int threads, int iters, double* sink, void* strea
 }  // extern "C"
 
 #include "ucp_config5.cuh"
+#include "ucp_mc.cuh"

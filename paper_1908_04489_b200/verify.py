@@ -2,9 +2,10 @@
 
 ``windowed_argmin`` re-derives one point of a partial-exhaustion sweep with
 scalar ``marginal_cost`` evaluations (so a device sweep can be checked point
-by point), ``exhaustive_argmin`` scans a full value lattice.  The
-Monte-Carlo objective and the pinned closed forms of the reference's oracle
-are outside this package's scope.
+by point), ``exhaustive_argmin`` scans a full value lattice, and
+``monte_carlo_objective`` (montecarlo.py) estimates J by simulation with the
+reference's generator and the device's per-sample costs.  The pinned closed
+forms of the reference's oracle stay outside this package.
 """
 from __future__ import annotations
 
@@ -14,9 +15,10 @@ from dataclasses import dataclass
 import numpy as np
 
 from .grids import window_indices
+from .montecarlo import monte_carlo_objective
 from .problem import NumericError, Problem
 
-__all__ = ["OracleConfig", "exhaustive_argmin", "windowed_argmin"]
+__all__ = ["OracleConfig", "exhaustive_argmin", "windowed_argmin", "monte_carlo_objective"]
 
 
 @dataclass(frozen=True)
@@ -34,6 +36,8 @@ class OracleConfig:
             raise ValueError(f"oracle needs u_lo < u_hi (got {self.u_lo}, {self.u_hi})")
         if int(self.steps) != self.steps or self.steps < 2:
             raise ValueError(f"oracle.steps must be an integer of at least 2 (got {self.steps})")
+        if int(self.mc_samples) != self.mc_samples or self.mc_samples < 1:
+            raise ValueError(f"oracle.mc_samples must be a positive integer (got {self.mc_samples})")
 
     @property
     def step(self) -> float:

@@ -10,6 +10,7 @@ def assert_bitwise(a, b, what=""):
     a = np.atleast_1d(np.asarray(a, dtype=np.float64))
     b = np.atleast_1d(np.asarray(b, dtype=np.float64))
     assert a.shape == b.shape, (what, a.shape, b.shape)
+    a, b = a.ravel(), b.ravel()
     ba, bb = bits(a), bits(b)
     bad = np.flatnonzero(ba != bb)
     # NaNs compare equal regardless of payload

@@ -227,17 +227,62 @@ def config5_fixtures():
     generic_fixture(Inventory(), "inv_default", extra={"stages": 2, "stage_cost": "piecewise_linear"})
 
 
+class _Recorder:
+    """Wraps a NumPy Generator and records what simulate_cost draws."""
+
+    def __init__(self, rng):
+        self.rng, self.draws = rng, []
+
+    def normal(self, *a):
+        self.draws.append(self.rng.normal(*a))
+        return self.draws[-1]
+
+    def uniform(self, *a):
+        self.draws.append(self.rng.uniform(*a))
+        return self.draws[-1]
+
+
+def mc_fixture():
+    """simulate_cost / monte_carlo_objective (oracle.py:98-105) on small
+    problems: the recorded draws, per-sample costs and (estimate, stderr)."""
+    from ucpsolve.oracle import OracleConfig, monte_carlo_objective
+
+    out = {}
+    cases = {"wc": Witsenhausen(grids=[(-25.0, 25.0, 201)] * 2),
+             "zd": ZeroDelay(grids=[(-5.0, 5.0, 201), (-6.0, 6.0, 241)]),
+             "inv": Inventory(grids=[(-3.0, 3.0, 241)] * 2),
+             "inv3q": Inventory(stages=3, stage_cost="quadratic", order_cost=0.3,
+                                grids=[(-3.0, 3.0, 97), (-2.5, 3.5, 131), (-3.0, 2.0, 111)])}
+    for i, (tag, prob) in enumerate(cases.items()):
+        U = perturbed(prob, seed=30 + i, scale=0.4)
+        for m in range(prob.M):
+            out[f"{tag}_u{m}"] = U.values(m)
+        rec = _Recorder(np.random.default_rng(90 + i))
+        out[f"{tag}_costs"] = prob.simulate_cost(U, rec, 2000)
+        out[f"{tag}_draws"] = np.stack(rec.draws)
+        for n, seed in ((2000, 90 + i), (100_000, 7)):
+            est, se = monte_carlo_objective(prob, U, OracleConfig(mc_samples=n, seed=seed))
+            out[f"{tag}_mc_{n}_{seed}"] = np.array([est, se])
+        out[f"{tag}_J"] = prob.objective(U)
+    np.savez_compressed(OUT / "mc.npz", **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-big", action="store_true", help="skip the d=2000 solve and 2^20 samples")
+    ap.add_argument("--only", choices=["mc"], help="regenerate one fixture file only")
     args = ap.parse_args()
     OUT.mkdir(parents=True, exist_ok=True)
+    if args.only == "mc":
+        mc_fixture()
+        return
     meta = {"numpy": np.__version__, "backend": kernels.BACKEND}
     import numba
 
     meta["numba"] = numba.__version__
     kernels_fixture()
     config5_fixtures()
+    mc_fixture()
     wc_phase_fixture(201, "d201")
     wc_phase_fixture(2000, "d2000")
     _, w201 = wc_solve_fixture(201, "d201")
