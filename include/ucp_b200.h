@@ -260,7 +260,8 @@ int ucp_mc_streams(const ucp_mc_problem* P);
  * the host by the reference's NumPy generator): bitwise simulate_cost */
 int ucp_mc_costs(const ucp_mc_problem* P, const double* draws, int64_t n, double* costs, void* stream);
 /* the device generator's draws for samples [begin, end), laid out [S][end-begin]
- * (Philox4x32-10, counter (i, stream), key = seed; Box-Muller for normals) */
+ * (Philox4x32-10, key = seed: counter (i, c) gives uniforms U[i][2c], U[i][2c+1];
+ * normals by Box-Muller on (U[i][0], U[i][1]), cosine then sine) */
 int ucp_mc_philox_draws(const ucp_mc_problem* P, uint64_t seed, int64_t begin, int64_t end, double* draws,
                         void* stream);
 /* fixed-order partial sums over chunks [chunk_begin, chunk_end) of n samples:

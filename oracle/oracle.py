@@ -585,34 +585,38 @@ def _u01(hi, lo):  # 53 bits -> (x + 0.5) * 2^-53, in (0, 1)
     return (x.astype(np.float64) + 0.5) * 2.0 ** -53
 
 
-def philox_uniform01(seed, idx, stream):
-    """The two unit uniforms of counter (idx, stream), key = seed."""
+def philox_uniform01(seed, idx, c):
+    """Unit uniforms U[i][2c], U[i][2c+1] of counter (idx, c), key = seed."""
     idx = np.asarray(idx, dtype=np.uint64)
-    w = philox4x32_10(idx & np.uint64(_U32), idx >> np.uint64(32), np.full(idx.shape, stream, np.uint64), 0,
+    w = philox4x32_10(idx & np.uint64(_U32), idx >> np.uint64(32), np.full(idx.shape, c, np.uint64), 0,
                       seed & _U32, (seed >> 32) & _U32)
     return _u01(w[0], w[1]), _u01(w[2], w[3])
 
 
 def philox_draws(p, seed, begin, end):
-    """Device draw streams for samples [begin, end): uniforms lo + (hi - lo) u
-    (bitwise), normals loc + scale * sqrt(-2 ln u1) cos(2 pi u2) (Box-Muller;
-    the device's log/cospi round differently from NumPy's, so normals agree
-    to a few ulp, not bitwise)."""
+    """Device draw streams for samples [begin, end), in the reference's stream
+    layout (csrc/ucp_mc.cuh: k_mc_draws).  Uniforms lo + (hi - lo) U[i][k]
+    are bitwise; normals come from Box-Muller on (U[i][0], U[i][1]):
+    r = sqrt(-2 ln u1), z = r cos(2 pi u2) and r sin(2 pi u2) -- the device's
+    log/sincospi round differently from NumPy's, so normals agree to a few
+    ulp, not bitwise."""
     idx = np.arange(begin, end, dtype=np.uint64)
     seed = int(seed) & ((1 << 64) - 1)
 
-    def normal(s, loc, scale):
-        u1, u2 = philox_uniform01(seed, idx, s)
-        return loc + scale * (np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2))
+    def U(k):
+        return philox_uniform01(seed, idx, k >> 1)[k & 1]
 
-    def uniform(s, lo, hi):
-        return lo + (hi - lo) * philox_uniform01(seed, idx, s)[0]
+    def box_muller():
+        u1, u2 = philox_uniform01(seed, idx, 0)
+        r = np.sqrt(-2.0 * np.log(u1))
+        return r * np.cos(2.0 * np.pi * u2), r * np.sin(2.0 * np.pi * u2)
 
     if p.name == "witsenhausen":
-        return np.stack([normal(0, 0.0, p.sigma), normal(1, 0.0, 1.0)])
+        zc, zs = box_muller()
+        return np.stack([0.0 + p.sigma * zc, 0.0 + 1.0 * zs])
     if p.name == "zero_delay":
-        return np.stack([normal(0, 0.0, 1.0), uniform(1, -1.0, 1.0)])
-    return np.stack([uniform(s, -1.0, 1.0) for s in range(p.M + 1)])
+        return np.stack([0.0 + 1.0 * box_muller()[0], -1.0 + 2.0 * U(2)])
+    return np.stack([-1.0 + 2.0 * U(s) for s in range(p.M + 1)])
 
 
 def _shuffle_tree(a):

@@ -9,8 +9,8 @@
 //  * BufferDraws -- draws made on the host by the reference's own NumPy
 //    generator (PCG64), in the order simulate_cost consumes them.  Costs are
 //    then bitwise the reference's (same expressions, left to right, no FMA).
-//  * PhiloxDraws -- counter-based Philox4x32-10 on the device: the draw of
-//    stream s for sample i depends only on (seed, i, s), so any sharding of
+//  * PhiloxDraws -- counter-based Philox4x32-10 on the device: the draws of
+//    sample i depend only on (seed, i), so any sharding of
 //    the samples over ranks/CTAs yields the same costs, and the fixed-shape
 //    reduction below makes the estimate bitwise independent of the rank count.
 //
@@ -37,11 +37,23 @@ __device__ __forceinline__ int64_t mc_nearest(double y, double a, double h, int6
   return i > d - 1 ? d - 1 : i;
 }
 
+// Draw interface: uniform2 returns the uniforms of logical streams 2c and
+// 2c+1 (the second only if 2c+1 < S); normal2 a pair of normals for streams
+// (s0, s1); normal1 one normal.
 struct BufferDraws {
   const double* p;  // [streams][n]
   int64_t n;
-  __device__ __forceinline__ double normal(int64_t i, int s, double, double) const { return p[(int64_t)s * n + i]; }
-  __device__ __forceinline__ double uniform(int64_t i, int s, double, double) const { return p[(int64_t)s * n + i]; }
+  __device__ __forceinline__ double at(int64_t i, int s) const { return p[(int64_t)s * n + i]; }
+  __device__ __forceinline__ void normal2(int64_t i, double, double, double, double, double& a, double& b) const {
+    a = at(i, 0);
+    b = at(i, 1);
+  }
+  __device__ __forceinline__ double normal1(int64_t i, int s, double, double) const { return at(i, s); }
+  __device__ __forceinline__ double uniform1(int64_t i, int s, double, double) const { return at(i, s); }
+  __device__ __forceinline__ void uniform2(int64_t i, int c, int S, double, double, double out[2]) const {
+    out[0] = at(i, 2 * c);
+    out[1] = 2 * c + 1 < S ? at(i, 2 * c + 1) : 0.0;
+  }
 };
 
 __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
@@ -69,24 +81,47 @@ __device__ __forceinline__ double mc_u01(uint32_t hi, uint32_t lo) {
   return __dmul_rn(__dadd_rn((double)x, 0.5), 1.1102230246251565e-16);
 }
 
+// Device generator: counter (i, c) of Philox4x32-10 (key = seed) yields the
+// unit uniforms U[i][2c], U[i][2c+1].  Normals come from Box-Muller on the
+// pair (U[i][0], U[i][1]): r = sqrt(-2 ln u1), z_cos = r cos(2 pi u2),
+// z_sin = r sin(2 pi u2).
 struct PhiloxDraws {
   uint32_t k0, k1;
-  __device__ __forceinline__ void block(int64_t i, int s, uint32_t w[4]) const {
-    philox4x32_10((uint32_t)i, (uint32_t)((uint64_t)i >> 32), (uint32_t)s, 0u, k0, k1, w);
-  }
-  // Box-Muller (cosine branch): z = sqrt(-2 ln u1) cos(2 pi u2); N(loc, scale) = loc + scale z
-  __device__ __forceinline__ double normal(int64_t i, int s, double loc, double scale) const {
+  int ubase;  // logical uniform stream s reads U[i][s + ubase] (zero_delay: 1, past the Box-Muller pair)
+  __device__ __forceinline__ void pair(int64_t i, int c, double& u1, double& u2) const {
     uint32_t w[4];
-    block(i, s, w);
-    const double u1 = mc_u01(w[0], w[1]), u2 = mc_u01(w[2], w[3]);
+    philox4x32_10((uint32_t)i, (uint32_t)((uint64_t)i >> 32), (uint32_t)c, 0u, k0, k1, w);
+    u1 = mc_u01(w[0], w[1]);
+    u2 = mc_u01(w[2], w[3]);
+  }
+  __device__ __forceinline__ void normal2(int64_t i, double loc0, double sc0, double loc1, double sc1, double& a,
+                                          double& b) const {
+    double u1, u2, sn, cs;
+    pair(i, 0, u1, u2);
+    const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+    sincospi(__dmul_rn(2.0, u2), &sn, &cs);
+    a = __dadd_rn(loc0, __dmul_rn(sc0, __dmul_rn(r, cs)));
+    b = __dadd_rn(loc1, __dmul_rn(sc1, __dmul_rn(r, sn)));
+  }
+  // stream 0 only (the cosine normal of pair 0)
+  __device__ __forceinline__ double normal1(int64_t i, int, double loc, double scale) const {
+    double u1, u2;
+    pair(i, 0, u1, u2);
     const double z = __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cospi(__dmul_rn(2.0, u2)));
     return __dadd_rn(loc, __dmul_rn(scale, z));
   }
-  // numpy's uniform(lo, hi): lo + (hi - lo) * u
-  __device__ __forceinline__ double uniform(int64_t i, int s, double lo, double hi) const {
-    uint32_t w[4];
-    block(i, s, w);
-    return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), mc_u01(w[0], w[1])));
+  // numpy's uniform(lo, hi) = lo + (hi - lo) * u of logical stream s
+  __device__ __forceinline__ double uniform1(int64_t i, int s, double lo, double hi) const {
+    double u1, u2;
+    const int k = s + ubase;
+    pair(i, k >> 1, u1, u2);
+    return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), (k & 1) ? u2 : u1));
+  }
+  __device__ __forceinline__ void uniform2(int64_t i, int c, int, double lo, double hi, double out[2]) const {
+    double u1, u2;
+    pair(i, c, u1, u2);
+    out[0] = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u1));
+    out[1] = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u2));
   }
 };
 
@@ -99,29 +134,34 @@ __device__ __forceinline__ double mc_gamma(const ucp_mc_problem& P, double x) { 
 template <class Draws>
 __device__ __forceinline__ double mc_cost(const ucp_mc_problem& P, const Draws& D, int64_t i) {
   if (P.kind == UCP_MC_WITSENHAUSEN) {  // witsenhausen.py:81-89
-    const double x0 = D.normal(i, 0, 0.0, P.sigma);
+    double x0, w;
+    D.normal2(i, 0.0, P.sigma, 0.0, 1.0, x0, w);
     const double u0 = P.u[0][mc_nearest(x0, P.a[0], P.h[0], P.d[0])];
     const double x1 = __dadd_rn(x0, u0);
-    const double w = D.normal(i, 1, 0.0, 1.0);
     const double u1 = P.u[1][mc_nearest(__dadd_rn(x1, w), P.a[1], P.h[1], P.d[1])];
     const double x2 = __dsub_rn(x1, u1);
     return __dadd_rn(__dmul_rn(__dmul_rn(__dmul_rn(P.k, P.k), u0), u0), __dmul_rn(x2, x2));
   }
   if (P.kind == UCP_MC_ZERO_DELAY) {  // zero_delay.py:88-94
-    const double x0 = D.normal(i, 0, 0.0, 1.0);
+    const double x0 = D.normal1(i, 0, 0.0, 1.0);
     const double u0 = P.u[0][mc_nearest(x0, P.a[0], P.h[0], P.d[0])];
-    const double w = D.uniform(i, 1, -1.0, 1.0);
+    const double w = D.uniform1(i, 1, -1.0, 1.0);
     const double u1 = P.u[1][mc_nearest(__dadd_rn(u0, w), P.a[1], P.h[1], P.d[1])];
     const double err = __dsub_rn(u1, x0);
     return __dadd_rn(__dmul_rn(__dmul_rn(P.power_weight, u0), u0), __dmul_rn(err, err));
   }
-  // inventory.py:152-166: stock snaps to the state grid at every boundary
-  const int M = P.stages;
-  double x = P.pts[0][mc_nearest(D.uniform(i, 0, -1.0, 1.0), P.a[0], P.h[0], P.d[0])];
+  // inventory.py:152-166: stock snaps to the state grid at every boundary;
+  // uniforms U[0] (initial stock) and U[1 + mm] (demand of stage mm), two per draw
+  const int M = P.stages, S = M + 1;
+  double u2[2];
+  D.uniform2(i, 0, S, -1.0, 1.0, u2);
+  double x = P.pts[0][mc_nearest(u2[0], P.a[0], P.h[0], P.d[0])];
   double total = 0.0;
   for (int mm = 0; mm < M; ++mm) {
     const double u = P.u[mm][mc_nearest(x, P.a[mm], P.h[mm], P.d[mm])];
-    const double w = D.uniform(i, 1 + mm, -1.0, 1.0);
+    const int s = 1 + mm;
+    if (s > 1 && !(s & 1)) D.uniform2(i, s >> 1, S, -1.0, 1.0, u2);
+    const double w = u2[s & 1];
     const int nx = mm + 1 < M ? mm + 1 : M - 1;
     x = P.pts[nx][mc_nearest(__dsub_rn(__dadd_rn(x, u), w), P.a[nx], P.h[nx], P.d[nx])];
     total = __dadd_rn(total, __dadd_rn(__dmul_rn(P.order_cost, u), mc_gamma(P, x)));
@@ -134,18 +174,19 @@ __global__ void k_mc_costs(const ucp_mc_problem P, BufferDraws D, int64_t n, dou
     out[i] = mc_cost(P, D, i);
 }
 
+// The device generator's draws in the reference's stream layout [S][n]
+// (BufferDraws order): what mc_cost consumes for each sample.
 __global__ void k_mc_draws(const ucp_mc_problem P, PhiloxDraws D, int64_t begin, int64_t end, double* __restrict__ out) {
   const int64_t n = end - begin;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = begin + t;
     if (P.kind == UCP_MC_WITSENHAUSEN) {
-      out[t] = D.normal(i, 0, 0.0, P.sigma);
-      out[n + t] = D.normal(i, 1, 0.0, 1.0);
+      D.normal2(i, 0.0, P.sigma, 0.0, 1.0, out[t], out[n + t]);
     } else if (P.kind == UCP_MC_ZERO_DELAY) {
-      out[t] = D.normal(i, 0, 0.0, 1.0);
-      out[n + t] = D.uniform(i, 1, -1.0, 1.0);
+      out[t] = D.normal1(i, 0, 0.0, 1.0);
+      out[n + t] = D.uniform1(i, 1, -1.0, 1.0);
     } else {
-      for (int s = 0; s <= P.stages; ++s) out[(int64_t)s * n + t] = D.uniform(i, s, -1.0, 1.0);
+      for (int s = 0; s <= P.stages; ++s) out[(int64_t)s * n + t] = D.uniform1(i, s, -1.0, 1.0);
     }
   }
 }
@@ -222,7 +263,9 @@ unsigned mc_grid(int64_t work, int threads) {
   return (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
-PhiloxDraws philox(uint64_t seed) { return PhiloxDraws{(uint32_t)seed, (uint32_t)(seed >> 32)}; }
+PhiloxDraws philox(const ucp_mc_problem* P, uint64_t seed) {
+  return PhiloxDraws{(uint32_t)seed, (uint32_t)(seed >> 32), P->kind == UCP_MC_ZERO_DELAY ? 1 : 0};
+}
 
 }  // namespace
 
@@ -249,7 +292,7 @@ int ucp_mc_philox_draws(const ucp_mc_problem* P, uint64_t seed, int64_t begin, i
   if ((rc = check_mc(P))) return rc;
   if (begin < 0 || end < begin || (end > begin && !draws)) return arg_fail("mc_philox_draws: bad range");
   if (end == begin) return UCP_OK;
-  k_mc_draws<<<mc_grid(end - begin, 256), 256, 0, as_stream(stream)>>>(*P, philox(seed), begin, end, draws);
+  k_mc_draws<<<mc_grid(end - begin, 256), 256, 0, as_stream(stream)>>>(*P, philox(P, seed), begin, end, draws);
   UCP_LAUNCHED("k_mc_draws");
   return UCP_OK;
 }
@@ -264,7 +307,7 @@ int ucp_mc_partials(const ucp_mc_problem* P, uint64_t seed, int64_t n, int64_t c
   if (chunk_end == chunk_begin) return UCP_OK;
   if (!partials) return arg_fail("mc_partials: null output");
   const unsigned grid = mc_grid((chunk_end - chunk_begin) * kMcThreads, kMcThreads);
-  k_mc_partials<<<grid, kMcThreads, 0, as_stream(stream)>>>(*P, philox(seed), n, chunk_begin, chunk_end, total,
+  k_mc_partials<<<grid, kMcThreads, 0, as_stream(stream)>>>(*P, philox(P, seed), n, chunk_begin, chunk_end, total,
                                                             partials);
   UCP_LAUNCHED("k_mc_partials");
   return UCP_OK;
