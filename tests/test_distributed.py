@@ -193,3 +193,31 @@ def test_sharded_device_solve_bitwise_world2(balanced, monkeypatch):
         np.testing.assert_array_equal(u1.view(np.uint64), np.asarray(ref.controllers.values(1)).view(np.uint64))
         assert np.float64(J).view(np.uint64) == np.float64(ref.final_objective).view(np.uint64)
         assert Js == [rr.objective for rr in ref.rounds]
+
+
+# ------------------------------------ device Monte-Carlo estimate, 2/3 ranks
+def _gpu_mc_worker(rank, world, port, q, n):
+    _init(rank, world, port)
+    import paper_1908_04489_b200 as P
+
+    torch.cuda.set_device(0)
+    prob = P.Inventory(stages=3, grids=[(-3.0, 3.0, 121)] * 3)
+    U = prob.identity_controllers()
+    out = P.device_monte_carlo_objective(prob, U, n, seed=11, sharding=P.from_process_group())
+    dist.destroy_process_group()
+    q.put((rank, out))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_monte_carlo_rank_invariant(world):
+    """Chunks split over ranks, partials all-gathered: every rank gets the
+    single-process bits."""
+    import paper_1908_04489_b200 as P
+
+    n = 5 * 4096 + 123
+    out = _spawn(_gpu_mc_worker, world, n)
+    prob = P.Inventory(stages=3, grids=[(-3.0, 3.0, 121)] * 3)
+    ref = P.device_monte_carlo_objective(prob, prob.identity_controllers(), n, seed=11)
+    for r in range(world):
+        assert np.array(out[r]).view(np.uint64).tolist() == np.array(ref).view(np.uint64).tolist()
