@@ -272,6 +272,50 @@ int ucp_mc_partials(const ucp_mc_problem* P, uint64_t seed, int64_t n, int64_t c
 /* fixed-order sum of n partials into *out (device) */
 int ucp_mc_reduce(const double* partials, int64_t n, double* out, void* stream);
 
+/* ---- batched multi-instance engine (config 4) -----------
+ * B Witsenhausen instances on the SAME grids (k, sigma free) advanced
+ * together: each call runs every kernel once over (instance, point).  Rows:
+ * u0[B][ld0], u1[B][ld1] (updated in place), f0/fw0[B][ld0] (host NumPy
+ * densities, witsenhausen.py:47-53), k[B].  Each instance's results are
+ * bitwise its single-instance solve's.  Replaces one solver.solve() per
+ * instance (solver.py:234-290) for k/sigma sweeps and multi-start. */
+typedef struct ucp_wc_batch_desc {
+  int64_t instances; /* B, 1..1024 */
+  double a0, h0;
+  int64_t d0;
+  double a1, h1;
+  int64_t d1;
+  const double* y0; /* shared grid points */
+  const double* y1;
+  double* u0; /* [B][ld0] */
+  double* u1; /* [B][ld1], 16-byte aligned rows */
+  int64_t ld0, ld1; /* even row strides */
+  const double* f0;  /* [B][ld0] */
+  const double* fw0; /* [B][ld0] */
+  const double* k;   /* [B] */
+  ucp_local_params lp0, lp1; /* per stage (shared) */
+  const int64_t* win_lo0; /* shared exhaustion windows (grids.py:180-195) */
+  const int64_t* win_hi0;
+  const int64_t* win_lo1;
+  const int64_t* win_hi1;
+  int64_t cand_bound0; /* sum of stage-0 window widths */
+} ucp_wc_batch_desc;
+typedef struct ucp_wc_batch ucp_wc_batch;
+int ucp_wc_batch_create(const ucp_wc_batch_desc* desc, ucp_wc_batch** out);
+int ucp_wc_batch_destroy(ucp_wc_batch* b);
+/* `iters` block iterations (kind 0 local update, 1 partial exhaustion; both
+ * stages each, solver.py:226-231) for instances ids[0..nslots) (host array).
+ * lane: scratch set (exhaustion needs lane 1); two lanes may run concurrently
+ * on two streams for disjoint instance sets.  err[b*6 + 3*m + e]: first bad
+ * point (atomicMin; initialise to UCP_NO_ERROR) of stage m, as err6 of
+ * ucp_wc_run_block_graph. */
+int ucp_wc_batch_iterate(ucp_wc_batch* b, int lane, int kind, const int32_t* ids, int32_t nslots, int iters,
+                         int64_t* err, void* stream);
+/* J[b] = objective of each listed instance (problem.py:110-127); err_obj[b]
+ * first non-finite integrand point. */
+int ucp_wc_batch_objective(ucp_wc_batch* b, int lane, const int32_t* ids, int32_t nslots, double* J,
+                           int64_t* err_obj, void* stream);
+
 /* ---- instrumentation ------------------------------------------------------
  * FP64 pipe throughput probe (no FMA: DMUL/DADD only, 8 independent chains
  * per thread).  Performs iters*16 DP ops per thread; sink must hold

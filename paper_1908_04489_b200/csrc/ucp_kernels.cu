@@ -17,7 +17,9 @@
 #include <atomic>
 #include <vector>
 #include <mutex>
+#include <shared_mutex>
 #include <unordered_set>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "../../include/ucp_b200.h"
@@ -84,6 +86,19 @@ struct WalkGrid {
 struct Mom3 {
   double t0, t1, t2;
 };
+
+// Instance dimension of the batched engine (config 4, ucp_wc_batch_*): a
+// launch covers slots blockIdx.y (k_moments: its work items), slot s running
+// instance ids[s].  Stage-0 arrays (u0, f0, fw0) of instance b start at
+// b*su0, u1 at b*su1; per-slot scratch at s*sslot; error slots at b*serr.
+// kNoBatch (ids == nullptr) is the single-instance case: every offset 0.
+struct BatchArgs {
+  const int32_t* ids;
+  int64_t su0, su1, sslot, serr;
+  const double* kvec;  // per-instance k (nullptr: the scalar argument)
+  __device__ __forceinline__ int inst(int slot) const { return ids ? ids[slot] : 0; }
+};
+constexpr BatchArgs kNoBatch = {nullptr, 0, 0, 0, 0, nullptr};
 
 WalkGrid make_walk_grid(double a, double h, int64_t d) {
   WalkGrid g;
@@ -280,11 +295,19 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_st
 // Local update, stage 0, part 1 (problem.py:95-97): the three FD probes
 // u+h, u, u-h of every point.  probe-major layout so a warp walks adjacent
 // centres (coalesced v1 reads).
-template <int kMode>
+template <int kMode, bool kBatch = false>
 __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_lu0_probe(const double* __restrict__ y0, const double* __restrict__ f0,
                             const double* __restrict__ u0, double k, const double* __restrict__ v1,
-                            WalkGrid g, double fd_step, int64_t begin, int64_t n, double* cost3) {
+                            WalkGrid g, double fd_step, int64_t begin, int64_t n, double* cost3, const BatchArgs B) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (kBatch) {
+    const int b = B.inst(blockIdx.y);
+    f0 += b * B.su0;
+    u0 += b * B.su0;
+    v1 += b * B.su1;
+    k = B.kvec[b];
+    cost3 += blockIdx.y * B.sslot;
+  }
   UCP_WALK_STAGE(v1, g.d);
   if (t >= 3 * n) return;
   int p = (int)(t / n);
@@ -310,12 +333,22 @@ __device__ __forceinline__ double newton_step(double u, double c1, double c2,
 // Local update, stage 0, part 2: derivatives (problem.py:99-101), step,
 // cost_new and the monotone guard (solver.py:193-203).  cost_old is the
 // bitwise-identical `mid` probe.
-template <int kMode>
+template <int kMode, bool kBatch = false>
 __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_lu0_finish(const double* __restrict__ y0, const double* __restrict__ f0,
                              const double* __restrict__ u0, double k, const double* __restrict__ v1,
                              WalkGrid g, ucp_local_params lp, int64_t begin, int64_t n,
-                             const double* __restrict__ cost3, double* out, int64_t* err) {
+                             const double* __restrict__ cost3, double* out, int64_t* err, const BatchArgs B) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (kBatch) {
+    const int b = B.inst(blockIdx.y);
+    f0 += b * B.su0;
+    u0 += b * B.su0;
+    v1 += b * B.su1;
+    k = B.kvec[b];
+    cost3 += blockIdx.y * B.sslot;
+    out += blockIdx.y * n;
+    err += b * B.serr;
+  }
   UCP_WALK_STAGE(v1, g.d);
   if (t >= n) return;
   int64_t i = begin + t;
@@ -338,11 +371,21 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_lu
 }
 
 // Objective integrand (problem.py:116-127): c_i = C0(u0_i, y0_i).
-template <int kMode>
+template <int kMode, bool kBatch = false>
 __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_obj_terms(const double* __restrict__ y0, const double* __restrict__ f0,
                             const double* __restrict__ u0, double k, const double* __restrict__ v1,
-                            WalkGrid g, int64_t begin, int64_t end, double* terms, int64_t* err) {
+                            WalkGrid g, int64_t begin, int64_t end, double* terms, int64_t* err,
+                            const BatchArgs B) {
   int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (kBatch) {
+    const int b = B.inst(blockIdx.y);
+    f0 += b * B.su0;
+    u0 += b * B.su0;
+    v1 += b * B.su1;
+    k = B.kvec[b];
+    terms += blockIdx.y * B.sslot;
+    err += b * B.serr;
+  }
   UCP_WALK_STAGE(v1, g.d);
   if (i >= end) return;
   double c = stage0_cost<kMode>(u0[i], y0[i], f0[i], k, v1, g);
@@ -355,8 +398,14 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ob
 // (interior chunk body unrolled so the shared loads run ahead of the
 // dependent adds).
 __global__ void k_trapezoid(const double* __restrict__ x, int64_t n, double spacing, double* out,
-                            int64_t* err) {
+                            int64_t* err, const BatchArgs B) {
   constexpr int kChunk = 2048;
+  if (B.ids) {  // one warp (CTA) per slot; J and the error slot per instance
+    const int b = B.inst(blockIdx.x);
+    x += blockIdx.x * B.sslot;
+    out += b;
+    if (err) err += b * B.serr;
+  }
   __shared__ double buf[kChunk];
   const int lane = threadIdx.x;
   double acc = 0.0;
@@ -457,13 +506,25 @@ __global__ void k_ex_fill(const double* __restrict__ u, const int64_t* __restric
   }
 }
 
-template <int kMode>
+template <int kMode, bool kBatch = false>
 __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ex0_eval(const double* __restrict__ y0, const double* __restrict__ f0,
                            const double* __restrict__ u0, double k, const double* __restrict__ v1,
                            WalkGrid g, const int64_t* __restrict__ total,
                            const int32_t* __restrict__ cand_pt, const int32_t* __restrict__ cand_j,
-                           double* costs) {
+                           double* costs, const BatchArgs B) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (kBatch) {  // per-slot candidate lists of capacity sslot; totals[slot]
+    const int b = B.inst(blockIdx.y);
+    total += blockIdx.y;
+    if ((int64_t)blockIdx.x * blockDim.x >= *total) return;  // whole CTA idle: skip the staging
+    f0 += b * B.su0;
+    u0 += b * B.su0;
+    v1 += b * B.su1;
+    k = B.kvec[b];
+    cand_pt += blockIdx.y * B.sslot;
+    cand_j += blockIdx.y * B.sslot;
+    costs += blockIdx.y * B.sslot;
+  }
   UCP_WALK_STAGE(v1, g.d);
   if (c >= *total) return;
   int32_t i = cand_pt[c];
@@ -474,9 +535,19 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ex
 // any non-finite candidate cost flags the point (solver.py:216-221).
 __global__ void k_ex_argmin(const double* __restrict__ u, const double* __restrict__ costs,
                             const int64_t* __restrict__ offs, const int32_t* __restrict__ cand_j,
-                            int64_t begin, int64_t n, double* out, int64_t* err) {
+                            int64_t begin, int64_t n, double* out, int64_t* err, const BatchArgs B,
+                            int64_t soffs) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
+  if (B.ids) {
+    const int b = B.inst(blockIdx.y);
+    u += b * B.su0;
+    costs += blockIdx.y * B.sslot;
+    cand_j += blockIdx.y * B.sslot;
+    offs += blockIdx.y * soffs;
+    out += blockIdx.y * n;
+    err += b * B.serr;
+  }
   int64_t lo = offs[t], hi = offs[t + 1];
   int64_t best = lo;
   double bv = costs[lo];
@@ -503,8 +574,18 @@ constexpr int kTile = 256;  // support points per shared-memory tile
 // the tail-weighted edge queries).
 __global__ void k_x1_prepare(const double* __restrict__ y0, const double* __restrict__ u0,
                              const double* __restrict__ w, int64_t d0, double a, double h, double b, double* x1,
-                             double2* xw, double2* tails, double2* tile_mm) {
+                             double2* xw, double2* tails, double2* tile_mm, const BatchArgs B) {
   __shared__ double smin[kTile], smax[kTile];
+  if (B.ids) {
+    const int inst = B.inst(blockIdx.y);
+    const int64_t ntiles = (d0 + kTile - 1) / kTile;
+    u0 += inst * B.su0;
+    w += inst * B.su0;
+    x1 += blockIdx.y * d0;
+    tails += blockIdx.y * d0;
+    xw += blockIdx.y * ntiles * kTile;
+    tile_mm += blockIdx.y * ntiles;
+  }
   __shared__ int snan;
   if (threadIdx.x == 0) snan = 0;
   __syncthreads();
@@ -591,7 +672,7 @@ constexpr int kMomUnroll = 4;
 __global__ void __launch_bounds__(kMomThreads, 6)
 k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ xw,
           const double2* __restrict__ tails, int64_t m, const double2* __restrict__ tile_mm, double a, double h,
-          int64_t d, double* o0, double* o1, double* o2, int* work_counter) {
+          int64_t d, double* o0, double* o1, double* o2, int* work_counter, int64_t nslots, int64_t sout) {
   // interior CTAs: (x, w) tiles arrive by bulk async copy (TMA engine) into a
   // double buffer, the next non-skipped tile in flight while this one is used
   __shared__ __align__(128) double2 sbuf[2][kTile];
@@ -604,6 +685,10 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
   for (int r = threadIdx.x; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
   const ucp_exp_entry* stab2 = reinterpret_cast<const ucp_exp_entry*>(stab);
   const int64_t nqb = (n + kMomThreads - 1) / kMomThreads;
+  // work items: the edge query blocks of every slot first (they visit the most
+  // tiles), then the interior blocks; one slot == the single-instance order
+  const int64_t nedge = nqb == 1 ? 1 : 2;
+  const int64_t nitems = nslots * nqb;
   const double b = a + h * (double)(d - 1);
   const double INV = inv_sqrt_2pi();
   const int64_t ntiles = (m + kTile - 1) / kTile;
@@ -615,10 +700,28 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
   }
   __syncthreads();
   uint32_t phase0 = 0, phase1 = 0;  // completions seen per barrier (parity), CTA-uniform
+  const double2* xw0 = xw;
+  const double2* tails0 = tails;
+  const double2* tile_mm0 = tile_mm;
+  double *o00 = o0, *o10 = o1, *o20 = o2;
   for (;;) {
     const int64_t k = s_work;
-    if (k >= nqb) break;
-    const int64_t qb = k == 0 ? 0 : (k == 1 ? nqb - 1 : k - 1);  // edge blocks first
+    if (k >= nitems) break;
+    int64_t slot, qb;
+    if (k < nslots * nedge) {
+      slot = k / nedge;
+      qb = (k % nedge) ? nqb - 1 : 0;
+    } else {
+      const int64_t r = k - nslots * nedge, per = nqb - nedge;
+      slot = r / per;
+      qb = 1 + r % per;
+    }
+    xw = xw0 + slot * ntiles * kTile;
+    tails = tails0 + slot * m;
+    tile_mm = tile_mm0 + slot * ntiles;
+    o0 = o00 + slot * sout;
+    o1 = o10 + slot * sout;
+    o2 = o20 + slot * sout;
     if (threadIdx.x == 0) s_left = s_right = 0;
     const int64_t t = qb * kMomThreads + threadIdx.x;
     const bool active = t < n;
@@ -856,9 +959,18 @@ __global__ void k_stage1_segmented(const double* __restrict__ u_flat, const int6
 
 __global__ void k_lu1(const double* __restrict__ u1, const double* __restrict__ m0,
                       const double* __restrict__ m1, const double* __restrict__ m2,
-                      ucp_local_params lp, int64_t begin, int64_t n, double* out, int64_t* err) {
+                      ucp_local_params lp, int64_t begin, int64_t n, double* out, int64_t* err, const BatchArgs BA) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
+  if (BA.ids) {  // moments per slot (stride sslot), output per slot (stride n)
+    const int b = BA.inst(blockIdx.y);
+    u1 += b * BA.su1;
+    m0 += blockIdx.y * BA.sslot;
+    m1 += blockIdx.y * BA.sslot;
+    m2 += blockIdx.y * BA.sslot;
+    out += blockIdx.y * n;
+    err += b * BA.serr;
+  }
   int64_t i = begin + t;
   const double A = m0[t], B = m1[t], C = m2[t];
   double u = u1[i];
@@ -884,9 +996,18 @@ __global__ void k_lu1(const double* __restrict__ u1, const double* __restrict__ 
 __global__ void k_ex1(const double* __restrict__ u1, const double* __restrict__ m0,
                       const double* __restrict__ m1, const double* __restrict__ m2,
                       const int64_t* __restrict__ lo, const int64_t* __restrict__ hi, int64_t begin,
-                      int64_t n, double* out, int64_t* err) {
+                      int64_t n, double* out, int64_t* err, const BatchArgs BA) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
+  if (BA.ids) {
+    const int b = BA.inst(blockIdx.y);
+    u1 += b * BA.su1;
+    m0 += blockIdx.y * BA.sslot;
+    m1 += blockIdx.y * BA.sslot;
+    m2 += blockIdx.y * BA.sslot;
+    out += blockIdx.y * n;
+    err += b * BA.serr;
+  }
   int64_t i = begin + t;
   const double A = m0[t], B = m1[t], C = m2[t];
   int64_t j0 = lo[i], j1 = hi[i];
@@ -934,6 +1055,13 @@ struct ucp_graph_entry {
   cudaGraphExec_t exec;
 };
 
+// CUDA-graph captures (ThreadLocal mode) run concurrently in the host threads
+// of solve_many; a device-synchronising call from ANY thread (cudaFree,
+// cudaFreeHost, cudaDeviceSynchronize) while a capture is open would
+// invalidate it.  Captures hold this lock shared; the library's
+// synchronising calls (workspace growth / destruction) hold it exclusively.
+std::shared_mutex g_capture_mu;
+
 struct ucp_workspace {
   void* buf[16] = {nullptr};
   size_t cap[16] = {0};
@@ -962,6 +1090,7 @@ int ws_get(ucp_workspace* ws, int slot, size_t bytes, void** out) {
     if (ws->cap_stream && cudaStreamIsCapturing(ws->cap_stream, &cs) == cudaSuccess &&
         cs != cudaStreamCaptureStatusNone)
       return arg_fail("workspace growth during graph capture");
+    std::unique_lock<std::shared_mutex> lk(g_capture_mu);
     // captured graphs hold workspace addresses: growing a buffer retires them
     // (an in-flight graph exec is freed asynchronously on completion)
     for (auto& g : ws->graphs) cudaGraphExecDestroy(g.exec);
@@ -993,7 +1122,7 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   if ((rc = ws_get(ws, WS_TOTAL, sizeof(int64_t) * 2, &pctr))) return rc;
   const double b = a + h * (double)(d - 1);
   k_x1_prepare<<<(unsigned)ntiles, kTile, 0, st>>>(y0, u0, w, m, a, h, b, (double*)px1, (double2*)pxw,
-                                                   (double2*)ptails, (double2*)ptile);
+                                                   (double2*)ptails, (double2*)ptile, kNoBatch);
   UCP_LAUNCHED("k_x1_prepare");
   if (nq <= kTwoPhaseMaxQueries && nq * m <= kTwoPhaseMaxPairs) {
     void* ppre;
@@ -1016,7 +1145,7 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > nqb) grid = nqb;
   k_moments<<<(unsigned)grid, kMomThreads, 0, st>>>(yq, nq, (const double2*)pxw, (const double2*)ptails, m,
-                                                      (const double2*)ptile, a, h, d, o0, o1, o2, counter);
+                                                      (const double2*)ptile, a, h, d, o0, o1, o2, counter, 1, 0);
   UCP_LAUNCHED("k_moments");
   return UCP_OK;
 }
@@ -1097,6 +1226,8 @@ int ucp_workspace_create(ucp_workspace** ws) {
 
 int ucp_workspace_destroy(ucp_workspace* ws) {
   if (!ws) return UCP_OK;
+  std::unique_lock<std::shared_mutex> lk(g_capture_mu);
+  cudaDeviceSynchronize();  // in-flight work may still read the buffers
   for (int i = 0; i < 16; ++i)
     if (ws->buf[i]) cudaFree(ws->buf[i]);
   if (ws->scan_tmp) cudaFree(ws->scan_tmp);
@@ -1152,7 +1283,7 @@ int ucp_gauss_moments_points(const double* y, int64_t n, const double* x, const 
 int ucp_trapezoid_sum(const double* samples, int64_t n, double spacing, double* out, int64_t* err,
                       void* stream) {
   if (n < 1) return arg_fail("trapezoid needs at least one sample");
-  k_trapezoid<<<1, 32, 0, as_stream(stream)>>>(samples, n, spacing, out, err);
+  k_trapezoid<<<1, 32, 0, as_stream(stream)>>>(samples, n, spacing, out, err, kNoBatch);
   UCP_LAUNCHED("k_trapezoid");
   return UCP_OK;
 }
@@ -1229,10 +1360,10 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
     if (int rc_ = check_aligned(u1)) return rc_;
     WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
     UCP_WALK_LAUNCH(k_lu0_probe, 3 * n, nblocks(3 * n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
-                                                     (double*)pc);
+                                                     (double*)pc, kNoBatch);
     UCP_LAUNCHED("k_lu0_probe");
     UCP_WALK_LAUNCH(k_lu0_finish, n, nblocks(n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, *lp, begin, n,
-                                                  (const double*)pc, out, err);
+                                                  (const double*)pc, out, err, kNoBatch);
     UCP_LAUNCHED("k_lu0_finish");
     return UCP_OK;
   }
@@ -1242,7 +1373,7 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
   if ((rc = run_moments(P->y1 + begin, n, P->y0, u0, P->fw0, P->d0, P->a1, P->h1, P->d1, m0, m0 + n,
                         m0 + 2 * n, ws, st)))
     return rc;
-  k_lu1<<<nblocks(n, 256), 256, 0, st>>>(u1, m0, m0 + n, m0 + 2 * n, *lp, begin, n, out, err);
+  k_lu1<<<nblocks(n, 256), 256, 0, st>>>(u1, m0, m0 + n, m0 + 2 * n, *lp, begin, n, out, err, kNoBatch);
   UCP_LAUNCHED("k_lu1");
   return UCP_OK;
 }
@@ -1266,7 +1397,8 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
     if ((rc = run_moments(P->y1 + begin, n, P->y0, u0, P->fw0, P->d0, P->a1, P->h1, P->d1, m0, m0 + n,
                           m0 + 2 * n, ws, st)))
       return rc;
-    k_ex1<<<nblocks(n, 256), 256, 0, st>>>(u1, m0, m0 + n, m0 + 2 * n, win_lo, win_hi, begin, n, out, err);
+    k_ex1<<<nblocks(n, 256), 256, 0, st>>>(u1, m0, m0 + n, m0 + 2 * n, win_lo, win_hi, begin, n, out, err,
+                                           kNoBatch);
     UCP_LAUNCHED("k_ex1");
     return UCP_OK;
   }
@@ -1279,6 +1411,7 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, counts, n + 1, st);
   if (ws->scan_cap < tmp_bytes) {
+    std::unique_lock<std::shared_mutex> lk(g_capture_mu);
     if (ws->scan_tmp) UCP_CHECK(cudaFree(ws->scan_tmp));
     UCP_CHECK(cudaMalloc(&ws->scan_tmp, tmp_bytes));
     ws->scan_cap = tmp_bytes;
@@ -1310,10 +1443,10 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
   if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
   UCP_WALK_LAUNCH(k_ex0_eval, total, nblocks(total, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, counts + n,
-                                                  (const int32_t*)ppt, (const int32_t*)pj, (double*)pc);
+                                                  (const int32_t*)ppt, (const int32_t*)pj, (double*)pc, kNoBatch);
   UCP_LAUNCHED("k_ex0_eval");
   k_ex_argmin<<<nblocks(n, 256), 256, 0, st>>>(u0, (const double*)pc, counts, (const int32_t*)pj, begin, n,
-                                               out, err);
+                                               out, err, kNoBatch, 0);
   UCP_LAUNCHED("k_ex_argmin");
   return UCP_OK;
 }
@@ -1419,6 +1552,7 @@ int ucp_wc_run_block_graph(const ucp_wc_problem* P, int kind, int iters, double*
     if (g.key == key) exec = g.exec;
   if (!exec) {
     if (!ws->cap_stream) UCP_CHECK(cudaStreamCreateWithFlags(&ws->cap_stream, cudaStreamNonBlocking));
+    std::shared_lock<std::shared_mutex> lk(g_capture_mu);
     UCP_CHECK(cudaStreamBeginCapture(ws->cap_stream, cudaStreamCaptureModeThreadLocal));
     rc = block_iteration(P, kind, u0, u1, lp, lo, hi, cand_bound0, scratch, err6, ws, ws->cap_stream);
     cudaGraph_t graph = nullptr;
@@ -1450,7 +1584,7 @@ int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const doub
   if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
   UCP_WALK_LAUNCH(k_obj_terms, end - begin, nblocks(end - begin, kWalkThreads), as_stream(stream), P->d1, P->y0, P->f0, u0, P->k, u1, g,
-                                                                          begin, end, terms, err);
+                                                                          begin, end, terms, err, kNoBatch);
   UCP_LAUNCHED("k_obj_terms");
   return UCP_OK;
 }
@@ -1466,3 +1600,4 @@ int ucp_fp64_probe(int blocks, int threads, int iters, double* sink, void* strea
 
 #include "ucp_config5.cuh"
 #include "ucp_mc.cuh"
+#include "ucp_batch.cuh"

@@ -108,7 +108,9 @@ class DeviceContext:
     def __del__(self):
         try:
             if self.ws:
-                torch.cuda.synchronize(self.device)
+                # synchronises the device itself, under the library's capture
+                # lock (a bare device sync here -- the GC may run this in any
+                # thread -- would invalidate another thread's graph capture)
                 self.lib.ucp_workspace_destroy(self.ws)
         except Exception:  # interpreter shutdown
             pass

@@ -311,3 +311,25 @@ def test_graph_replayed_blocks_bitwise_and_errors(P, golden, kind):
             prob.flush_errors()
         msgs.append(str(e.value))
     assert msgs[0] == msgs[1]
+
+
+@pytest.mark.gpu
+def test_concurrent_graph_capture_with_workspace_churn():
+    """solve_many: graph captures in some host threads while others grow or
+    destroy workspaces (device-synchronising calls) -- results stay bitwise
+    the sequential solves'."""
+    import gc
+
+    import paper_1908_04489_b200 as P
+
+    cfg = P.SolverConfig(max_rounds=4)
+    specs = [(0.05 + 0.1 * i, (3.0, 5.0, 7.0)[i % 3], 301 + 97 * (i % 5)) for i in range(24)]
+    probs = [P.Witsenhausen(k=k, sigma=s, grids=[(-25.0, 25.0, d)] * 2) for k, s, d in specs]
+    got = P.solve_many(probs, cfg, concurrency=12)
+    del probs
+    gc.collect()
+    for (k, s, d), r in zip(specs, got):
+        ref = P.solve(P.Witsenhausen(k=k, sigma=s, grids=[(-25.0, 25.0, d)] * 2), cfg)
+        assert r.final_objective == ref.final_objective
+        for m in range(2):
+            assert np.array_equal(np.asarray(r.controllers.values(m)), np.asarray(ref.controllers.values(m)))
