@@ -20,7 +20,7 @@ struct ucp_wc_batch {
     double *scratch0 = nullptr, *scratch1 = nullptr, *cost3 = nullptr, *mom = nullptr, *terms = nullptr;
     double *x1 = nullptr, *costs = nullptr;
     double2 *tails = nullptr, *xw = nullptr, *tile_mm = nullptr;
-    int64_t *offs = nullptr, *totals = nullptr;
+    int64_t *offs = nullptr, *totals = nullptr, *counts = nullptr, *chunk_tot = nullptr;
     int32_t *cand_pt = nullptr, *cand_j = nullptr;
     int* counter = nullptr;
   } lane[2];
@@ -46,63 +46,80 @@ __global__ void k_bcopy(const double* __restrict__ src, int64_t n, double* __res
   dst[(int64_t)ids[blockIdx.y] * ld + i] = src[(int64_t)blockIdx.y * n + i];
 }
 
-// Exhaustion candidates of one slot per CTA: count (adjacent repeats
-// collapsed, as k_ex_count), block-wide exclusive scan, fill (as k_ex_fill).
-constexpr int kCandThreads = 512;
-__global__ void __launch_bounds__(kCandThreads) k_bex_cands(const double* __restrict__ u0, const int64_t* __restrict__ lo,
-                                                            const int64_t* __restrict__ hi, int64_t d0, const BatchArgs B,
-                                                            int64_t* offs, int64_t* totals, int32_t* cand_pt,
-                                                            int32_t* cand_j) {
+// Exhaustion candidates, (chunk of kCandThreads points, slot) per CTA:
+// k_bex_count counts each point's candidates (adjacent repeats collapsed, as
+// k_ex_count) and the chunk total; k_bex_fill takes its chunk's base from
+// the preceding chunk totals, block-scans the counts and fills (as k_ex_fill).
+constexpr int kCandThreads = 256;
+__device__ __forceinline__ int64_t window_count(const double* __restrict__ u, int64_t j0, int64_t j1) {
+  int64_t c = 1;
+  double prev = u[j0];
+  for (int64_t j = j0 + 1; j <= j1; ++j) {
+    const double x = u[j];
+    c += (x != prev);
+    prev = x;
+  }
+  return c;
+}
+
+__global__ void __launch_bounds__(kCandThreads) k_bex_count(const double* __restrict__ u0, const int64_t* __restrict__ lo,
+                                                            const int64_t* __restrict__ hi, int64_t d0,
+                                                            const BatchArgs B, int64_t* counts, int64_t* chunk_tot) {
+  using Reduce = cub::BlockReduce<int64_t, kCandThreads>;
+  __shared__ typename Reduce::TempStorage tmp;
+  const int slot = blockIdx.y;
+  const double* u = u0 + (int64_t)B.inst(slot) * B.su0;
+  const int64_t i = (int64_t)blockIdx.x * kCandThreads + threadIdx.x;
+  const int64_t c = i < d0 ? window_count(u, lo[i], hi[i]) : 0;
+  if (i < d0) counts[(int64_t)slot * d0 + i] = c;
+  const int64_t tot = Reduce(tmp).Sum(c);
+  if (threadIdx.x == 0) chunk_tot[(int64_t)slot * gridDim.x + blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kCandThreads) k_bex_fill(const double* __restrict__ u0, const int64_t* __restrict__ lo,
+                                                           const int64_t* __restrict__ hi, int64_t d0,
+                                                           const BatchArgs B, const int64_t* __restrict__ counts,
+                                                           const int64_t* __restrict__ chunk_tot, int64_t* offs,
+                                                           int64_t* totals, int32_t* cand_pt, int32_t* cand_j) {
   using Scan = cub::BlockScan<int64_t, kCandThreads>;
   __shared__ typename Scan::TempStorage tmp;
-  __shared__ int64_t s_run;
-  const int slot = blockIdx.x;
+  __shared__ int64_t s_base;
+  const int slot = blockIdx.y;
   const double* u = u0 + (int64_t)B.inst(slot) * B.su0;
   offs += (int64_t)slot * (d0 + 1);
   cand_pt += (int64_t)slot * B.sslot;
   cand_j += (int64_t)slot * B.sslot;
-  if (threadIdx.x == 0) s_run = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < d0; base += kCandThreads) {
-    const int64_t i = base + threadIdx.x;
-    int64_t c = 0;
-    if (i < d0) {
-      c = 1;
-      double prev = u[lo[i]];
-      for (int64_t j = lo[i] + 1; j <= hi[i]; ++j) {
-        const double x = u[j];
-        c += (x != prev);
-        prev = x;
-      }
-    }
-    int64_t pos, agg;
-    Scan(tmp).ExclusiveSum(c, pos, agg);
-    const int64_t run = s_run;
-    pos += run;
-    if (i < d0) {
-      offs[i] = pos;
-      const int64_t j0 = lo[i];
-      double prev = u[j0];
-      cand_pt[pos] = (int32_t)i;
-      cand_j[pos] = (int32_t)j0;
-      ++pos;
-      for (int64_t j = j0 + 1; j <= hi[i]; ++j) {
-        const double x = u[j];
-        if (x != prev) {
-          cand_pt[pos] = (int32_t)i;
-          cand_j[pos] = (int32_t)j;
-          ++pos;
-        }
-        prev = x;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_run = run + agg;
-    __syncthreads();
-  }
   if (threadIdx.x == 0) {
-    offs[d0] = s_run;
-    totals[slot] = s_run;
+    int64_t base = 0;
+    for (unsigned c = 0; c < blockIdx.x; ++c) base += chunk_tot[(int64_t)slot * gridDim.x + c];
+    s_base = base;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kCandThreads + threadIdx.x;
+  const int64_t c = i < d0 ? counts[(int64_t)slot * d0 + i] : 0;
+  int64_t pos, agg;
+  Scan(tmp).ExclusiveSum(c, pos, agg);
+  pos += s_base;
+  if (i < d0) {
+    offs[i] = pos;
+    const int64_t j0 = lo[i];
+    double prev = u[j0];
+    cand_pt[pos] = (int32_t)i;
+    cand_j[pos] = (int32_t)j0;
+    ++pos;
+    for (int64_t j = j0 + 1; j <= hi[i]; ++j) {
+      const double x = u[j];
+      if (x != prev) {
+        cand_pt[pos] = (int32_t)i;
+        cand_j[pos] = (int32_t)j;
+        ++pos;
+      }
+      prev = x;
+    }
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    offs[d0] = s_base + agg;
+    totals[slot] = s_base + agg;
   }
 }
 
@@ -170,9 +187,12 @@ int batch_iteration(ucp_wc_batch* b, ucp_wc_batch::Lane& L, int kind, int S, int
     UCP_LAUNCHED("k_lu0_finish");
   } else {
     const BatchArgs B = batch_args(b, L.ids, b->cbpad);
-    k_bex_cands<<<S, kCandThreads, 0, st>>>(D.u0, D.win_lo0, D.win_hi0, d0, B, L.offs, L.totals, L.cand_pt,
-                                            L.cand_j);
-    UCP_LAUNCHED("k_bex_cands");
+    const dim3 cgrid(nblocks(d0, kCandThreads), S);
+    k_bex_count<<<cgrid, kCandThreads, 0, st>>>(D.u0, D.win_lo0, D.win_hi0, d0, B, L.counts, L.chunk_tot);
+    UCP_LAUNCHED("k_bex_count");
+    k_bex_fill<<<cgrid, kCandThreads, 0, st>>>(D.u0, D.win_lo0, D.win_hi0, d0, B, L.counts, L.chunk_tot, L.offs,
+                                               L.totals, L.cand_pt, L.cand_j);
+    UCP_LAUNCHED("k_bex_fill");
     UCP_WALK_LAUNCH_B(k_ex0_eval, S * b->cbpad, dim3(nblocks(b->cbpad, kWalkThreads), S), st, d1, D.y0, D.f0, D.u0,
                       0.0, D.u1, g, L.totals, L.cand_pt, L.cand_j, L.costs, B);
     UCP_LAUNCHED("k_ex0_eval");
@@ -238,7 +258,8 @@ int ucp_wc_batch_create(const ucp_wc_batch_desc* desc, ucp_wc_batch** out) {
         (rc = balloc(b, &L.counter, 1)))
       break;
     if (l == 1 && ((rc = balloc(b, &L.costs, B * b->cbpad)) || (rc = balloc(b, &L.offs, B * (d0 + 1))) ||
-                   (rc = balloc(b, &L.totals, B)) || (rc = balloc(b, &L.cand_pt, B * b->cbpad)) ||
+                   (rc = balloc(b, &L.totals, B)) || (rc = balloc(b, &L.counts, B * d0)) ||
+                   (rc = balloc(b, &L.chunk_tot, B * ((d0 + kCandThreads - 1) / kCandThreads))) || (rc = balloc(b, &L.cand_pt, B * b->cbpad)) ||
                    (rc = balloc(b, &L.cand_j, B * b->cbpad))))
       break;
   }

@@ -19,6 +19,7 @@
 #include <mutex>
 #include <shared_mutex>
 #include <unordered_set>
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
 
