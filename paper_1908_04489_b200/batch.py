@@ -23,6 +23,7 @@ through ``solve``.
 from __future__ import annotations
 
 import ctypes
+import threading
 import time
 
 import numpy as np
@@ -37,6 +38,7 @@ from .solver import RoundReport, SolveResult, SolverConfig, adaptive_allocation,
 __all__ = ["solve_batch", "MAX_BATCH"]
 
 MAX_BATCH = 1024
+LAST_STATS: dict = {}  # host-side timing of the last solve_batch (diagnostics)
 c_i64, c_dbl, c_vp, c_int, c_i32 = ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int, ctypes.c_int32
 
 
@@ -83,8 +85,74 @@ def batchable(problems) -> bool:
     return all(p.grids == g for p in problems[1:])
 
 
+class _Engine:
+    """A created ucp_wc_batch plus the HBM rows it points at, reused by every
+    solve_batch call of the same shape (no allocation or device sync per call)."""
+
+    def __init__(self, dev, B, g0, g1, cfg, lib):
+        from ._device import to_device_i64
+        from .grids import node_window_bounds
+
+        self.lib = lib
+        d0, d1 = g0.d, g1.d
+        ld0, ld1 = d0 + (d0 & 1), d1 + (d1 & 1)
+        self.y0, self.y1 = to_device_f64(g0.points, dev), to_device_f64(g1.points, dev)
+        self.U0 = torch.zeros((B, ld0), dtype=F64, device=dev)
+        self.U1 = torch.zeros((B, ld1), dtype=F64, device=dev)
+        self.F0 = torch.zeros((B, ld0), dtype=F64, device=dev)
+        self.FW0 = torch.zeros((B, ld0), dtype=F64, device=dev)
+        self.K = torch.zeros(B, dtype=F64, device=dev)
+        lo0, hi0 = node_window_bounds(g0, cfg.radius_for(g0))
+        lo1, hi1 = node_window_bounds(g1, cfg.radius_for(g1))
+        self.win = [to_device_i64(x, dev) for x in (lo0, hi0, lo1, hi1)]
+        bound0 = int((hi0 - lo0 + 1).sum())
+        self.desc = WcBatchDesc(B, g0.a, g0.spacing, d0, g1.a, g1.spacing, d1, ptr(self.y0), ptr(self.y1),
+                                ptr(self.U0), ptr(self.U1), ld0, ld1, ptr(self.F0), ptr(self.FW0), ptr(self.K),
+                                _lib.LocalParams(cfg.fd_step, cfg.curvature_min, cfg.grad_step, cfg.cap_for(g0)),
+                                _lib.LocalParams(cfg.fd_step, cfg.curvature_min, cfg.grad_step, cfg.cap_for(g1)),
+                                *(ptr(w) for w in self.win), bound0)
+        self.handle = c_vp()
+        _lib.check(lib.ucp_wc_batch_create(ctypes.byref(self.desc), ctypes.byref(self.handle)), "ucp_wc_batch_create")
+        self.err = torch.empty((B, 6), dtype=I64, device=dev)
+        self.err_obj = torch.empty(B, dtype=I64, device=dev)
+        self.J = torch.zeros((3, B), dtype=F64, device=dev)
+        self.lanes = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.lib.ucp_wc_batch_destroy(self.handle)  # synchronises under the capture lock
+        except Exception:  # interpreter shutdown
+            pass
+
+
+_ENGINES: dict = {}
+
+
+def _engine(dev, B, g0, g1, cfg, lib) -> _Engine:
+    key = (dev.index, B, g0, g1, cfg.radius_for(g0), cfg.radius_for(g1), cfg.fd_step, cfg.curvature_min,
+           cfg.grad_step, cfg.cap_for(g0), cfg.cap_for(g1))
+    eng = _ENGINES.get(key)
+    if eng is None:
+        while len(_ENGINES) >= 2:  # keep the two most recent shapes
+            _ENGINES.pop(next(iter(_ENGINES)))
+        eng = _ENGINES[key] = _Engine(dev, B, g0, g1, cfg, lib)
+    return eng
+
+
+_LOCK = threading.Lock()  # engines are shared: one solve_batch at a time
+
+
 def solve_batch(problems, cfg: SolverConfig | None = None, initials=None) -> list:
     """Solve Witsenhausen instances sharing their grids as one batch (see module doc)."""
+    with _LOCK:
+        return _solve_batch(problems, cfg, initials)
+
+
+def _solve_batch(problems, cfg, initials) -> list:
+    from ._device import require_cuda
+
+    t_start = time.perf_counter()
     problems = list(problems)
     if not batchable(problems) and not (len(problems) == 1 and batchable(problems * 2)):
         raise ValueError("solve_batch needs 1..1024 Witsenhausen instances on identical grids")
@@ -92,41 +160,42 @@ def solve_batch(problems, cfg: SolverConfig | None = None, initials=None) -> lis
     B = len(problems)
     initials = list(initials) if initials is not None else [None] * B
     lib = _bind()
-    p0 = problems[0]
-    D = p0.device_context()
-    dev = D.device
-    g0, g1 = p0.grids
+    dev = require_cuda(problems[0]._device_arg)
+    g0, g1 = problems[0].grids
     d0, d1 = g0.d, g1.d
-    ld0, ld1 = d0 + (d0 & 1), d1 + (d1 & 1)
-
-    U0 = torch.zeros((B, ld0), dtype=F64, device=dev)
-    U1 = torch.zeros((B, ld1), dtype=F64, device=dev)
-    F0 = torch.zeros((B, ld0), dtype=F64, device=dev)
-    FW0 = torch.zeros((B, ld0), dtype=F64, device=dev)
-    for i, p in enumerate(problems):
-        U = p.identity_controllers() if initials[i] is None else initials[i]
-        p.check_controllers(U)
-        U0[i, :d0] = U.device_values(0, dev)
-        U1[i, :d1] = U.device_values(1, dev)
-        F0[i, :d0] = to_device_f64(p._f0, dev)
-        FW0[i, :d0] = to_device_f64(p._fw0, dev)
-    K = torch.tensor([p.k for p in problems], dtype=F64, device=dev)
-    lo0, hi0 = D.window(p0, 0, cfg.radius_for(g0))
-    lo1, hi1 = D.window(p0, 1, cfg.radius_for(g1))
-    bound0 = D.candidate_bound(p0, 0, cfg.radius_for(g0), 0, d0)
-    desc = WcBatchDesc(B, g0.a, g0.spacing, d0, g1.a, g1.spacing, d1, ptr(D.y0), ptr(D.y1), ptr(U0), ptr(U1), ld0,
-                       ld1, ptr(F0), ptr(FW0), ptr(K),
-                       _lib.LocalParams(cfg.fd_step, cfg.curvature_min, cfg.grad_step, cfg.cap_for(g0)),
-                       _lib.LocalParams(cfg.fd_step, cfg.curvature_min, cfg.grad_step, cfg.cap_for(g1)),
-                       ptr(lo0), ptr(hi0), ptr(lo1), ptr(hi1), bound0)
-    handle = c_vp()
-    _lib.check(lib.ucp_wc_batch_create(ctypes.byref(desc), ctypes.byref(handle)), "ucp_wc_batch_create")
-    err = torch.full((B, 6), NO_ERROR, dtype=I64, device=dev)
-    err_obj = torch.full((B,), NO_ERROR, dtype=I64, device=dev)
-    J = torch.zeros((3, B), dtype=F64, device=dev)  # rows: start / after local / after exhaustion
-    lanes = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-    for s in lanes:
-        s.wait_stream(torch.cuda.current_stream(dev))
+    eng = _engine(dev, B, g0, g1, cfg, lib)
+    U0, U1 = eng.U0, eng.U1
+    # per-call rows, staged on the host and uploaded in one copy each
+    host = np.zeros((3, B, U0.shape[1]))
+    host[0, :, :d0] = np.stack([p._f0 for p in problems])
+    host[1, :, :d0] = np.stack([p._fw0 for p in problems])
+    host[2, :, :d0] = g0.points
+    rows1 = np.zeros((B, U1.shape[1]))
+    rows1[:, :d1] = g1.points
+    on_dev = []
+    for i, U in enumerate(initials):
+        if U is None:
+            continue
+        problems[i].check_controllers(U)
+        if U[0].on_device or U[1].on_device:
+            on_dev.append(i)
+        else:
+            host[2, i, :d0] = U.values(0)
+            rows1[i, :d1] = U.values(1)
+    eng.F0.copy_(torch.from_numpy(host[0]))
+    eng.FW0.copy_(torch.from_numpy(host[1]))
+    U0.copy_(torch.from_numpy(host[2]))
+    U1.copy_(torch.from_numpy(rows1))
+    for i in on_dev:
+        U0[i, :d0] = initials[i].device_values(0, dev)
+        U1[i, :d1] = initials[i].device_values(1, dev)
+    eng.K.copy_(torch.tensor([p.k for p in problems], dtype=F64))
+    handle = eng.handle
+    err, err_obj, J, lanes = eng.err, eng.err_obj, eng.J, eng.lanes
+    err.fill_(NO_ERROR)
+    err_obj.fill_(NO_ERROR)
+    for s_ in lanes:
+        s_.wait_stream(torch.cuda.current_stream(dev))
 
     def call(name, *args):
         _lib.check(getattr(lib, name)(*args), name)
@@ -139,6 +208,7 @@ def solve_batch(problems, cfg: SolverConfig | None = None, initials=None) -> lis
         solve(problems[i], cfg, initials[i])
         raise RuntimeError(f"batch instance {i} flagged a numeric error its single solve did not reproduce")
 
+    stats = {"t_setup": time.perf_counter() - t_start, "events": 0, "decisions": 0, "t_sync": 0.0}
     try:
         n = cfg.iters_per_round
         adaptive = cfg.fixed_local_iters is None
@@ -179,9 +249,13 @@ def solve_batch(problems, cfg: SolverConfig | None = None, initials=None) -> lis
             # instances change lanes at block ends: order the two streams
             lanes[1].wait_stream(lanes[0])
             lanes[0].wait_stream(lanes[1])
+            stats["events"] += 1
             if not ended_e:
                 continue
+            stats["decisions"] += 1
+            ts = time.perf_counter()
             lanes[0].synchronize()
+            stats["t_sync"] += time.perf_counter() - ts
             host_j = J.cpu().numpy()
             e_host = err.cpu().numpy()
             eo_host = err_obj.cpu().numpy()
@@ -208,6 +282,9 @@ def solve_batch(problems, cfg: SolverConfig | None = None, initials=None) -> lis
                 round_index[i] += 1
                 phase[i], rem[i] = 0, n_local[i]
         torch.cuda.current_stream(dev).wait_stream(lanes[0])
+        stats["t_loop_end"] = time.perf_counter() - t_start
+        LAST_STATS.clear()
+        LAST_STATS.update(stats)
         out = []
         for i in everyone:
             U = ControllerSet((SampledController(g0, U0[i, :d0].clone(), _trusted_device=True),
@@ -216,4 +293,5 @@ def solve_batch(problems, cfg: SolverConfig | None = None, initials=None) -> lis
                                    termination=termination[i]))
         return out
     finally:
-        lib.ucp_wc_batch_destroy(handle)  # synchronises the device under the capture lock
+        torch.cuda.current_stream(dev).wait_stream(lanes[0])
+        torch.cuda.current_stream(dev).wait_stream(lanes[1])

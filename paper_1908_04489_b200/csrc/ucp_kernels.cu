@@ -669,8 +669,10 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // Persistent CTAs pull 128-query blocks from an atomic counter, the two edge
 // blocks first (they visit the most tiles).
 constexpr int kMomThreads = 128;
-constexpr int kMomUnroll = 4;
-__global__ void __launch_bounds__(kMomThreads, 6)
+// kUnroll pairs' exp() in flight per thread; the batched engine (few CTAs per
+// SM) instantiates a deeper unroll with a looser register bound.
+template <int kMomUnroll = 4, int kMinBlocks = 6>
+__global__ void __launch_bounds__(kMomThreads, kMinBlocks)
 k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ xw,
           const double2* __restrict__ tails, int64_t m, const double2* __restrict__ tile_mm, double a, double h,
           int64_t d, double* o0, double* o1, double* o2, int* work_counter, int64_t nslots, int64_t sout) {
@@ -828,20 +830,32 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
           slr[r] = r < cnt ? tails[base + r] : make_double2(0.0, 0.0);
         }
         __syncthreads();
-        for (int r = 0; r < cnt; ++r) {
-          const double xi = sxw[r].x;
-          const double diff = yt - xi;
-          double wp = 0.0;
-          if (diff <= kGaussCut && diff >= -kGaussCut)
-            wp = (factor * ucp_exp_core((-0.5 * diff) * diff, stab2)) * INV;
-          if (at_left) wp += slr[r].x;   // phi_cdf(a - xi) / h
-          if (at_right) wp += slr[r].y;  // phi_cdf(xi - b) / h
-          if (wp != 0.0) {
-            wp *= sxw[r].y;
-            acc0 += wp;
-            const double wx = wp * xi;
-            acc1 += wx;
-            acc2 += wx * xi;
+        // kernels.py:466-482 in order; the exp() of kMomUnroll pairs is
+        // evaluated ahead (independent) and used only where the reference
+        // evaluates it.  Padding slots (x = +inf, tails 0) give wp == 0.
+        for (int r0 = 0; r0 < kTile; r0 += kMomUnroll) {
+          double e[kMomUnroll];
+#pragma unroll
+          for (int q = 0; q < kMomUnroll; ++q) {
+            const double diff = yt - sxw[r0 + q].x;
+            e[q] = ucp_exp_core((-0.5 * diff) * diff, stab2);
+          }
+#pragma unroll
+          for (int q = 0; q < kMomUnroll; ++q) {
+            const int r = r0 + q;
+            const double xi = sxw[r].x;
+            const double diff = yt - xi;
+            double wp = 0.0;
+            if (diff <= kGaussCut && diff >= -kGaussCut) wp = (factor * e[q]) * INV;
+            if (at_left) wp += slr[r].x;   // phi_cdf(a - xi) / h
+            if (at_right) wp += slr[r].y;  // phi_cdf(xi - b) / h
+            if (wp != 0.0) {
+              wp *= sxw[r].y;
+              acc0 += wp;
+              const double wx = wp * xi;
+              acc1 += wx;
+              acc2 += wx * xi;
+            }
           }
         }
       }
@@ -1141,11 +1155,11 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   int dev = 0, sms = 0, per_sm = 0;
   UCP_CHECK(cudaGetDevice(&dev));
   UCP_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  UCP_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_moments, kMomThreads, 0));
+  UCP_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_moments<>, kMomThreads, 0));
   int64_t nqb = (nq + kMomThreads - 1) / kMomThreads;
   int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > nqb) grid = nqb;
-  k_moments<<<(unsigned)grid, kMomThreads, 0, st>>>(yq, nq, (const double2*)pxw, (const double2*)ptails, m,
+  k_moments<><<<(unsigned)grid, kMomThreads, 0, st>>>(yq, nq, (const double2*)pxw, (const double2*)ptails, m,
                                                       (const double2*)ptile, a, h, d, o0, o1, o2, counter, 1, 0);
   UCP_LAUNCHED("k_moments");
   return UCP_OK;
