@@ -77,7 +77,8 @@ def main():
         print(json.dumps({
             "metric": "instance solves/s (config 4: 64 Witsenhausen instances, d=2000, to convergence)",
             "value": args.instances / wall, "unit": "solves/s", "n_gpus": world, "wall_s": wall,
-            "concurrency": args.concurrency, "sequential_gpu_s_per_instance": seq,
+            "engine": "batch (one kernel over (instance, point) per step)" if P.solver.BATCH_ENGINE else
+            f"threads+streams (concurrency {args.concurrency})", "sequential_gpu_s_per_instance": seq,
             "rounds": [r.total_rounds for r in mine][:8], "J_first": [r.final_objective for r in mine][:4],
             "cpu_baseline": cpu, "scaling": "weak-free (replicas only)"}), flush=True)
     if world > 1:
