@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <array>
@@ -956,6 +957,155 @@ k_mom_accum(const double* __restrict__ pre, int64_t n, const double* __restrict_
   }
 }
 
+// Small query sets, fused form (replaces k_mom_pairs + k_mom_accum): one CTA
+// owns kFQ queries.  Producer warps compute the per-pair terms of one x1
+// tile -- wp*w, (wp*w)*x, ((wp*w)*x)*x for live pairs (wp != 0), +0.0 for
+// skipped ones (kernels.py:474-485; adding +0.0 to an accumulator that
+// started at +0.0 never changes its bits) -- into a shared-memory stage while
+// 3*kFQ consumer threads (one per query and accumulator) add the previous
+// stage's terms serially in ascending support order.  Two stages, named
+// barriers (FULL: producers arrive / consumers wait; EMPTY: the reverse).
+// Tiles without a nonzero term for any query of the CTA are skipped by both
+// roles (same test as k_moments).  Bitwise equal to the serial reference.
+constexpr int kFQ = 16;                      // queries per CTA
+constexpr int kFConsWarps = 2;               // 3*kFQ = 48 consumer threads
+constexpr int kFProdWarps = 6;               // 192 producer threads
+constexpr int kFThreads = 32 * (kFConsWarps + kFProdWarps);
+constexpr int kFProd = 32 * kFProdWarps;
+static_assert(kFProd % kFQ == 0, "producer threads keep one query each");
+constexpr size_t kFSmem = 2 * 3 * kTile * kFQ * sizeof(double);  // 192 KiB
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+__global__ void __launch_bounds__(kFThreads, 1)
+k_mom_fused(const double* __restrict__ yq, int64_t n, const double* __restrict__ x, const double* __restrict__ w,
+            const double2* __restrict__ tails, const double2* __restrict__ tile_mm, int64_t m, double a, double h,
+            int64_t d, double* o0, double* o1, double* o2) {
+  extern __shared__ __align__(16) double fbuf[];  // [2][3][kTile][kFQ]
+  __shared__ __align__(16) uint64_t stab[256];
+  __shared__ double sx[kTile], sw[kTile];
+  __shared__ double2 stl[kTile];
+  __shared__ int s_left, s_right;
+  __shared__ double s_ymin, s_ymax;
+  const int tid = threadIdx.x;
+  for (int r = tid; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
+  const ucp_exp_entry* stab2 = reinterpret_cast<const ucp_exp_entry*>(stab);
+  const int64_t q0 = (int64_t)blockIdx.x * kFQ;
+  const double b = a + h * (double)(d - 1);
+  if (tid == 0) {
+    int l = 0, rr = 0;
+    double lo = INFINITY, hi = -INFINITY;
+    for (int k = 0; k < kFQ; ++k) {
+      const int64_t q = q0 + k < n ? q0 + k : n - 1;
+      const double yt = yq[q];
+      long long j = (long long)ceil((yt - a) / h - 0.5);
+      if (j < 0) j = 0;
+      if (j > d - 1) j = d - 1;
+      l |= j == 0;
+      rr |= j == d - 1;
+      lo = fmin(lo, yt);
+      hi = fmax(hi, yt);
+    }
+    s_left = l;
+    s_right = rr;
+    s_ymin = lo;
+    s_ymax = hi;
+  }
+  __syncthreads();
+  const bool has_left = s_left != 0, has_right = s_right != 0;
+  const double ymin = s_ymin, ymax = s_ymax;
+  const int64_t ntiles = (m + kTile - 1) / kTile;
+  auto live_tile = [&](int64_t tile) -> bool {
+    const double2 mm = tile_mm[tile];
+    const bool gauss_out = ymin - mm.y > kGaussCut || ymax - mm.x < -kGaussCut;
+    const bool left_out = !has_left || a - mm.x <= -kGaussCut;
+    const bool right_out = !has_right || mm.y - b <= -kGaussCut;
+    return !(gauss_out && left_out && right_out);
+  };
+  constexpr int kFull = 1, kEmpty = 3, kProd = 5;  // named barrier ids (0 is __syncthreads)
+  const int warp = tid >> 5;
+  if (warp >= kFConsWarps) {
+    // ---------------- producers
+    const int t = tid - 32 * kFConsWarps;
+    const int qq = t % kFQ;
+    const int64_t q = q0 + qq < n ? q0 + qq : n - 1;
+    const double yt = yq[q];
+    long long j = (long long)ceil((yt - a) / h - 0.5);
+    if (j < 0) j = 0;
+    if (j > d - 1) j = d - 1;
+    const bool at_left = j == 0, at_right = j == d - 1;
+    const double factor = (at_left || at_right) ? 0.5 : 1.0;
+    const double INV = inv_sqrt_2pi();
+    int k = 0;
+    for (int64_t tile = 0; tile < ntiles; ++tile) {
+      if (!live_tile(tile)) continue;
+      const int buf = k & 1;
+      if (k >= 2) named_sync(kEmpty + buf, kFThreads);
+      double* st = fbuf + (size_t)buf * 3 * kTile * kFQ;
+      const int64_t base = tile * kTile;
+      // the tile's support data, staged once per stage by the producers
+      named_sync(kProd, kFProd);  // every producer is done with the previous tile's copy
+      for (int r = t; r < kTile; r += kFProd) {
+        const int64_t i = base + r;
+        sx[r] = i < m ? x[i] : 0.0;
+        sw[r] = i < m ? w[i] : 0.0;
+        stl[r] = i < m ? tails[i] : make_double2(0.0, 0.0);
+      }
+      named_sync(kProd, kFProd);
+      for (int r = t / kFQ; r < kTile; r += kFProd / kFQ) {
+        const int64_t i = base + r;
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+        if (i < m) {
+          const double xi = sx[r];
+          const double diff = yt - xi;
+          double wp = 0.0;
+          if (diff <= kGaussCut && diff >= -kGaussCut)
+            wp = (factor * ucp_exp_core((-0.5 * diff) * diff, stab2)) * INV;
+          if (at_left) wp += stl[r].x;
+          if (at_right) wp += stl[r].y;
+          if (wp != 0.0) {
+            t0 = wp * sw[r];
+            t1 = t0 * xi;
+            t2 = t1 * xi;
+          }
+        }
+        st[(0 * kTile + r) * kFQ + qq] = t0;
+        st[(1 * kTile + r) * kFQ + qq] = t1;
+        st[(2 * kTile + r) * kFQ + qq] = t2;
+      }
+      named_arrive(kFull + buf, kFThreads);
+      ++k;
+    }
+    // absorb the consumers' last EMPTY arrivals so every barrier completes
+    for (int kk = k - 2 > 0 ? k - 2 : 0; kk < k; ++kk) named_sync(kEmpty + (kk & 1), kFThreads);
+  } else {
+    // ---------------- consumers: thread (plane, query)
+    const bool cons = tid < 3 * kFQ;
+    const int plane = tid / kFQ, qq = tid % kFQ;
+    double acc = 0.0;
+    int k = 0;
+    for (int64_t tile = 0; tile < ntiles; ++tile) {
+      if (!live_tile(tile)) continue;
+      const int buf = k & 1;
+      named_sync(kFull + buf, kFThreads);
+      if (cons) {
+        const double* st = fbuf + (size_t)buf * 3 * kTile * kFQ + (size_t)plane * kTile * kFQ + qq;
+#pragma unroll 16
+        for (int r = 0; r < kTile; ++r) acc += st[r * kFQ];
+      }
+      named_arrive(kEmpty + buf, kFThreads);
+      ++k;
+    }
+    const int64_t q = q0 + qq;
+    if (cons && q < n) (plane == 0 ? o0 : plane == 1 ? o1 : o2)[q] = acc;
+  }
+}
+
 // Stage-1 candidates: C1(u, y) = A u^2 - 2 B u + C (witsenhausen.py:73-78).
 __global__ void k_stage1_segmented(const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
                                    int64_t nseg, const double* __restrict__ m0,
@@ -1095,6 +1245,11 @@ enum {
 static_assert(WS_NSLOTS <= 16, "workspace slots");
 // two-phase moments when the query set cannot fill the GPU with the direct kernel
 constexpr int64_t kTwoPhaseMaxQueries = 8192;
+// UCP_FUSED_MOMENTS=0 selects the two-kernel form (k_mom_pairs + k_mom_accum)
+const bool g_fused_moments = [] {
+  const char* e = getenv("UCP_FUSED_MOMENTS");
+  return !(e && e[0] == '0');
+}();
 constexpr int64_t kTwoPhaseMaxPairs = (int64_t)1 << 25;  // 256 MiB of pre-weights
 // sync-free exhaustion when the candidate upper bound fits (16 B per candidate)
 constexpr int64_t kSyncFreeMaxCand = (int64_t)1 << 27;
@@ -1139,6 +1294,14 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   k_x1_prepare<<<(unsigned)ntiles, kTile, 0, st>>>(y0, u0, w, m, a, h, b, (double*)px1, (double2*)pxw,
                                                    (double2*)ptails, (double2*)ptile, kNoBatch);
   UCP_LAUNCHED("k_x1_prepare");
+  if (nq <= kTwoPhaseMaxQueries && g_fused_moments) {
+    static std::once_flag once;
+    std::call_once(once, [] { cudaFuncSetAttribute(k_mom_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem); });
+    k_mom_fused<<<nblocks(nq, kFQ), kFThreads, kFSmem, st>>>(yq, nq, (const double*)px1, w, (const double2*)ptails,
+                                                            (const double2*)ptile, m, a, h, d, o0, o1, o2);
+    UCP_LAUNCHED("k_mom_fused");
+    return UCP_OK;
+  }
   if (nq <= kTwoPhaseMaxQueries && nq * m <= kTwoPhaseMaxPairs) {
     void* ppre;
     if ((rc = ws_get(ws, WS_PAIRS, sizeof(double) * (size_t)(nq * m), &ppre))) return rc;
