@@ -967,13 +967,19 @@ k_mom_accum(const double* __restrict__ pre, int64_t n, const double* __restrict_
 // barriers (FULL: producers arrive / consumers wait; EMPTY: the reverse).
 // Tiles without a nonzero term for any query of the CTA are skipped by both
 // roles (same test as k_moments).  Bitwise equal to the serial reference.
-constexpr int kFQ = 16;                      // queries per CTA
-constexpr int kFConsWarps = 2;               // 3*kFQ = 48 consumer threads
-constexpr int kFProdWarps = 6;               // 192 producer threads
+#ifndef UCP_FQ
+#define UCP_FQ 8
+#endif
+#ifndef UCP_FPROD_WARPS
+#define UCP_FPROD_WARPS 10
+#endif
+constexpr int kFQ = UCP_FQ;                  // queries per CTA
+constexpr int kFConsWarps = (3 * kFQ + 31) / 32;  // one consumer thread per (query, accumulator)
+constexpr int kFProdWarps = UCP_FPROD_WARPS;
 constexpr int kFThreads = 32 * (kFConsWarps + kFProdWarps);
 constexpr int kFProd = 32 * kFProdWarps;
 static_assert(kFProd % kFQ == 0, "producer threads keep one query each");
-constexpr size_t kFSmem = 2 * 3 * kTile * kFQ * sizeof(double);  // 192 KiB
+constexpr size_t kFSmem = 2 * 3 * kTile * kFQ * sizeof(double);  // 96 KiB at kFQ = 8: two CTAs per SM
 
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -982,7 +988,7 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-__global__ void __launch_bounds__(kFThreads, 1)
+__global__ void __launch_bounds__(kFThreads, kFQ <= 8 ? 2 : 1)
 k_mom_fused(const double* __restrict__ yq, int64_t n, const double* __restrict__ x, const double* __restrict__ w,
             const double2* __restrict__ tails, const double2* __restrict__ tile_mm, int64_t m, double a, double h,
             int64_t d, double* o0, double* o1, double* o2) {
@@ -997,24 +1003,24 @@ k_mom_fused(const double* __restrict__ yq, int64_t n, const double* __restrict__
   const ucp_exp_entry* stab2 = reinterpret_cast<const ucp_exp_entry*>(stab);
   const int64_t q0 = (int64_t)blockIdx.x * kFQ;
   const double b = a + h * (double)(d - 1);
-  if (tid == 0) {
-    int l = 0, rr = 0;
-    double lo = INFINITY, hi = -INFINITY;
-    for (int k = 0; k < kFQ; ++k) {
-      const int64_t q = q0 + k < n ? q0 + k : n - 1;
-      const double yt = yq[q];
-      long long j = (long long)ceil((yt - a) / h - 0.5);
-      if (j < 0) j = 0;
-      if (j > d - 1) j = d - 1;
-      l |= j == 0;
-      rr |= j == d - 1;
-      lo = fmin(lo, yt);
-      hi = fmax(hi, yt);
+  if (tid < 32) {  // the CTA's query range and edge flags (warp 0, one query per lane)
+    const int64_t q = q0 + (tid % kFQ) < n ? q0 + (tid % kFQ) : n - 1;
+    const double yt = yq[q];
+    long long j = (long long)ceil((yt - a) / h - 0.5);
+    if (j < 0) j = 0;
+    if (j > d - 1) j = d - 1;
+    const unsigned l = __ballot_sync(0xffffffffu, j == 0), rr = __ballot_sync(0xffffffffu, j == d - 1);
+    double lo = yt, hi = yt;
+    for (int off = 16; off > 0; off >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, off));
     }
-    s_left = l;
-    s_right = rr;
-    s_ymin = lo;
-    s_ymax = hi;
+    if (tid == 0) {
+      s_left = l != 0;
+      s_right = rr != 0;
+      s_ymin = lo;
+      s_ymax = hi;
+    }
   }
   __syncthreads();
   const bool has_left = s_left != 0, has_right = s_right != 0;
@@ -1057,7 +1063,12 @@ k_mom_fused(const double* __restrict__ yq, int64_t n, const double* __restrict__
         stl[r] = i < m ? tails[i] : make_double2(0.0, 0.0);
       }
       named_sync(kProd, kFProd);
-      for (int r = t / kFQ; r < kTile; r += kFProd / kFQ) {
+      constexpr int kRowStep = kFProd / kFQ;
+      constexpr int kRows = (kTile + kRowStep - 1) / kRowStep;
+#pragma unroll 4
+      for (int rr = 0; rr < kRows; ++rr) {
+        const int r = t / kFQ + rr * kRowStep;
+        if (r >= kTile) break;
         const int64_t i = base + r;
         double t0 = 0.0, t1 = 0.0, t2 = 0.0;
         if (i < m) {
