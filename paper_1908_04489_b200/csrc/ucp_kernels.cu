@@ -508,6 +508,33 @@ __global__ void k_ex_fill(const double* __restrict__ u, const int64_t* __restric
   }
 }
 
+// Warp-per-point form of k_ex_fill (same candidates, same order): lane l of
+// a 32-node chunk keeps node j when j == lo or u[j] != u[j-1]; ballot +
+// popc ranks the kept nodes.  Used when the windows are short enough that a
+// lone thread's serial fill is latency-bound (small grids).
+__global__ void k_ex_fill_warp(const double* __restrict__ u, const int64_t* __restrict__ lo,
+                               const int64_t* __restrict__ hi, int64_t begin, int64_t n,
+                               const int64_t* __restrict__ offs, int32_t* cand_pt, int32_t* cand_j) {
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= n) return;  // warp-uniform
+  const int64_t i = begin + t;
+  const int64_t j0 = lo[i], j1 = hi[i];
+  int64_t pos = offs[t];
+  for (int64_t c = j0; c <= j1; c += 32) {
+    const int64_t j = c + lane;
+    const bool valid = j <= j1;
+    const bool keep = valid && (j == j0 || u[j] != u[j - 1]);
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int64_t at = pos + __popc(mask & ((1u << lane) - 1u));
+      cand_pt[at] = (int32_t)i;
+      cand_j[at] = (int32_t)j;
+    }
+    pos += __popc(mask);
+  }
+}
+
 template <int kMode, bool kBatch = false>
 __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ex0_eval(const double* __restrict__ y0, const double* __restrict__ f0,
                            const double* __restrict__ u0, double k, const double* __restrict__ v1,
@@ -1256,6 +1283,8 @@ enum {
 static_assert(WS_NSLOTS <= 16, "workspace slots");
 // two-phase moments when the query set cannot fill the GPU with the direct kernel
 constexpr int64_t kTwoPhaseMaxQueries = 8192;
+// warp-per-point candidate fill below this many points (one thread per point above)
+constexpr int64_t kWarpFillMaxPoints = 1 << 16;
 // UCP_FUSED_MOMENTS=0 selects the two-kernel form (k_mom_pairs + k_mom_accum)
 const bool g_fused_moments = [] {
   const char* e = getenv("UCP_FUSED_MOMENTS");
@@ -1626,7 +1655,11 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
   if ((rc = ws_get(ws, WS_CAND_PT, sizeof(int32_t) * (size_t)total, &ppt))) return rc;
   if ((rc = ws_get(ws, WS_CAND_J, sizeof(int32_t) * (size_t)total, &pj))) return rc;
   if ((rc = ws_get(ws, WS_COST, sizeof(double) * (size_t)total, &pc))) return rc;
-  k_ex_fill<<<nblocks(n, 256), 256, 0, st>>>(u0, win_lo, win_hi, begin, n, counts, (int32_t*)ppt,
+  if (n <= kWarpFillMaxPoints)
+    k_ex_fill_warp<<<nblocks(32 * n, 256), 256, 0, st>>>(u0, win_lo, win_hi, begin, n, counts, (int32_t*)ppt,
+                                                        (int32_t*)pj);
+  else
+    k_ex_fill<<<nblocks(n, 256), 256, 0, st>>>(u0, win_lo, win_hi, begin, n, counts, (int32_t*)ppt,
                                                (int32_t*)pj);
   UCP_LAUNCHED("k_ex_fill");
   if (int rc_ = check_aligned(u1)) return rc_;
