@@ -315,6 +315,30 @@ def run_ours(args):
              "termination": rp.termination, "reference_cpu_s": 1437.4,
              "reference_cpu": "numba reference, 8-core Xeon (SURVEY.md Appendix B)"}
     del pp, rp
+    # config 4: 64 independent instances (k in [0.05, 1], sigma in {3, 5, 7}) at d=2000 to
+    # convergence -- the batched engine (one kernel over (instance, point) per step);
+    # instances k % world per rank ("replicas only")
+    sweep = [(0.05 + 0.95 * i / 63, (3.0, 5.0, 7.0)[i % 3]) for i in range(64)]
+    P.solve_many([P.Witsenhausen(k=k, sigma=s_) for k, s_ in sweep[:4]], P.SolverConfig(max_rounds=2),
+                 sharding=sh)  # first launches of the batched kernels
+    sprobs = [P.Witsenhausen(k=k, sigma=s_) for k, s_ in sweep]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = time.perf_counter()
+    sres = P.solve_many(sprobs, P.SolverConfig(), sharding=sh)
+    torch.cuda.synchronize()
+    swall = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(swall, op=dist.ReduceOp.MAX)
+    swall = float(swall.item())
+    config4 = {"config": "64 Witsenhausen instances, k = 0.05 + 0.95 i/63, sigma = (3, 5, 7)[i % 3], d=2000, "
+                         "default SolverConfig, to convergence; instances k % world per rank",
+               "wall_s": swall, "solves_per_s": 64 / swall, "engine": "batched (csrc/ucp_batch.cuh)",
+               "rounds_max": max(r.total_rounds for r in sres if r is not None),
+               "reference_cpu_s_per_instance": 7.5,
+               "reference_cpu": "oracle port on 16 cores, profiles/r1_sweep_c4.json"}
+    del sprobs, sres
 
     prob = P.Witsenhausen(k=K_WC, sigma=SIGMA, grids=[(*SPAN, d), (*SPAN, d)])
     h = prob.grids[0].spacing
@@ -463,7 +487,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(args, d, counts),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "phase_ms": dict(zip(["local0", "local1", "exh0", "exh1", "objective"], phase_ms.round(3).tolist())),
-            "time_to_converge": c1, "time_to_converge_paper_size": paper, "gpu": torch.cuda.get_device_name(dev),
+            "time_to_converge": c1, "time_to_converge_paper_size": paper, "config4_sweep": config4,
+            "gpu": torch.cuda.get_device_name(dev),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -35,7 +35,7 @@ from .device_problem import NO_ERROR
 from .grids import ControllerSet, SampledController
 from .solver import RoundReport, SolveResult, SolverConfig, adaptive_allocation, solve
 
-__all__ = ["solve_batch", "MAX_BATCH"]
+__all__ = ["solve_batch", "schedule_rounds", "MAX_BATCH"]
 
 MAX_BATCH = 1024
 LAST_STATS: dict = {}  # host-side timing of the last solve_batch (diagnostics)
@@ -140,6 +140,87 @@ def _engine(dev, B, g0, g1, cfg, lib) -> _Engine:
     return eng
 
 
+def schedule_rounds(dev, B: int, cfg: SolverConfig, stats: dict | None = None):
+    """Per-instance round schedules of B instances advanced in lock-step ticks
+    (reference solver.py:234-290 for each instance).
+
+    ``dev`` provides iterate(kind, ids, iters) [kind 0 local / 1 exhaustion],
+    objective(lane, ids, row) [row 0 start, 1 after local, 2 after
+    exhaustion], order() [join the two lanes], read() -> (J[3, B], err[B, 6],
+    err_obj[B]) after a synchronisation, and failed(i) [raise instance i's
+    error].  Returns (final objectives, round reports, terminations).
+    Host-side only, so it is tested on CPU with an oracle-backed ``dev``.
+    """
+    stats = stats if stats is not None else {}
+    stats.setdefault("events", 0)
+    stats.setdefault("decisions", 0)
+    n = cfg.iters_per_round
+    adaptive = cfg.fixed_local_iters is None
+    everyone = list(range(B))
+    dev.objective(0, everyone, 0)
+    host_j, _, eo = dev.read()
+    bad = (np.asarray(eo) != NO_ERROR).nonzero()[0]
+    if bad.size:
+        dev.failed(int(bad[0]))
+    current = [float(host_j[0, i]) for i in everyone]
+    n_local = [n // 2 if adaptive else cfg.fixed_local_iters] * B
+    phase = [0] * B  # 0 local block, 1 exhaustion block
+    rem = list(n_local)
+    round_index = [1] * B
+    reports = [[] for _ in range(B)]
+    termination = ["max_rounds"] * B
+    active = list(everyone)
+    t_round = time.perf_counter()
+    while active:
+        L = [i for i in active if phase[i] == 0]
+        E = [i for i in active if phase[i] == 1]
+        k = min(rem[i] for i in active)
+        if L:
+            dev.iterate(0, L, k)
+        if E:
+            dev.iterate(1, E, k)
+        for i in active:
+            rem[i] -= k
+        ended_l = [i for i in L if rem[i] == 0]
+        ended_e = [i for i in E if rem[i] == 0]
+        if ended_l:
+            dev.objective(0, ended_l, 1)
+            for i in ended_l:
+                phase[i], rem[i] = 1, n - n_local[i]
+        if ended_e:
+            dev.objective(1, ended_e, 2)
+        dev.order()
+        stats["events"] += 1
+        if not ended_e:
+            continue
+        # N_L + N_P = iters_per_round: every active instance ends its round here
+        stats["decisions"] += 1
+        host_j, e_host, eo_host = dev.read()
+        wall = (time.perf_counter() - t_round) * 1000.0
+        t_round = time.perf_counter()
+        for i in ended_e:
+            if (np.asarray(e_host[i]) != NO_ERROR).any() or eo_host[i] != NO_ERROR:
+                dev.failed(i)
+            after_local, after_exh = float(host_j[1, i]), float(host_j[2, i])
+            local_gain = abs(current[i] - after_local)
+            exhaustion_gain = abs(after_local - after_exh)
+            current[i] = after_exh
+            reports[i].append(RoundReport(round_index[i], after_exh, local_gain, exhaustion_gain, n_local[i],
+                                          n - n_local[i], wall, after_local))
+            if local_gain + exhaustion_gain <= cfg.precision:
+                termination[i] = "converged"
+                active.remove(i)
+                continue
+            if round_index[i] == cfg.max_rounds:
+                active.remove(i)
+                continue
+            if adaptive:
+                n_local[i], _ = adaptive_allocation(local_gain, exhaustion_gain, n)
+            round_index[i] += 1
+            phase[i], rem[i] = 0, n_local[i]
+    return current, reports, termination
+
+
 _LOCK = threading.Lock()  # engines are shared: one solve_batch at a time
 
 
@@ -200,93 +281,41 @@ def _solve_batch(problems, cfg, initials) -> list:
     def call(name, *args):
         _lib.check(getattr(lib, name)(*args), name)
 
-    def objective(lane, ids, row):
-        call("ucp_wc_batch_objective", handle, lane, _ids(ids), len(ids), J[row].data_ptr(), ptr(err_obj),
-             lanes[lane].cuda_stream)
+    class Dev:
+        """The device side of the schedule (see schedule_rounds)."""
 
-    def failed(i):  # re-run alone: raises the reference's exact error
-        solve(problems[i], cfg, initials[i])
-        raise RuntimeError(f"batch instance {i} flagged a numeric error its single solve did not reproduce")
+        def iterate(self, kind, ids, iters):
+            lane = kind  # lane 0: local-update group, lane 1: exhaustion group
+            call("ucp_wc_batch_iterate", handle, lane, kind, _ids(ids), len(ids), iters, ptr(err),
+                 lanes[lane].cuda_stream)
 
-    stats = {"t_setup": time.perf_counter() - t_start, "events": 0, "decisions": 0, "t_sync": 0.0}
-    try:
-        n = cfg.iters_per_round
-        adaptive = cfg.fixed_local_iters is None
-        everyone = list(range(B))
-        objective(0, everyone, 0)
-        lanes[0].synchronize()
-        host_j = J[0].cpu().numpy()
-        bad = (err_obj.cpu().numpy() != NO_ERROR).nonzero()[0]
-        if bad.size:
-            failed(int(bad[0]))
-        current = host_j.astype(np.float64).tolist()
-        n_local = [n // 2 if adaptive else cfg.fixed_local_iters] * B
-        phase = [0] * B  # 0 local block, 1 exhaustion block
-        rem = list(n_local)
-        round_index = [1] * B
-        reports = [[] for _ in range(B)]
-        termination = ["max_rounds"] * B
-        active = list(everyone)
-        t_round = time.perf_counter()
-        while active:
-            L = [i for i in active if phase[i] == 0]
-            E = [i for i in active if phase[i] == 1]
-            k = min(rem[i] for i in active)
-            if L:
-                call("ucp_wc_batch_iterate", handle, 0, 0, _ids(L), len(L), k, ptr(err), lanes[0].cuda_stream)
-            if E:
-                call("ucp_wc_batch_iterate", handle, 1, 1, _ids(E), len(E), k, ptr(err), lanes[1].cuda_stream)
-            for i in active:
-                rem[i] -= k
-            ended_l = [i for i in L if rem[i] == 0]
-            ended_e = [i for i in E if rem[i] == 0]
-            if ended_l:
-                objective(0, ended_l, 1)
-                for i in ended_l:
-                    phase[i], rem[i] = 1, n - n_local[i]
-            if ended_e:
-                objective(1, ended_e, 2)
-            # instances change lanes at block ends: order the two streams
+        def objective(self, lane, ids, row):
+            call("ucp_wc_batch_objective", handle, lane, _ids(ids), len(ids), J[row].data_ptr(), ptr(err_obj),
+                 lanes[lane].cuda_stream)
+
+        def order(self):  # instances change lanes at block ends
             lanes[1].wait_stream(lanes[0])
             lanes[0].wait_stream(lanes[1])
-            stats["events"] += 1
-            if not ended_e:
-                continue
-            stats["decisions"] += 1
+
+        def read(self):
             ts = time.perf_counter()
             lanes[0].synchronize()
             stats["t_sync"] += time.perf_counter() - ts
-            host_j = J.cpu().numpy()
-            e_host = err.cpu().numpy()
-            eo_host = err_obj.cpu().numpy()
-            wall = (time.perf_counter() - t_round) * 1000.0
-            t_round = time.perf_counter()
-            for i in ended_e:
-                if (e_host[i] != NO_ERROR).any() or eo_host[i] != NO_ERROR:
-                    failed(i)
-                after_local, after_exh = float(host_j[1, i]), float(host_j[2, i])
-                local_gain = abs(current[i] - after_local)
-                exhaustion_gain = abs(after_local - after_exh)
-                current[i] = after_exh
-                reports[i].append(RoundReport(round_index[i], after_exh, local_gain, exhaustion_gain, n_local[i],
-                                              n - n_local[i], wall, after_local))
-                if local_gain + exhaustion_gain <= cfg.precision:
-                    termination[i] = "converged"
-                    active.remove(i)
-                    continue
-                if round_index[i] == cfg.max_rounds:
-                    active.remove(i)
-                    continue
-                if adaptive:
-                    n_local[i], _ = adaptive_allocation(local_gain, exhaustion_gain, n)
-                round_index[i] += 1
-                phase[i], rem[i] = 0, n_local[i]
+            return J.cpu().numpy(), err.cpu().numpy(), err_obj.cpu().numpy()
+
+        def failed(self, i):  # re-run alone: raises the reference's exact error
+            solve(problems[i], cfg, initials[i])
+            raise RuntimeError(f"batch instance {i} flagged a numeric error its single solve did not reproduce")
+
+    stats = {"t_setup": time.perf_counter() - t_start, "t_sync": 0.0}
+    try:
+        current, reports, termination = schedule_rounds(Dev(), B, cfg, stats)
         torch.cuda.current_stream(dev).wait_stream(lanes[0])
         stats["t_loop_end"] = time.perf_counter() - t_start
         LAST_STATS.clear()
         LAST_STATS.update(stats)
         out = []
-        for i in everyone:
+        for i in range(B):
             U = ControllerSet((SampledController(g0, U0[i, :d0].clone(), _trusted_device=True),
                                SampledController(g1, U1[i, :d1].clone(), _trusted_device=True)))
             out.append(SolveResult(controllers=U, final_objective=current[i], rounds=tuple(reports[i]),
