@@ -1283,6 +1283,12 @@ enum {
 static_assert(WS_NSLOTS <= 16, "workspace slots");
 // two-phase moments when the query set cannot fill the GPU with the direct kernel
 constexpr int64_t kTwoPhaseMaxQueries = 8192;
+// fused moments below this many queries (above, k_moments' persistent CTAs
+// have enough query blocks to fill the GPU); env UCP_FUSED_MAX_QUERIES
+const int64_t kFusedMaxQueries = [] {
+  const char* e = getenv("UCP_FUSED_MAX_QUERIES");
+  return e ? (int64_t)atoll(e) : (int64_t)16384;  // crossover measured with tools/moments_sweep.py
+}();
 // warp-per-point candidate fill below this many points (one thread per point above)
 constexpr int64_t kWarpFillMaxPoints = 1 << 16;
 // UCP_FUSED_MOMENTS=0 selects the two-kernel form (k_mom_pairs + k_mom_accum)
@@ -1334,7 +1340,7 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   k_x1_prepare<<<(unsigned)ntiles, kTile, 0, st>>>(y0, u0, w, m, a, h, b, (double*)px1, (double2*)pxw,
                                                    (double2*)ptails, (double2*)ptile, kNoBatch);
   UCP_LAUNCHED("k_x1_prepare");
-  if (nq <= kTwoPhaseMaxQueries && g_fused_moments) {
+  if (nq <= kFusedMaxQueries && g_fused_moments) {
     static std::once_flag once;
     std::call_once(once, [] { cudaFuncSetAttribute(k_mom_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem); });
     k_mom_fused<<<nblocks(nq, kFQ), kFThreads, kFSmem, st>>>(yq, nq, (const double*)px1, w, (const double2*)ptails,
