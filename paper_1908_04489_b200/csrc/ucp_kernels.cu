@@ -901,90 +901,8 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
   }
 }
 
-// Small query sets (d ~ 2000): the direct kernel above would run a handful of
-// CTAs whose serial pair loops are pure latency.  Two-phase form instead:
-//  (A) every (support point i, query q) pair's pre-weight -- the reference's
-//      `wp` before `wp *= w[i]` (kernels.py:474-480) -- in parallel, stored
-//      q-contiguous;
-//  (B) one thread per query accumulates them in ascending i exactly as the
-//      reference does (`if wp != 0: wp *= w[i]; acc += ...`).
-// Same operations in the same order per pair and per accumulator: bitwise
-// equal to the direct kernel.
-constexpr int kPairChunk = 16;
-__global__ void __launch_bounds__(128)
-k_mom_pairs(const double* __restrict__ yq, int64_t n, const double* __restrict__ x,
-            const double2* __restrict__ tails, int64_t m, double a, double h, int64_t d, double* pre) {
-  __shared__ __align__(16) uint64_t stab[256];
-  for (int r = threadIdx.x; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
-  __syncthreads();
-  const ucp_exp_entry* stab2 = reinterpret_cast<const ucp_exp_entry*>(stab);
-  const int64_t q = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
-  if (q >= n) return;
-  const double yt = yq[q];
-  long long j = (long long)ceil((yt - a) / h - 0.5);
-  if (j < 0) j = 0;
-  if (j > d - 1) j = d - 1;
-  const bool at_left = j == 0, at_right = j == d - 1;
-  const double factor = (at_left || at_right) ? 0.5 : 1.0;
-  const double INV = inv_sqrt_2pi();
-  const int64_t i0 = (int64_t)blockIdx.x * kPairChunk;
-  const int64_t i1 = i0 + kPairChunk < m ? i0 + kPairChunk : m;
-  for (int64_t i = i0; i < i1; ++i) {
-    const double xi = x[i];
-    const double diff = yt - xi;
-    double wp = 0.0;
-    if (diff <= kGaussCut && diff >= -kGaussCut) wp = (factor * ucp_exp_core((-0.5 * diff) * diff, stab2)) * INV;
-    if (at_left) wp += tails[i].x;
-    if (at_right) wp += tails[i].y;
-    pre[i * n + q] = wp;
-  }
-}
-
-__global__ void __launch_bounds__(128)
-k_mom_accum(const double* __restrict__ pre, int64_t n, const double* __restrict__ x,
-            const double* __restrict__ w, int64_t m, double* o0, double* o1, double* o2) {
-  // latency-bound by construction (one serial chain per query): keep 32
-  // pre-weight loads in flight per thread, x/w staged through shared memory
-  constexpr int kB = 32;
-  __shared__ double sx[256], sw[256];
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = q < n;
-  const double* col = pre + (active ? q : 0);
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-  for (int64_t base = 0; base < m; base += 256) {
-    const int cnt = (int)(m - base < 256 ? m - base : 256);
-    __syncthreads();
-    for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
-      sx[r] = x[base + r];
-      sw[r] = w[base + r];
-    }
-    __syncthreads();
-    for (int r0 = 0; r0 < cnt; r0 += kB) {
-      double pv[kB];
-#pragma unroll
-      for (int k = 0; k < kB; ++k) pv[k] = (active && r0 + k < cnt) ? __ldcs(col + (base + r0 + k) * n) : 0.0;
-#pragma unroll
-      for (int k = 0; k < kB; ++k) {
-        double wp = pv[k];
-        if (wp != 0.0) {  // kernels.py:481 (padding slots are 0.0)
-          const double xi = sx[r0 + k];
-          wp *= sw[r0 + k];
-          acc0 += wp;
-          const double wx = wp * xi;
-          acc1 += wx;
-          acc2 += wx * xi;
-        }
-      }
-    }
-  }
-  if (active) {
-    o0[q] = acc0;
-    o1[q] = acc1;
-    o2[q] = acc2;
-  }
-}
-
-// Small query sets, fused form (replaces k_mom_pairs + k_mom_accum): one CTA
+// Small query sets (d ~ 2000 .. 16k): the direct kernel above would run too
+// few CTAs, each query's serial pair loop pure latency.  Fused form: one CTA
 // owns kFQ queries.  Producer warps compute the per-pair terms of one x1
 // tile -- wp*w, (wp*w)*x, ((wp*w)*x)*x for live pairs (wp != 0), +0.0 for
 // skipped ones (kernels.py:474-485; adding +0.0 to an accumulator that
@@ -1277,12 +1195,10 @@ struct ucp_workspace {
 
 namespace {
 enum {
-  WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS, WS_PAIRS,
+  WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS,
   WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_NSLOTS
 };
 static_assert(WS_NSLOTS <= 16, "workspace slots");
-// two-phase moments when the query set cannot fill the GPU with the direct kernel
-constexpr int64_t kTwoPhaseMaxQueries = 8192;
 // fused moments below this many queries (above, k_moments' persistent CTAs
 // have enough query blocks to fill the GPU); env UCP_FUSED_MAX_QUERIES
 const int64_t kFusedMaxQueries = [] {
@@ -1291,12 +1207,6 @@ const int64_t kFusedMaxQueries = [] {
 }();
 // warp-per-point candidate fill below this many points (one thread per point above)
 constexpr int64_t kWarpFillMaxPoints = 1 << 16;
-// UCP_FUSED_MOMENTS=0 selects the two-kernel form (k_mom_pairs + k_mom_accum)
-const bool g_fused_moments = [] {
-  const char* e = getenv("UCP_FUSED_MOMENTS");
-  return !(e && e[0] == '0');
-}();
-constexpr int64_t kTwoPhaseMaxPairs = (int64_t)1 << 25;  // 256 MiB of pre-weights
 // sync-free exhaustion when the candidate upper bound fits (16 B per candidate)
 constexpr int64_t kSyncFreeMaxCand = (int64_t)1 << 27;
 
@@ -1340,23 +1250,12 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   k_x1_prepare<<<(unsigned)ntiles, kTile, 0, st>>>(y0, u0, w, m, a, h, b, (double*)px1, (double2*)pxw,
                                                    (double2*)ptails, (double2*)ptile, kNoBatch);
   UCP_LAUNCHED("k_x1_prepare");
-  if (nq <= kFusedMaxQueries && g_fused_moments) {
+  if (nq <= kFusedMaxQueries) {
     static std::once_flag once;
     std::call_once(once, [] { cudaFuncSetAttribute(k_mom_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem); });
     k_mom_fused<<<nblocks(nq, kFQ), kFThreads, kFSmem, st>>>(yq, nq, (const double*)px1, w, (const double2*)ptails,
                                                             (const double2*)ptile, m, a, h, d, o0, o1, o2);
     UCP_LAUNCHED("k_mom_fused");
-    return UCP_OK;
-  }
-  if (nq <= kTwoPhaseMaxQueries && nq * m <= kTwoPhaseMaxPairs) {
-    void* ppre;
-    if ((rc = ws_get(ws, WS_PAIRS, sizeof(double) * (size_t)(nq * m), &ppre))) return rc;
-    dim3 grid_a((unsigned)((m + kPairChunk - 1) / kPairChunk), nblocks(nq, 128));
-    k_mom_pairs<<<grid_a, 128, 0, st>>>(yq, nq, (const double*)px1, (const double2*)ptails, m, a, h, d,
-                                        (double*)ppre);
-    UCP_LAUNCHED("k_mom_pairs");
-    k_mom_accum<<<nblocks(nq, 128), 128, 0, st>>>((const double*)ppre, nq, (const double*)px1, w, m, o0, o1, o2);
-    UCP_LAUNCHED("k_mom_accum");
     return UCP_OK;
   }
   int* counter = (int*)((int64_t*)pctr + 1);

@@ -238,17 +238,18 @@ def test_no_cpu_fallback_and_launches(P):
     assert _lib.LIB_PATH.exists()
 
 
-@pytest.mark.parametrize("nq,m", [(10_000, 4096), (9000, 257)])
+@pytest.mark.parametrize("nq,m", [(10_000, 4096), (9000, 257), (20_000, 4096), (17_000, 257), (3, 5000)])
 def test_moments_direct_path_vs_oracle(P, oracle_mod, nq, m):
-    """Query sets above the two-phase threshold take the persistent tiled kernel
-    (tile skipping, edge blocks, work queue); bitwise vs the oracle."""
+    """Both moments kernels on unsorted queries: up to 16,384 queries the fused
+    producer/consumer kernel, above it the persistent tiled kernel (tile
+    skipping, edge blocks, work queue); bitwise vs the oracle."""
     rng = np.random.default_rng(nq)
     a, b = -20.0, 20.0
     h = (b - a) / (m - 1)
     x = np.sort(rng.uniform(-35, 35, m)) + rng.normal(0, 0.5, m)  # mostly increasing, some disorder
     x[::97] = x[::97][::-1]
     w = np.abs(rng.normal(0, 1, m)) * h
-    y = np.concatenate([[a, b, a - 1.0, b + 1.0], rng.uniform(a - 2, b + 2, nq - 4)])
+    y = np.concatenate([[a, b, a - 1.0, b + 1.0], rng.uniform(a - 2, b + 2, max(nq - 4, 0))])[:nq]
     got = P.kernels.gauss_moments_points(y, x, w, a, h, m)
     want = oracle_mod.gauss_moments_points(y, x, w, a, h, m)
     for k in range(3):
