@@ -19,6 +19,7 @@
 #include <vector>
 #include <mutex>
 #include <shared_mutex>
+#include <set>
 #include <unordered_set>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
@@ -75,6 +76,17 @@ int arg_fail(const char* msg) {
 }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Opt a kernel in to more than 48 KiB of dynamic shared memory, once per
+// (kernel, device): the attribute lives in each device's context.
+std::mutex g_smem_mu;
+std::set<std::pair<const void*, int>> g_smem_ok;
+void smem_opt_in(const void* fn, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_smem_mu);
+  if (g_smem_ok.insert({fn, dev}).second) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 inline unsigned nblocks(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
 // --------------------------------------------------------------------------
@@ -1251,8 +1263,7 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
                                                    (double2*)ptails, (double2*)ptile, kNoBatch);
   UCP_LAUNCHED("k_x1_prepare");
   if (nq <= kFusedMaxQueries) {
-    static std::once_flag once;
-    std::call_once(once, [] { cudaFuncSetAttribute(k_mom_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem); });
+    smem_opt_in(reinterpret_cast<const void*>(k_mom_fused), kFSmem);
     k_mom_fused<<<nblocks(nq, kFQ), kFThreads, kFSmem, st>>>(yq, nq, (const double*)px1, w, (const double2*)ptails,
                                                             (const double2*)ptile, m, a, h, d, o0, o1, o2);
     UCP_LAUNCHED("k_mom_fused");
@@ -1287,14 +1298,9 @@ bool walk_latency_mode(int64_t n_walks) {
 // kSmemWalkMax doubles of v1 fit the opt-in shared memory of one CTA
 constexpr int64_t kSmemWalkMax = 27648;  // 216 KiB of the 227 KiB opt-in per CTA
 
-std::mutex g_smem_mu;
-std::unordered_set<const void*> g_smem_ok;
-
 template <class K>
-void allow_smem(K* kernel) {  // opt in to >48 KiB dynamic shared memory, once per kernel
-  std::lock_guard<std::mutex> lock(g_smem_mu);
-  if (g_smem_ok.insert(reinterpret_cast<const void*>(kernel)).second)
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemWalkMax * sizeof(double)));
+void allow_smem(K* kernel) {  // opt in to >48 KiB dynamic shared memory (walk kernels)
+  smem_opt_in(reinterpret_cast<const void*>(kernel), kSmemWalkMax * sizeof(double));
 }
 
 #define UCP_WALK_LAUNCH(kernel, n_walks, grid, stream, d_v1, ...)                                   \
