@@ -131,7 +131,6 @@ class _DeviceSweeps:
         """problem.py:110-127: stage-0 integrand on device + serial trapezoid."""
         self.check_controllers(U)
         D = self.device_context()
-        D.errors.flush(sharding)
         g = self.grids[0]
         ts = self._uptrs(U)
         begin, end = sharding.bounds(g.d)
@@ -141,7 +140,7 @@ class _DeviceSweeps:
         sharding.allgather_(terms)
         sharding.allreduce_min_(res[1:])
         _lib.call("ucp_trapezoid_sum", ptr(terms), g.d, g.spacing, res[:1].data_ptr(), None, D.stream)
-        host = res.cpu().numpy()
+        host = D.errors.flush(sharding, extra=res)  # earlier phases' failures first, one sync
         bad = int(host[1])
         if bad != NO_ERROR:
             raise NumericError(

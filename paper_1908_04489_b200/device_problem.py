@@ -53,13 +53,21 @@ class ErrorLog:
         self.meta.extend(metas)
         return self.rows[start:start + need]
 
-    def flush(self, sharding: Sharding) -> None:
+    def flush(self, sharding: Sharding, extra: torch.Tensor | None = None):
+        """Read the pending rows (one device-to-host copy, together with the
+        int64 tensor ``extra`` if given, whose host copy is returned) and
+        raise the first recorded failure."""
         n = len(self.meta)
         if n == 0:
-            return
+            return None if extra is None else extra.cpu().numpy()
         rows = self.rows[:n]
         sharding.allreduce_min_(rows)
-        host = rows.cpu().numpy()
+        if extra is None:
+            host = rows.cpu().numpy()
+            extra_host = None
+        else:
+            both = torch.cat([rows.reshape(-1), extra.reshape(-1)]).cpu().numpy()
+            host, extra_host = both[: 3 * n].reshape(n, 3), both[3 * n:]
         rows.fill_(NO_ERROR)
         meta, self.meta = self.meta, []
         for entry, row in zip(meta, host):
@@ -73,6 +81,7 @@ class ErrorLog:
                 self.problem._replay_block_error(entry[2], sharding)
                 raise AssertionError("block failure did not reproduce")
             raise _phase_error(self.problem, kind, m, row)
+        return extra_host
 
 
 def _phase_error(problem, kind, m, row):

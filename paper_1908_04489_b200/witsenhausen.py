@@ -253,7 +253,6 @@ class Witsenhausen(Problem):
         """problem.py:110-127: stage-0 integrand on device, then the serial trapezoid."""
         self.check_controllers(U)
         D = self.device_context()
-        D.errors.flush(sharding)  # earlier phases fail first, in order
         g = self.grids[0]
         u0, u1 = self._uv(U)
         bounds = self._plan(0, U, sharding)
@@ -265,7 +264,9 @@ class Witsenhausen(Problem):
         terms = sharding.gather(buf, bounds, g.d)
         sharding.allreduce_min_(res[1:])
         _lib.call("ucp_trapezoid_sum", ptr(terms), g.d, g.spacing, res[:1].data_ptr(), None, D.stream)
-        host = res.cpu().numpy()
+        # one synchronisation: the pending phase-error rows and J travel together;
+        # earlier phases' failures are raised first, in order
+        host = D.errors.flush(sharding, extra=res)
         bad = int(host[1])
         if bad != NO_ERROR:
             raise NumericError(
