@@ -42,7 +42,17 @@ P.Witsenhausen(grids=[(-25.0, 25.0, 201)] * 2).objective(
     P.Witsenhausen(grids=[(-25.0, 25.0, 201)] * 2).identity_controllers())  # context warm-up
 torch.cuda.synchronize()
 t = time.perf_counter()
-res = P.solve(prob, cfg, initial=initial)
+t_last = [t]
+
+
+def progress(r):
+    now = time.perf_counter()
+    print(json.dumps({"round": r.round_index, "J": r.objective, "local_iters": r.local_iters,
+                      "elapsed_s": now - t, "round_s": now - t_last[0]}), flush=True)
+    t_last[0] = now
+
+
+res = P.solve(prob, cfg, initial=initial, on_round=progress)
 torch.cuda.synchronize()
 wall = time.perf_counter() - t
 print(json.dumps({"d": args.d, "warm": args.warm, "search_radius": cfg.radius_for(prob.grids[0]),
