@@ -63,7 +63,7 @@ class ErrorLog:
         rows = self.rows[:n]
         sharding.allreduce_min_(rows)
         if extra is None:
-            host = rows.cpu().numpy()
+            host = rows.cpu().numpy().copy()  # (a CPU tensor's .cpu() is itself: rows are reset below)
             extra_host = None
         else:
             both = torch.cat([rows.reshape(-1), extra.reshape(-1)]).cpu().numpy()
