@@ -221,3 +221,33 @@ def test_device_monte_carlo_rank_invariant(world):
     ref = P.device_monte_carlo_objective(prob, prob.identity_controllers(), n, seed=11)
     for r in range(world):
         assert np.array(out[r]).view(np.uint64).tolist() == np.array(ref).view(np.uint64).tolist()
+
+
+# ------------------------- config 4 across ranks: instances k % world, batched
+def _gpu_many_worker(rank, world, port, q):
+    _init(rank, world, port)
+    import paper_1908_04489_b200 as P
+
+    torch.cuda.set_device(0)
+    probs = [P.Witsenhausen(k=0.1 + 0.2 * i, sigma=(3.0, 5.0)[i % 2], grids=[(-25.0, 25.0, 201)] * 2)
+             for i in range(6)]
+    res = P.solve_many(probs, P.SolverConfig(max_rounds=3), sharding=P.from_process_group())
+    out = {k: (r.final_objective, np.asarray(r.controllers.values(0))) for k, r in enumerate(res) if r is not None}
+    dist.destroy_process_group()
+    q.put((rank, out))
+
+
+@pytest.mark.gpu
+def test_solve_many_replicas_world2():
+    """Each rank solves its instances (k % world) with the batched engine;
+    every instance is bitwise its single-process solve."""
+    import paper_1908_04489_b200 as P
+
+    out = _spawn(_gpu_many_worker, 2)
+    assert sorted(out[0]) == [0, 2, 4] and sorted(out[1]) == [1, 3, 5]
+    for r in (0, 1):
+        for k, (J, u0) in out[r].items():
+            p = P.Witsenhausen(k=0.1 + 0.2 * k, sigma=(3.0, 5.0)[k % 2], grids=[(-25.0, 25.0, 201)] * 2)
+            ref = P.solve(p, P.SolverConfig(max_rounds=3))
+            assert J == ref.final_objective
+            assert np.array_equal(u0.view(np.uint64), np.asarray(ref.controllers.values(0)).view(np.uint64))
