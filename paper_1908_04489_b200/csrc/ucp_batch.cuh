@@ -34,6 +34,14 @@ constexpr int kMaxBatchIds = 1024;
 #define UCP_BATCH_MOM_UNROLL 8
 #endif
 constexpr int kBatchMomUnroll = UCP_BATCH_MOM_UNROLL;
+#ifndef UCP_BATCH_MOM_QT
+#define UCP_BATCH_MOM_QT 128
+#endif
+#ifndef UCP_BATCH_MOM_MINB
+#define UCP_BATCH_MOM_MINB 3
+#endif
+constexpr int kBatchMomQT = UCP_BATCH_MOM_QT;  // queries per CTA work item
+constexpr int kBatchMomMinB = UCP_BATCH_MOM_MINB;
 struct IdList {
   int32_t v[kMaxBatchIds];
 };
@@ -165,11 +173,12 @@ int batch_moments(ucp_wc_batch* b, ucp_wc_batch::Lane& L, int S, cudaStream_t st
   int dev = 0, sms = 0, per_sm = 0;
   UCP_CHECK(cudaGetDevice(&dev));
   UCP_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  UCP_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_moments<kBatchMomUnroll, 3>, kMomThreads, 0));
-  const int64_t nitems = (int64_t)S * ((D.d1 + kMomThreads - 1) / kMomThreads);
+  UCP_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, k_moments<kBatchMomUnroll, kBatchMomMinB, kBatchMomQT>, kBatchMomQT, 0));
+  const int64_t nitems = (int64_t)S * ((D.d1 + kBatchMomQT - 1) / kBatchMomQT);
   int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > nitems) grid = nitems;
-  k_moments<kBatchMomUnroll, 3><<<(unsigned)grid, kMomThreads, 0, st>>>(D.y1, D.d1, L.xw, L.tails, m, L.tile_mm, D.a1, D.h1, D.d1, L.mom,
+  k_moments<kBatchMomUnroll, kBatchMomMinB, kBatchMomQT><<<(unsigned)grid, kBatchMomQT, 0, st>>>(D.y1, D.d1, L.xw, L.tails, m, L.tile_mm, D.a1, D.h1, D.d1, L.mom,
                                                     L.mom + D.d1, L.mom + 2 * D.d1, L.counter, S, 3 * D.d1);
   UCP_LAUNCHED("k_moments");
   return UCP_OK;

@@ -711,8 +711,8 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 constexpr int kMomThreads = 128;
 // kUnroll pairs' exp() in flight per thread; the batched engine (few CTAs per
 // SM) instantiates a deeper unroll with a looser register bound.
-template <int kMomUnroll = 4, int kMinBlocks = 6>
-__global__ void __launch_bounds__(kMomThreads, kMinBlocks)
+template <int kMomUnroll = 4, int kMinBlocks = 6, int kQT = kMomThreads>
+__global__ void __launch_bounds__(kQT, kMinBlocks)
 k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ xw,
           const double2* __restrict__ tails, int64_t m, const double2* __restrict__ tile_mm, double a, double h,
           int64_t d, double* o0, double* o1, double* o2, int* work_counter, int64_t nslots, int64_t sout) {
@@ -722,12 +722,12 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
   __shared__ __align__(8) uint64_t sbar[2];
   __shared__ double2 slr[kTile];
   __shared__ __align__(16) uint64_t stab[256];
-  __shared__ double s_ymin[kMomThreads / 32], s_ymax[kMomThreads / 32];
+  __shared__ double s_ymin[kQT / 32], s_ymax[kQT / 32];
   __shared__ int s_left, s_right;
   __shared__ long long s_work;
   for (int r = threadIdx.x; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
   const ucp_exp_entry* stab2 = reinterpret_cast<const ucp_exp_entry*>(stab);
-  const int64_t nqb = (n + kMomThreads - 1) / kMomThreads;
+  const int64_t nqb = (n + kQT - 1) / kQT;
   // work items: the edge query blocks of every slot first (they visit the most
   // tiles), then the interior blocks; one slot == the single-instance order
   const int64_t nedge = nqb == 1 ? 1 : 2;
@@ -766,7 +766,7 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
     o1 = o10 + slot * sout;
     o2 = o20 + slot * sout;
     if (threadIdx.x == 0) s_left = s_right = 0;
-    const int64_t t = qb * kMomThreads + threadIdx.x;
+    const int64_t t = qb * kQT + threadIdx.x;
     const bool active = t < n;
     const double yt = active ? yq[t] : yq[n - 1];
     long long j = (long long)ceil((yt - a) / h - 0.5);
@@ -789,7 +789,7 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
     __syncthreads();
     ymin = s_ymin[0];
     ymax = s_ymax[0];
-    for (int r = 1; r < kMomThreads / 32; ++r) {
+    for (int r = 1; r < kQT / 32; ++r) {
       ymin = fmin(ymin, s_ymin[r]);
       ymax = fmax(ymax, s_ymax[r]);
     }
@@ -865,7 +865,7 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
         const int64_t base = tile * kTile;
         const int cnt = (int)(m - base < kTile ? m - base : kTile);
         __syncthreads();
-        for (int r = threadIdx.x; r < kTile; r += kMomThreads) {
+        for (int r = threadIdx.x; r < kTile; r += kQT) {
           sxw[r] = xw[base + r];
           slr[r] = r < cnt ? tails[base + r] : make_double2(0.0, 0.0);
         }
