@@ -41,6 +41,10 @@ constexpr int kBatchMomUnroll = UCP_BATCH_MOM_UNROLL;
 #define UCP_BATCH_MOM_MINB 3
 #endif
 constexpr int kBatchMomQT = UCP_BATCH_MOM_QT;  // queries per CTA work item
+#ifndef UCP_BATCH_FUSED_MAX
+#define UCP_BATCH_FUSED_MAX 6000
+#endif
+constexpr int64_t kBatchFusedMaxQueries = UCP_BATCH_FUSED_MAX;  // slots x queries for the fused moments
 constexpr int kBatchMomMinB = UCP_BATCH_MOM_MINB;
 struct IdList {
   int32_t v[kMaxBatchIds];
@@ -169,6 +173,15 @@ int batch_moments(ucp_wc_batch* b, ucp_wc_batch::Lane& L, int S, cudaStream_t st
                                                             D.a1 + D.h1 * (double)(D.d1 - 1), L.x1, L.xw, L.tails,
                                                             L.tile_mm, B);
   UCP_LAUNCHED("k_x1_prepare");
+  if ((int64_t)S * D.d1 <= kBatchFusedMaxQueries) {
+    // few slots (the tail of a sweep): the latency-oriented fused kernel
+    smem_opt_in(reinterpret_cast<const void*>(k_mom_fused), kFSmem);
+    k_mom_fused<<<dim3(nblocks(D.d1, kFQ), S), kFThreads, kFSmem, st>>>(D.y1, D.d1, L.x1, D.fw0, L.tails, L.tile_mm, m,
+                                                                      D.a1, D.h1, D.d1, L.mom, L.mom + D.d1,
+                                                                      L.mom + 2 * D.d1, L.ids, D.ld0, 3 * D.d1);
+    UCP_LAUNCHED("k_mom_fused");
+    return UCP_OK;
+  }
   UCP_CHECK(cudaMemsetAsync(L.counter, 0, sizeof(int), st));
   int dev = 0, sms = 0, per_sm = 0;
   UCP_CHECK(cudaGetDevice(&dev));

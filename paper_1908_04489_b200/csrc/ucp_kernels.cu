@@ -948,8 +948,19 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
 __global__ void __launch_bounds__(kFThreads, kFQ <= 8 ? 2 : 1)
 k_mom_fused(const double* __restrict__ yq, int64_t n, const double* __restrict__ x, const double* __restrict__ w,
             const double2* __restrict__ tails, const double2* __restrict__ tile_mm, int64_t m, double a, double h,
-            int64_t d, double* o0, double* o1, double* o2) {
+            int64_t d, double* o0, double* o1, double* o2, const int32_t* __restrict__ ids, int64_t su0,
+            int64_t sout) {
   extern __shared__ __align__(16) double fbuf[];  // [2][3][kTile][kFQ]
+  if (ids) {  // batched engine: slot blockIdx.y runs instance ids[slot]
+    const int64_t slot = blockIdx.y, nt = (m + kTile - 1) / kTile;
+    x += slot * m;
+    tails += slot * m;
+    tile_mm += slot * nt;
+    w += (int64_t)ids[slot] * su0;
+    o0 += slot * sout;
+    o1 += slot * sout;
+    o2 += slot * sout;
+  }
   __shared__ __align__(16) uint64_t stab[256];
   __shared__ double sx[kTile], sw[kTile];
   __shared__ double2 stl[kTile];
@@ -1265,7 +1276,8 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   if (nq <= kFusedMaxQueries) {
     smem_opt_in(reinterpret_cast<const void*>(k_mom_fused), kFSmem);
     k_mom_fused<<<nblocks(nq, kFQ), kFThreads, kFSmem, st>>>(yq, nq, (const double*)px1, w, (const double2*)ptails,
-                                                            (const double2*)ptile, m, a, h, d, o0, o1, o2);
+                                                            (const double2*)ptile, m, a, h, d, o0, o1, o2,
+                                                            nullptr, 0, 0);
     UCP_LAUNCHED("k_mom_fused");
     return UCP_OK;
   }

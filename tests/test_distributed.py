@@ -251,3 +251,33 @@ def test_solve_many_replicas_world2():
             ref = P.solve(p, P.SolverConfig(max_rounds=3))
             assert J == ref.final_objective
             assert np.array_equal(u0.view(np.uint64), np.asarray(ref.controllers.values(0)).view(np.uint64))
+
+
+# ---------------------------- config 5 sharded over two ranks (grid points)
+def _gpu_c5_worker(rank, world, port, q):
+    _init(rank, world, port)
+    import paper_1908_04489_b200 as P
+
+    torch.cuda.set_device(0)
+    out = {}
+    for name, prob in (("inv3", P.Inventory(stages=3, grids=[(-3.0, 3.0, 121)] * 3)),
+                       ("zd", P.ZeroDelay(grids=[(-5.0, 5.0, 201), (-6.0, 6.0, 241)]))):
+        res = P.solve(prob, P.SolverConfig(max_rounds=3), sharding=P.from_process_group())
+        out[name] = (res.final_objective, [np.asarray(res.controllers.values(m)) for m in range(prob.M)])
+    dist.destroy_process_group()
+    q.put((rank, out))
+
+
+@pytest.mark.gpu
+def test_config5_sharded_solve_bitwise_world2():
+    import paper_1908_04489_b200 as P
+
+    out = _spawn(_gpu_c5_worker, 2)
+    refs = {"inv3": P.solve(P.Inventory(stages=3, grids=[(-3.0, 3.0, 121)] * 3), P.SolverConfig(max_rounds=3)),
+            "zd": P.solve(P.ZeroDelay(grids=[(-5.0, 5.0, 201), (-6.0, 6.0, 241)]), P.SolverConfig(max_rounds=3))}
+    for r in (0, 1):
+        for name, (J, us) in out[r].items():
+            ref = refs[name]
+            assert J == ref.final_objective, (name, r)
+            for m, u in enumerate(us):
+                assert np.array_equal(u.view(np.uint64), np.asarray(ref.controllers.values(m)).view(np.uint64))
