@@ -334,3 +334,26 @@ def test_concurrent_graph_capture_with_workspace_churn():
         assert r.final_objective == ref.final_objective
         for m in range(2):
             assert np.array_equal(np.asarray(r.controllers.values(m)), np.asarray(ref.controllers.values(m)))
+
+
+@pytest.mark.parametrize("nq,m,special", [(100, 1, None), (64, 2, None), (300, 300, "nan"), (300, 513, "dup"),
+                                          (20_000, 300, "nan")])
+def test_moments_edge_inputs_vs_oracle(P, oracle_mod, nq, m, special):
+    """Tiny support sets, a NaN support point (its tile is never skipped and
+    NaN reaches every query that sees the tails or the pdf), duplicated
+    support points -- fused and persistent kernels, bitwise vs the oracle."""
+    rng = np.random.default_rng(m + nq)
+    a, b = -10.0, 10.0
+    d = 401
+    h = (b - a) / (d - 1)
+    x = rng.uniform(-30, 30, m)
+    if special == "nan":
+        x[m // 3] = np.nan
+    if special == "dup":
+        x[1::2] = x[0::2][: x[1::2].size]
+    w = np.abs(rng.normal(0, 1, m)) * h
+    y = np.concatenate([[a, b], rng.uniform(a - 3, b + 3, nq - 2)])
+    got = P.kernels.gauss_moments_points(y, x, w, a, h, d)
+    want = oracle_mod.gauss_moments_points(y, x, w, a, h, d)
+    for k in range(3):
+        assert_bitwise(got[k], want[k], f"M{k}")
