@@ -89,6 +89,33 @@ void smem_opt_in(const void* fn, size_t bytes) {
 }
 inline unsigned nblocks(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
+// Programmatic dependent launch: kernels of a block iteration are launched
+// with programmatic stream serialisation, wait for their predecessor with
+// griddepcontrol.wait before touching its outputs, and let their successor
+// launch early (griddepcontrol.launch_dependents) -- the launch gap between
+// dependent kernels overlaps the predecessor's tail.  Both instructions are
+// no-ops for kernels launched without the attribute.  UCP_PDL=0 disables it.
+const bool g_pdl = [] {
+  const char* e = getenv("UCP_PDL");
+  return !(e && e[0] == '0');
+}();
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // --------------------------------------------------------------------------
 // Stage-0 inner moments: the windowed Gaussian walk of kernels.py:406-445.
 // --------------------------------------------------------------------------
@@ -278,6 +305,8 @@ __device__ __forceinline__ void flag_min(int64_t* slot, int64_t i) {
 template <int kMode>
 __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_gauss_grid(const double* __restrict__ s, int64_t n, const double* __restrict__ v,
                              WalkGrid g, double* t0, double* t1, double* t2) {
+  pdl_wait();
+  pdl_trigger();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   UCP_WALK_STAGE(v, g.d);
   if (t >= n) return;
@@ -294,6 +323,8 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_st
                                    int64_t nseg, const double* __restrict__ y_seg,
                                    const double* __restrict__ f0_seg, double k,
                                    const double* __restrict__ v1, WalkGrid g, double* out) {
+  pdl_wait();
+  pdl_trigger();
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t n = offsets[nseg];
   UCP_WALK_STAGE(v1, g.d);
@@ -313,6 +344,8 @@ template <int kMode, bool kBatch = false>
 __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_lu0_probe(const double* __restrict__ y0, const double* __restrict__ f0,
                             const double* __restrict__ u0, double k, const double* __restrict__ v1,
                             WalkGrid g, double fd_step, int64_t begin, int64_t n, double* cost3, const BatchArgs B) {
+  pdl_wait();
+  pdl_trigger();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (kBatch) {
     const int b = B.inst(blockIdx.y);
@@ -352,6 +385,8 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_lu
                              const double* __restrict__ u0, double k, const double* __restrict__ v1,
                              WalkGrid g, ucp_local_params lp, int64_t begin, int64_t n,
                              const double* __restrict__ cost3, double* out, int64_t* err, const BatchArgs B) {
+  pdl_wait();
+  pdl_trigger();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (kBatch) {
     const int b = B.inst(blockIdx.y);
@@ -390,6 +425,8 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ob
                             const double* __restrict__ u0, double k, const double* __restrict__ v1,
                             WalkGrid g, int64_t begin, int64_t end, double* terms, int64_t* err,
                             const BatchArgs B) {
+  pdl_wait();
+  pdl_trigger();
   int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (kBatch) {
     const int b = B.inst(blockIdx.y);
@@ -484,6 +521,8 @@ __global__ void k_segmented_argmin(const double* __restrict__ costs, const int64
 // flatten_windows dedups, kernels.py:163-187).
 __global__ void k_ex_count(const double* __restrict__ u, const int64_t* __restrict__ lo,
                            const int64_t* __restrict__ hi, int64_t begin, int64_t n, int64_t* counts) {
+  pdl_wait();
+  pdl_trigger();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   int64_t i = begin + t;
@@ -527,6 +566,8 @@ __global__ void k_ex_fill(const double* __restrict__ u, const int64_t* __restric
 __global__ void k_ex_fill_warp(const double* __restrict__ u, const int64_t* __restrict__ lo,
                                const int64_t* __restrict__ hi, int64_t begin, int64_t n,
                                const int64_t* __restrict__ offs, int32_t* cand_pt, int32_t* cand_j) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= n) return;  // warp-uniform
@@ -553,6 +594,8 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ex
                            WalkGrid g, const int64_t* __restrict__ total,
                            const int32_t* __restrict__ cand_pt, const int32_t* __restrict__ cand_j,
                            double* costs, const BatchArgs B) {
+  pdl_wait();
+  pdl_trigger();
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (kBatch) {  // per-slot candidate lists of capacity sslot; totals[slot]
     const int b = B.inst(blockIdx.y);
@@ -578,6 +621,8 @@ __global__ void k_ex_argmin(const double* __restrict__ u, const double* __restri
                             const int64_t* __restrict__ offs, const int32_t* __restrict__ cand_j,
                             int64_t begin, int64_t n, double* out, int64_t* err, const BatchArgs B,
                             int64_t soffs) {
+  pdl_wait();
+  pdl_trigger();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   if (B.ids) {
@@ -617,6 +662,8 @@ __global__ void k_x1_prepare(const double* __restrict__ y0, const double* __rest
                              const double* __restrict__ w, int64_t d0, double a, double h, double b, double* x1,
                              double2* xw, double2* tails, double2* tile_mm, const BatchArgs B) {
   __shared__ double smin[kTile], smax[kTile];
+  pdl_wait();
+  pdl_trigger();
   if (B.ids) {
     const int inst = B.inst(blockIdx.y);
     const int64_t ntiles = (d0 + kTile - 1) / kTile;
@@ -951,6 +998,8 @@ k_mom_fused(const double* __restrict__ yq, int64_t n, const double* __restrict__
             int64_t d, double* o0, double* o1, double* o2, const int32_t* __restrict__ ids, int64_t su0,
             int64_t sout) {
   extern __shared__ __align__(16) double fbuf[];  // [2][3][kTile][kFQ]
+  pdl_wait();
+  pdl_trigger();
   if (ids) {  // batched engine: slot blockIdx.y runs instance ids[slot]
     const int64_t slot = blockIdx.y, nt = (m + kTile - 1) / kTile;
     x += slot * m;
@@ -1104,6 +1153,8 @@ __global__ void k_stage1_segmented(const double* __restrict__ u_flat, const int6
 __global__ void k_lu1(const double* __restrict__ u1, const double* __restrict__ m0,
                       const double* __restrict__ m1, const double* __restrict__ m2,
                       ucp_local_params lp, int64_t begin, int64_t n, double* out, int64_t* err, const BatchArgs BA) {
+  pdl_wait();
+  pdl_trigger();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   if (BA.ids) {  // moments per slot (stride sslot), output per slot (stride n)
@@ -1141,6 +1192,8 @@ __global__ void k_ex1(const double* __restrict__ u1, const double* __restrict__ 
                       const double* __restrict__ m1, const double* __restrict__ m2,
                       const int64_t* __restrict__ lo, const int64_t* __restrict__ hi, int64_t begin,
                       int64_t n, double* out, int64_t* err, const BatchArgs BA) {
+  pdl_wait();
+  pdl_trigger();
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   if (BA.ids) {
@@ -1169,6 +1222,13 @@ __global__ void k_ex1(const double* __restrict__ u1, const double* __restrict__ 
   }
   if (!ok) flag_min(err, i);
   out[i] = bu;
+}
+
+__global__ void k_copy(const double* __restrict__ src, double* __restrict__ dst, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[i];
 }
 
 __global__ void k_device_libm(int which, const double* __restrict__ x, int64_t n, double* out) {
@@ -1270,14 +1330,14 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   if ((rc = ws_get(ws, WS_TILE, sizeof(double2) * (size_t)ntiles, &ptile))) return rc;
   if ((rc = ws_get(ws, WS_TOTAL, sizeof(int64_t) * 2, &pctr))) return rc;
   const double b = a + h * (double)(d - 1);
-  k_x1_prepare<<<(unsigned)ntiles, kTile, 0, st>>>(y0, u0, w, m, a, h, b, (double*)px1, (double2*)pxw,
-                                                   (double2*)ptails, (double2*)ptile, kNoBatch);
+  UCP_CHECK(launch_pdl(k_x1_prepare, dim3((unsigned)ntiles), dim3(kTile), 0, st, y0, u0, w, m, a, h, b, (double*)px1,
+                       (double2*)pxw, (double2*)ptails, (double2*)ptile, kNoBatch));
   UCP_LAUNCHED("k_x1_prepare");
   if (nq <= kFusedMaxQueries) {
     smem_opt_in(reinterpret_cast<const void*>(k_mom_fused), kFSmem);
-    k_mom_fused<<<nblocks(nq, kFQ), kFThreads, kFSmem, st>>>(yq, nq, (const double*)px1, w, (const double2*)ptails,
-                                                            (const double2*)ptile, m, a, h, d, o0, o1, o2,
-                                                            nullptr, 0, 0);
+    UCP_CHECK(launch_pdl(k_mom_fused, dim3(nblocks(nq, kFQ)), dim3(kFThreads), kFSmem, st, yq, nq, (const double*)px1,
+                         w, (const double2*)ptails, (const double2*)ptile, m, a, h, d, o0, o1, o2,
+                         (const int32_t*)nullptr, (int64_t)0, (int64_t)0));
     UCP_LAUNCHED("k_mom_fused");
     return UCP_OK;
   }
@@ -1322,6 +1382,21 @@ void allow_smem(K* kernel) {  // opt in to >48 KiB dynamic shared memory (walk k
     } else if ((d_v1) <= kSmemWalkMax) {                                                          \
       allow_smem(kernel<2>);                                                                      \
       kernel<2><<<(grid), kWalkThreads, (size_t)(d_v1) * sizeof(double), (stream)>>>(__VA_ARGS__); \
+    } else {                                                                                      \
+      kernel<1><<<(grid), kWalkThreads, 0, (stream)>>>(__VA_ARGS__);                              \
+    }                                                                                             \
+  } while (0)
+
+// Same, with programmatic dependent launch in the latency regime (the
+// local-update chain, where it measurably shortens the iteration).
+#define UCP_WALK_LAUNCH_PDL(kernel, n_walks, grid, stream, d_v1, ...)                               \
+  do {                                                                                            \
+    if (!walk_latency_mode(n_walks)) {                                                            \
+      kernel<0><<<(grid), kWalkThreads, 0, (stream)>>>(__VA_ARGS__);                              \
+    } else if ((d_v1) <= kSmemWalkMax) {                                                          \
+      allow_smem(kernel<2>);                                                                      \
+      UCP_CHECK(launch_pdl(kernel<2>, dim3(grid), dim3(kWalkThreads), (size_t)(d_v1) * sizeof(double), \
+                           (stream), __VA_ARGS__));                                               \
     } else {                                                                                      \
       kernel<1><<<(grid), kWalkThreads, 0, (stream)>>>(__VA_ARGS__);                              \
     }                                                                                             \
@@ -1500,10 +1575,10 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
     if ((rc = ws_get(ws, WS_COST, sizeof(double) * 3 * (size_t)n, &pc))) return rc;
     if (int rc_ = check_aligned(u1)) return rc_;
     WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
-    UCP_WALK_LAUNCH(k_lu0_probe, 3 * n, nblocks(3 * n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
+    UCP_WALK_LAUNCH_PDL(k_lu0_probe, 3 * n, nblocks(3 * n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
                                                      (double*)pc, kNoBatch);
     UCP_LAUNCHED("k_lu0_probe");
-    UCP_WALK_LAUNCH(k_lu0_finish, n, nblocks(n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, *lp, begin, n,
+    UCP_WALK_LAUNCH_PDL(k_lu0_finish, n, nblocks(n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, *lp, begin, n,
                                                   (const double*)pc, out, err, kNoBatch);
     UCP_LAUNCHED("k_lu0_finish");
     return UCP_OK;
@@ -1514,7 +1589,8 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
   if ((rc = run_moments(P->y1 + begin, n, P->y0, u0, P->fw0, P->d0, P->a1, P->h1, P->d1, m0, m0 + n,
                         m0 + 2 * n, ws, st)))
     return rc;
-  k_lu1<<<nblocks(n, 256), 256, 0, st>>>(u1, m0, m0 + n, m0 + 2 * n, *lp, begin, n, out, err, kNoBatch);
+  UCP_CHECK(launch_pdl(k_lu1, dim3(nblocks(n, 256)), dim3(256), 0, st, (const double*)u1, (const double*)m0,
+                       (const double*)(m0 + n), (const double*)(m0 + 2 * n), *lp, begin, n, out, err, kNoBatch));
   UCP_LAUNCHED("k_lu1");
   return UCP_OK;
 }
@@ -1644,7 +1720,7 @@ static int block_iteration(const ucp_wc_problem* P, int kind, double* u0, double
       rc = ucp_wc_exhaustion(P, m, u0, u1, lo[m], hi[m], m == 0 ? cand_bound0 : 0, 0, d[m], scratch[m], err6 + 3 * m,
                              ws, st);
     if (rc) return rc;
-    UCP_CHECK(cudaMemcpyAsync(u[m], scratch[m], sizeof(double) * (size_t)d[m], cudaMemcpyDeviceToDevice, st));
+    UCP_CHECK(launch_pdl(k_copy, dim3(nblocks(d[m], 256)), dim3(256), 0, st, (const double*)scratch[m], u[m], d[m]));
   }
   return UCP_OK;
 }
