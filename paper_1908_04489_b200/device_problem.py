@@ -74,6 +74,10 @@ class ErrorLog:
             kind, m = entry[0], entry[1]
             if not (row != NO_ERROR).any():
                 continue
+            if kind == "objective":
+                # a deferred objective (payload: its controller set); its row
+                # sits between the phases queued before and after it
+                raise _objective_error(self.problem, entry[2], int(row[0]))
             if kind == "block":
                 # a graph-replayed block only records the minimum over its
                 # iterations: re-run it eagerly from its input snapshot so the
@@ -82,6 +86,13 @@ class ErrorLog:
                 raise AssertionError("block failure did not reproduce")
             raise _phase_error(self.problem, kind, m, row)
         return extra_host
+
+
+def _objective_error(problem, U, bad):
+    g = problem.grids[0]
+    return NumericError(
+        f"{problem.name}: non-finite objective integrand at stage 0, grid point {bad} "
+        f"(y={g.points[bad]!r}, u={U.values(0)[bad]!r})")
 
 
 def _phase_error(problem, kind, m, row):

@@ -249,8 +249,10 @@ class Witsenhausen(Problem):
         self.device_run_block(kind, iters, U, cfg, graphs=False)
         self.device_context().errors.flush(sharding)
 
-    def device_objective(self, U: ControllerSet, sharding: Sharding = LOCAL) -> float:
-        """problem.py:110-127: stage-0 integrand on device, then the serial trapezoid."""
+    def _queue_objective(self, U: ControllerSet, sharding: Sharding, err: torch.Tensor) -> torch.Tensor:
+        """Queue the objective of U (problem.py:110-127: stage-0 integrand, then
+        the serial trapezoid); returns a device int64[1] holding J's bits, the
+        first non-finite integrand point goes to ``err`` (atomicMin)."""
         self.check_controllers(U)
         D = self.device_context()
         g = self.grids[0]
@@ -258,21 +260,43 @@ class Witsenhausen(Problem):
         bounds = self._plan(0, U, sharding)
         begin, end = sharding.shard(bounds)
         buf = sharding.padded_buffer(bounds, D.device)
-        res = torch.full((2,), NO_ERROR, dtype=I64, device=D.device)  # [J bits, first bad point]
+        jbits = torch.empty(1, dtype=I64, device=D.device)
         _lib.call("ucp_wc_objective_terms", ctypes.byref(D.P), ptr(u0), ptr(u1), begin, end,
-                  sharding.rank_ptr(buf, bounds), res[1:].data_ptr(), D.stream)
+                  sharding.rank_ptr(buf, bounds), err.data_ptr(), D.stream)
         terms = sharding.gather(buf, bounds, g.d)
-        sharding.allreduce_min_(res[1:])
-        _lib.call("ucp_trapezoid_sum", ptr(terms), g.d, g.spacing, res[:1].data_ptr(), None, D.stream)
-        # one synchronisation: the pending phase-error rows and J travel together;
-        # earlier phases' failures are raised first, in order
-        host = D.errors.flush(sharding, extra=res)
-        bad = int(host[1])
+        sharding.allreduce_min_(err)
+        _lib.call("ucp_trapezoid_sum", ptr(terms), g.d, g.spacing, jbits.data_ptr(), None, D.stream)
+        return jbits
+
+    def device_objective(self, U: ControllerSet, sharding: Sharding = LOCAL, deferred=()) -> float:
+        """problem.py:110-127 on the device.  ``deferred`` objectives (from
+        device_objective_deferred) are read in the same synchronisation."""
+        D = self.device_context()
+        res = torch.full((1,), NO_ERROR, dtype=I64, device=D.device)
+        jbits = self._queue_objective(U, sharding, res)
+        # one synchronisation: the pending phase-error rows (deferred objectives
+        # among them, in queue order) and every J travel together
+        extra = torch.cat([res, jbits] + [p[0] for p in deferred])
+        host = D.errors.flush(sharding, extra=extra)
+        bad = int(host[0])
         if bad != NO_ERROR:
+            g = self.grids[0]
             raise NumericError(
                 f"{self.name}: non-finite objective integrand at stage 0, grid point {bad} "
                 f"(y={g.points[bad]!r}, u={U.values(0)[bad]!r})")
-        return float(host[:1].view(np.float64)[0])
+        vals = host[1:].view(np.float64)
+        for p, v in zip(deferred, vals[1:]):
+            p[1].append(float(v))
+        return float(vals[0])
+
+    def device_objective_deferred(self, U: ControllerSet, sharding: Sharding = LOCAL):
+        """Queue the objective of U without synchronising; its failure is
+        raised in queue order by the next synchronisation, and its value is
+        read by the next device_objective(..., deferred=[handle])."""
+        D = self.device_context()
+        row = D.errors.slots([("objective", 0, U)], sharding)[0]
+        jbits = self._queue_objective(U, sharding, row[:1])
+        return (jbits, [])
 
     def flush_errors(self, sharding: Sharding = LOCAL) -> None:
         if self._dev is not None:

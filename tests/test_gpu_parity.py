@@ -357,3 +357,26 @@ def test_moments_edge_inputs_vs_oracle(P, oracle_mod, nq, m, special):
     want = oracle_mod.gauss_moments_points(y, x, w, a, h, d)
     for k in range(3):
         assert_bitwise(got[k], want[k], f"M{k}")
+
+
+def test_deferred_objective_value_and_error_order(P):
+    """The post-local objective is queued without a synchronisation: its value
+    is bitwise the synchronous one, and a failure is raised (with the
+    reference's message) before anything queued after it."""
+    prob = P.Witsenhausen(grids=[(-25.0, 25.0, 201)] * 2)
+    g0, g1 = prob.grids
+    rng = np.random.default_rng(5)
+    U = P.ControllerSet((P.SampledController(g0, g0.points + rng.uniform(-1, 1, g0.d)),
+                         P.SampledController(g1, g1.points)))
+    V = prob.identity_controllers()
+    want = prob.device_objective(U)
+    h = prob.device_objective_deferred(U)
+    other = prob.device_objective(V, deferred=[h])
+    assert h[1] == [want] and other == prob.device_objective(V)
+    bad = P.ControllerSet((P.SampledController(g0, np.full(g0.d, 1e200)), P.SampledController(g1, g1.points)))
+    with pytest.raises(P.NumericError) as sync_err:
+        prob.device_objective(bad)
+    h = prob.device_objective_deferred(bad)
+    with pytest.raises(P.NumericError) as got:
+        prob.device_objective(V, deferred=[h])
+    assert str(got.value) == str(sync_err.value)
