@@ -4,6 +4,8 @@ synchronisation point with the reference's exception) and a generic device
 context used by the config-5 problems."""
 from __future__ import annotations
 
+import weakref
+
 import ctypes
 
 import numpy as np
@@ -31,9 +33,17 @@ class ErrorLog:
 
     def __init__(self, device, problem, capacity: int = 1024):
         self.device = device
-        self.problem = problem
+        # weak: problem -> context -> log -> problem would be a cycle, and a
+        # cycle is only freed by the cyclic GC -- at an arbitrary moment, e.g.
+        # inside another solve, where the context's teardown synchronises
+        # the device
+        self._problem = weakref.ref(problem) if problem is not None else (lambda: None)
         self.rows = torch.full((capacity, 3), NO_ERROR, dtype=I64, device=device)
         self.meta: list[tuple] = []
+
+    @property
+    def problem(self):
+        return self._problem()
 
     def slot(self, kind: str, stage: int, sharding: Sharding) -> torch.Tensor:
         if len(self.meta) == self.rows.shape[0]:

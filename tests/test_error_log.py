@@ -16,10 +16,14 @@ class _Prob:
         self.grids = [P.make_grid(-25.0, 25.0, 11), P.make_grid(-25.0, 25.0, 11)]
 
 
+_PROBLEMS = []  # the log holds its problem weakly
+
+
 def _log():
     from paper_1908_04489_b200.device_problem import ErrorLog
 
-    return ErrorLog(torch.device("cpu"), _Prob(), capacity=8)
+    _PROBLEMS.append(_Prob())
+    return ErrorLog(torch.device("cpu"), _PROBLEMS[-1], capacity=8)
 
 
 def test_clean_rows_return_extra():
