@@ -127,26 +127,45 @@ class _DeviceSweeps:
     def device_exhaustion(self, m, U, cfg, sharding: Sharding = LOCAL):
         return self._sweep("exhaustion", m, U, cfg, sharding)
 
-    def device_objective(self, U: ControllerSet, sharding: Sharding = LOCAL) -> float:
-        """problem.py:110-127: stage-0 integrand on device + serial trapezoid."""
+    def _queue_objective(self, U: ControllerSet, sharding: Sharding, err: torch.Tensor) -> torch.Tensor:
+        """Queue the objective (problem.py:110-127: stage-0 integrand + serial
+        trapezoid); returns device int64[1] with J's bits, first bad point -> err."""
         self.check_controllers(U)
         D = self.device_context()
         g = self.grids[0]
         ts = self._uptrs(U)
         begin, end = sharding.bounds(g.d)
         terms = sharding.out_buffer(g.d, D.device)
-        res = torch.full((2,), NO_ERROR, dtype=I64, device=D.device)
-        self._abi_terms(ts, begin, end, terms, res[1:])
+        jbits = torch.empty(1, dtype=I64, device=D.device)
+        self._abi_terms(ts, begin, end, terms, err)
         sharding.allgather_(terms)
-        sharding.allreduce_min_(res[1:])
-        _lib.call("ucp_trapezoid_sum", ptr(terms), g.d, g.spacing, res[:1].data_ptr(), None, D.stream)
-        host = D.errors.flush(sharding, extra=res)  # earlier phases' failures first, one sync
-        bad = int(host[1])
+        sharding.allreduce_min_(err)
+        _lib.call("ucp_trapezoid_sum", ptr(terms), g.d, g.spacing, jbits.data_ptr(), None, D.stream)
+        return jbits
+
+    def device_objective(self, U: ControllerSet, sharding: Sharding = LOCAL, deferred=()) -> float:
+        """problem.py:110-127 on the device; ``deferred`` objectives (from
+        device_objective_deferred) are read in the same synchronisation."""
+        D = self.device_context()
+        res = torch.full((1,), NO_ERROR, dtype=I64, device=D.device)
+        jbits = self._queue_objective(U, sharding, res)
+        host = D.errors.flush(sharding, extra=torch.cat([res, jbits] + [p[0] for p in deferred]))
+        bad = int(host[0])
         if bad != NO_ERROR:
+            g = self.grids[0]
             raise NumericError(
                 f"{self.name}: non-finite objective integrand at stage 0, grid point {bad} "
                 f"(y={g.points[bad]!r}, u={U.values(0)[bad]!r})")
-        return float(host[:1].view(np.float64)[0])
+        vals = host[1:].view(np.float64)
+        for p, v in zip(deferred, vals[1:]):
+            p[1].append(float(v))
+        return float(vals[0])
+
+    def device_objective_deferred(self, U: ControllerSet, sharding: Sharding = LOCAL):
+        """Queue the objective without synchronising (see Witsenhausen)."""
+        D = self.device_context()
+        row = D.errors.slots([("objective", 0, U)], sharding)[0]
+        return (self._queue_objective(U, sharding, row[:1]), [])
 
     def objective(self, U) -> float:
         return self.device_objective(U)
