@@ -316,6 +316,20 @@ int ucp_wc_batch_iterate(ucp_wc_batch* b, int lane, int kind, const int32_t* ids
 int ucp_wc_batch_objective(ucp_wc_batch* b, int lane, const int32_t* ids, int32_t nslots, double* J,
                            int64_t* err_obj, void* stream);
 
+/* ---- NCCL plumbing for non-Python hosts ----------------------
+ * One communicator per rank (one process per GPU, the current device).  Rank
+ * 0 creates the id and the host ships it to the other ranks out of band.
+ * A phase's controller shard is exchanged with ucp_allgather_f64 (in place
+ * when send == recv + rank * count), error slots with ucp_allreduce_min_i64.
+ * The Python host does the same through torch.distributed (distributed.py). */
+#define UCP_COMM_ID_BYTES 128
+typedef struct ucp_comm ucp_comm;
+int ucp_comm_unique_id(unsigned char* id /* [UCP_COMM_ID_BYTES] */);
+int ucp_comm_init(int nranks, int rank, const unsigned char* id, ucp_comm** comm);
+int ucp_comm_destroy(ucp_comm* comm);
+int ucp_allgather_f64(ucp_comm* comm, const double* send, double* recv, int64_t count, void* stream);
+int ucp_allreduce_min_i64(ucp_comm* comm, int64_t* buf, int64_t count, void* stream);
+
 /* ---- instrumentation ------------------------------------------------------
  * FP64 pipe throughput probe (no FMA: DMUL/DADD only, 8 independent chains
  * per thread).  Performs iters*16 DP ops per thread; sink must hold

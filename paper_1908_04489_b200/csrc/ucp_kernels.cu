@@ -1822,3 +1822,4 @@ int ucp_fp64_probe(int blocks, int threads, int iters, double* sink, void* strea
 #include "ucp_config5.cuh"
 #include "ucp_mc.cuh"
 #include "ucp_batch.cuh"
+#include "ucp_comm.cuh"

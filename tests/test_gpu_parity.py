@@ -380,3 +380,20 @@ def test_deferred_objective_value_and_error_order(P):
     with pytest.raises(P.NumericError) as got:
         prob.device_objective(V, deferred=[h])
     assert str(got.value) == str(sync_err.value)
+
+
+def test_nccl_comm_single_rank(P):
+    """The C-ABI NCCL plumbing (ucp_comm_*) on one rank: in-place all-gather
+    and MIN all-reduce leave the data as is (multi-rank exchanges go through
+    torch.distributed in the Python host and need one GPU per rank)."""
+    uid = P.NcclComm.unique_id()
+    comm = P.NcclComm(1, 0, uid)
+    x = torch.arange(10, dtype=torch.float64, device="cuda")
+    comm.allgather_(x)
+    e = torch.tensor([5, 3, 9], dtype=torch.int64, device="cuda")
+    comm.allreduce_min_(e)
+    torch.cuda.synchronize()
+    assert x.cpu().tolist() == list(map(float, range(10))) and e.cpu().tolist() == [5, 3, 9]
+    comm.close()
+    with pytest.raises(ValueError):
+        P.NcclComm(2, 5, uid)
