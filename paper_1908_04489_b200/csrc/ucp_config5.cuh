@@ -271,7 +271,10 @@ __global__ void k_gen_exh_eval(Cost cost, const double* __restrict__ u, const in
   const int64_t k = t / n, p = t - k * n;
   const int64_t i = begin + p;
   const int64_t j = lo[i] + k;
-  if (j <= hi[i]) costs[p * wmax + k] = cost(u[j], i);
+  // a value equal to its window predecessor has the same cost and never wins
+  // the first-minimum: not evaluated (the reference's flatten_windows dedups
+  // the same adjacent repeats, kernels.py:163-187)
+  if (j <= hi[i] && !(k > 0 && u[j] == u[j - 1])) costs[p * wmax + k] = cost(u[j], i);
 }
 
 __global__ void k_gen_exh_pick(const double* __restrict__ u, const int64_t* __restrict__ lo,
@@ -281,11 +284,13 @@ __global__ void k_gen_exh_pick(const double* __restrict__ u, const int64_t* __re
   if (t >= n) return;
   const int64_t i = begin + t;
   const double* c = costs + t * wmax;
-  const int64_t w = hi[i] - lo[i] + 1;
+  const int64_t j0 = lo[i];
+  const int64_t w = hi[i] - j0 + 1;
   int64_t best = 0;
   double bv = c[0];
   bool ok = finite(bv);
   for (int64_t k = 1; k < w; ++k) {
+    if (u[j0 + k] == u[j0 + k - 1]) continue;  // adjacent repeat: same cost, not evaluated
     const double x = c[k];
     ok = ok && finite(x);
     if (x < bv) {
