@@ -59,6 +59,64 @@ __device__ __forceinline__ Mom3U unif_moments_at(double x, const double* __restr
   return r;
 }
 
+// The same moments with the interior cells' terms read from tables: a cell
+// at least two cells inside the window [cell(x - rad), cell(x + rad)]
+// overlaps it completely (its bounds are the neighbours' shared edges,
+// computed from the same exact half-integers), so its overlap is rj - lj
+// whatever x is and its three terms ov, ov*v, (ov*v)*v are per-grid constants
+// for a given v (k_unif_cell_terms).  Same additions in the same order:
+// bitwise equal.
+__device__ __forceinline__ Mom3U unif_moments_at_tab(double x, const double* __restrict__ v, double a, double h,
+                                                     int64_t d, double rad, const double* __restrict__ c0,
+                                                     const double* __restrict__ c1, const double* __restrict__ c2) {
+  const double xlo = x - rad, xhi = x + rad;
+  const long long jlo = cell_index(xlo, a, h, d), jhi = cell_index(xhi, a, h, d);
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  auto edge = [&](long long j) {
+    const double lj = cell_left(j, a, h), rj = cell_right(j, a, h, d);
+    const double lo = xlo > lj ? xlo : lj;
+    const double hi = xhi < rj ? xhi : rj;
+    const double ov = hi - lo;
+    if (ov > 0.0) {
+      const double vj = __ldg(v + j);
+      acc0 += ov;
+      const double ovv = ov * vj;
+      acc1 += ovv;
+      acc2 += ovv * vj;
+    }
+  };
+  if (jlo <= jhi) {
+    // two cells at each end exactly (the cell next to an end cell may be
+    // clipped by the rounding of (x -/+ rad - a)/h), the rest from the tables
+    const long long e0 = jlo + 1 < jhi ? jlo + 1 : jhi;
+    for (long long j = jlo; j <= e0; ++j) edge(j);
+    for (long long j = jlo + 2; j <= jhi - 2; ++j) {
+      acc0 += __ldg(c0 + j);
+      acc1 += __ldg(c1 + j);
+      acc2 += __ldg(c2 + j);
+    }
+    for (long long j = (jhi - 1 > jlo + 2 ? jhi - 1 : jlo + 2); j <= jhi; ++j) edge(j);
+  }
+  const double inv = 1.0 / (2.0 * rad);
+  Mom3U r;
+  r.s0 = acc0 * inv;
+  r.s1 = acc1 * inv;
+  r.s2 = acc2 * inv;
+  return r;
+}
+
+// per-cell interior terms for unif_moments_at_tab (end cells are never interior)
+__global__ void k_unif_cell_terms(const double* __restrict__ v, double a, double h, int64_t d, double* c0, double* c1,
+                                  double* c2) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d) return;
+  const double ov = cell_right(j, a, h, d) - cell_left(j, a, h);
+  const double ovv = ov * v[j];
+  c0[j] = ov;
+  c1[j] = ovv;
+  c2[j] = ovv * v[j];
+}
+
 // kernels.py:532-555: E[g] under U(x - rad, x + rad)
 __device__ __forceinline__ double unif_ball_at(double x, const double* __restrict__ g, double a, double h, int64_t d,
                                                double rad) {
@@ -176,8 +234,10 @@ struct ZdCost0 {
   const double* v1;
   double a1, h1, pw;
   int64_t d1;
+  const double* tab = nullptr;  // [3][d1] interior-cell terms of v1 (nullptr: direct loop)
   __device__ __forceinline__ double operator()(double u, int64_t i) const {
-    const Mom3U s = unif_moments_at(u, v1, a1, h1, d1, 1.0);
+    const Mom3U s = tab ? unif_moments_at_tab(u, v1, a1, h1, d1, 1.0, tab, tab + d1, tab + 2 * d1)
+                        : unif_moments_at(u, v1, a1, h1, d1, 1.0);
     const double y = y0[i];
     const double distortion = (((s.s0 * y) * y) - ((2.0 * s.s1) * y)) + s.s2;
     return f0[i] * (((pw * u) * u) + distortion);
@@ -394,6 +454,20 @@ ZdCost0 zd_cost0(const ucp_zd_problem* P, const double* u1) {
   return c;
 }
 
+// the functor with its interior-cell tables, built once per call in the workspace
+int zd_cost0_tab(const ucp_zd_problem* P, const double* u1, ucp_workspace* ws, cudaStream_t st, ZdCost0* out) {
+  ZdCost0 c = zd_cost0(P, u1);
+  void* pt;
+  int rc;
+  if ((rc = ws_get(ws, WS_C5_TAB, sizeof(double) * 3 * (size_t)P->d1, &pt))) return rc;
+  double* t = (double*)pt;
+  k_unif_cell_terms<<<nblocks(P->d1, 256), 256, 0, st>>>(u1, P->a1, P->h1, P->d1, t, t + P->d1, t + 2 * P->d1);
+  UCP_LAUNCHED("k_unif_cell_terms");
+  c.tab = t;
+  *out = c;
+  return UCP_OK;
+}
+
 // zero_delay.py:77-83: decoder moments at queries y (centres u0, weights fw0, values y0)
 int zd_moments(const ucp_zd_problem* P, const double* u0, const double* yq, int64_t nq, ucp_workspace* ws,
                cudaStream_t st, QuadCost* q) {
@@ -554,7 +628,8 @@ int ucp_zd_cost(const ucp_zd_problem* P, int stage, const double* u0, const doub
   if (nseg <= 0 || n_cand <= 0) return UCP_OK;
   cudaStream_t st = as_stream(stream);
   if (stage == 0) {
-    ZdCost0 c = zd_cost0(P, u1);
+    ZdCost0 c;
+    if ((rc = zd_cost0_tab(P, u1, ws, st, &c))) return rc;
     c.y0 = y_seg;  // per-segment observation and density
     c.f0 = f0_seg;
     k_gen_segmented<ZdCost0><<<nblocks(n_cand, 128), 128, 0, st>>>(c, u_flat, offsets, nseg, out);
@@ -581,7 +656,11 @@ int ucp_zd_local_update(const ucp_zd_problem* P, int stage, const double* u0, co
   if (n == 0) return UCP_OK;
   cudaStream_t st = as_stream(stream);
   const double floor = P->h1;  // zero_delay.py:56-65: probe >= one decoder cell, both stages
-  if (stage == 0) return launch_gen_local(zd_cost0(P, u1), u0, lp, floor, 0, begin, n, out, err, ws, st);
+  if (stage == 0) {
+    ZdCost0 c;
+    if ((rc = zd_cost0_tab(P, u1, ws, st, &c))) return rc;
+    return launch_gen_local(c, u0, lp, floor, 0, begin, n, out, err, ws, st);
+  }
   QuadCost q;
   if ((rc = zd_moments(P, u0, P->y1 + begin, n, ws, st, &q))) return rc;
   q.begin = begin;
@@ -599,7 +678,11 @@ int ucp_zd_exhaustion(const ucp_zd_problem* P, int stage, const double* u0, cons
   const int64_t n = end - begin;
   if (n == 0) return UCP_OK;
   cudaStream_t st = as_stream(stream);
-  if (stage == 0) return launch_gen_exhaust(zd_cost0(P, u1), u0, win_lo, win_hi, wmax, 0, begin, n, out, err, ws, st);
+  if (stage == 0) {
+    ZdCost0 c;
+    if ((rc = zd_cost0_tab(P, u1, ws, st, &c))) return rc;
+    return launch_gen_exhaust(c, u0, win_lo, win_hi, wmax, 0, begin, n, out, err, ws, st);
+  }
   QuadCost q;
   if ((rc = zd_moments(P, u0, P->y1 + begin, n, ws, st, &q))) return rc;
   q.begin = begin;
