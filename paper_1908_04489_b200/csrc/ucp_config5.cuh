@@ -133,6 +133,36 @@ __device__ __forceinline__ double unif_ball_at(double x, const double* __restric
   return acc * (1.0 / (2.0 * rad));
 }
 
+// unif_ball_at with the interior cells' terms (rj - lj) * g_j from a table
+// (k_unif_ball_terms); two cells at each end computed exactly, as in
+// unif_moments_at_tab.  Same additions in the same order: bitwise equal.
+__device__ __forceinline__ double unif_ball_at_tab(double x, const double* __restrict__ g, double a, double h,
+                                                   int64_t d, double rad, const double* __restrict__ tg) {
+  const double xlo = x - rad, xhi = x + rad;
+  const long long jlo = cell_index(xlo, a, h, d), jhi = cell_index(xhi, a, h, d);
+  double acc = 0.0;
+  auto edge = [&](long long j) {
+    const double lj = cell_left(j, a, h), rj = cell_right(j, a, h, d);
+    const double lo = xlo > lj ? xlo : lj;
+    const double hi = xhi < rj ? xhi : rj;
+    const double ov = hi - lo;
+    if (ov > 0.0) acc += ov * __ldg(g + j);
+  };
+  if (jlo <= jhi) {
+    const long long e0 = jlo + 1 < jhi ? jlo + 1 : jhi;
+    for (long long j = jlo; j <= e0; ++j) edge(j);
+    for (long long j = jlo + 2; j <= jhi - 2; ++j) acc += __ldg(tg + j);
+    for (long long j = (jhi - 1 > jlo + 2 ? jhi - 1 : jlo + 2); j <= jhi; ++j) edge(j);
+  }
+  return acc * (1.0 / (2.0 * rad));
+}
+
+__global__ void k_unif_ball_terms(const double* __restrict__ g, double a, double h, int64_t d, double* tg) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d) return;
+  tg[j] = (cell_right(j, a, h, d) - cell_left(j, a, h)) * g[j];
+}
+
 __global__ void k_unif_moments_grid(const double* __restrict__ x, int64_t n, const double* __restrict__ v, double a,
                                     double h, int64_t d, double rad, double* s0, double* s1, double* s2) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -263,9 +293,11 @@ struct InvCost {
   const double* gnext;
   double am, hm, an, hn, oc;
   int64_t dm, dn;
+  const double* tg = nullptr;  // interior-cell terms of gnext (nullptr: direct loop)
   __device__ __forceinline__ double operator()(double u, int64_t i) const {
     const double y = ym[i];
-    const double expect = unif_ball_at(y + u, gnext, an, hn, dn, 1.0);
+    const double expect = tg ? unif_ball_at_tab(y + u, gnext, an, hn, dn, 1.0, tg)
+                             : unif_ball_at(y + u, gnext, an, hn, dn, 1.0);
     const double weight = fm[cell_index(y, am, hm, dm)];
     return weight * ((oc * u) + expect);
   }
@@ -392,7 +424,8 @@ __global__ void k_gen_segmented(Cost cost, const double* __restrict__ u_flat, co
 // gs[M] = gamma(terminal points) when gnext == nullptr.
 __global__ void k_inv_downstream(const double* __restrict__ pts, const double* __restrict__ u, int64_t n,
                                  const double* __restrict__ gnext, double an, double hn, int64_t dn, double oc,
-                                 int quadratic, double hr, double br, double* out) {
+                                 int quadratic, double hr, double br, double* out,
+                                 const double* __restrict__ tg = nullptr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double x = pts[i];
@@ -402,7 +435,8 @@ __global__ void k_inv_downstream(const double* __restrict__ pts, const double* _
     return;
   }
   const double ui = u[i];
-  const double expect = unif_ball_at(x + ui, gnext, an, hn, dn, 1.0);
+  const double expect =
+      tg ? unif_ball_at_tab(x + ui, gnext, an, hn, dn, 1.0, tg) : unif_ball_at(x + ui, gnext, an, hn, dn, 1.0);
   out[i] = gam + ((oc * ui) + expect);
 }
 
@@ -544,11 +578,16 @@ int inv_downstream(const ucp_inv_problem* P, int m, const double* const* u, ucp_
                                                              0.0, P->quadratic, P->holding_rate, P->backlog_rate,
                                                              bufs[cur]);
   UCP_LAUNCHED("k_inv_downstream");
+  void* ptg;
+  if ((rc = ws_get(ws, WS_C5_GT0, sizeof(double) * (size_t)dmax, &ptg))) return rc;
   for (int mm = M - 1; mm >= m + 1; --mm) {
     const int nx = inv_state(P, mm + 1);
+    k_unif_ball_terms<<<nblocks(P->d[nx], 256), 256, 0, st>>>(bufs[cur], P->a[nx], P->h[nx], P->d[nx], (double*)ptg);
+    UCP_LAUNCHED("k_unif_ball_terms");
     k_inv_downstream<<<nblocks(P->d[mm], 128), 128, 0, st>>>(P->pts[mm], u[mm], P->d[mm], bufs[cur], P->a[nx],
                                                              P->h[nx], P->d[nx], P->order_cost, P->quadratic,
-                                                             P->holding_rate, P->backlog_rate, bufs[cur ^ 1]);
+                                                             P->holding_rate, P->backlog_rate, bufs[cur ^ 1],
+                                                             (const double*)ptg);
     UCP_LAUNCHED("k_inv_downstream");
     cur ^= 1;
   }
@@ -573,6 +612,11 @@ int inv_cost(const ucp_inv_problem* P, int m, const double* const* u, ucp_worksp
   c->hn = P->h[nx];
   c->dn = P->d[nx];
   c->oc = P->order_cost;
+  void* ptg;
+  if ((rc = ws_get(ws, WS_C5_GT1, sizeof(double) * (size_t)P->d[nx], &ptg))) return rc;
+  k_unif_ball_terms<<<nblocks(P->d[nx], 256), 256, 0, st>>>(gn, P->a[nx], P->h[nx], P->d[nx], (double*)ptg);
+  UCP_LAUNCHED("k_unif_ball_terms");
+  c->tg = (const double*)ptg;
   return UCP_OK;
 }
 

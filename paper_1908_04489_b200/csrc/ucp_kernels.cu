@@ -1267,8 +1267,8 @@ struct ucp_graph_entry {
 std::shared_mutex g_capture_mu;
 
 struct ucp_workspace {
-  void* buf[16] = {nullptr};
-  size_t cap[16] = {0};
+  void* buf[24] = {nullptr};
+  size_t cap[24] = {0};
   void* scan_tmp = nullptr;
   size_t scan_cap = 0;
   int64_t* h_total = nullptr;           // pinned
@@ -1279,9 +1279,9 @@ struct ucp_workspace {
 namespace {
 enum {
   WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS,
-  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_C5_TAB, WS_NSLOTS
+  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_C5_TAB, WS_C5_GT0, WS_C5_GT1, WS_NSLOTS
 };
-static_assert(WS_NSLOTS <= 16, "workspace slots");
+static_assert(WS_NSLOTS <= 24, "workspace slots");
 // fused moments below this many queries (above, k_moments' persistent CTAs
 // have enough query blocks to fill the GPU); env UCP_FUSED_MAX_QUERIES
 const int64_t kFusedMaxQueries = [] {
@@ -1444,7 +1444,7 @@ int ucp_workspace_destroy(ucp_workspace* ws) {
   if (!ws) return UCP_OK;
   std::unique_lock<std::shared_mutex> lk(g_capture_mu);
   cudaDeviceSynchronize();  // in-flight work may still read the buffers
-  for (int i = 0; i < 16; ++i)
+  for (int i = 0; i < 24; ++i)
     if (ws->buf[i]) cudaFree(ws->buf[i]);
   if (ws->scan_tmp) cudaFree(ws->scan_tmp);
   if (ws->h_total) cudaFreeHost(ws->h_total);
