@@ -185,61 +185,161 @@ __global__ void k_unif_ball_sum(const double* __restrict__ x, const double* __re
 // kernels.py:558-577, one thread per output node j, centres in ascending i.
 // masses = mscale * f (the reference forms g.spacing * f as an array first:
 // the same single rounding per element), centres = cpts + cu (points + u).
-__global__ void k_unif_propagate(const double* __restrict__ f, double mscale, const double* __restrict__ cpts,
-                                 const double* __restrict__ cu, int64_t n, double a, double h, int64_t d,
-                                 double rad, double* out) {
-  __shared__ double sm[256], sc[256];
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const double lj = j < d ? cell_left(j, a, h) : 0.0, rj = j < d ? cell_right(j, a, h, d) : 0.0;
-  double acc = 0.0;
-  for (int64_t base = 0; base < n; base += 256) {
-    const int cnt = (int)(n - base < 256 ? n - base : 256);
-    __syncthreads();
-    for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
-      sm[r] = mscale == 1.0 ? f[base + r] : mscale * f[base + r];
-      sc[r] = cu ? cpts[base + r] + cu[base + r] : cpts[base + r];
+// Sources whose ball [c - rad, c + rad] misses a warp's whole cell span
+// [Lw, Rw] add nothing to any of its cells (hi <= Lw <= lj gives ov <= 0, and
+// so does lo >= Rw >= rj; NaN centres stay in), so each warp compacts the
+// sources that can touch it, in ascending order, into its own shared buffer
+// and runs the reference's serial loop over those only: the same additions in
+// the same order, bitwise equal, with the loop shortened to the sources in
+// reach.  kUnifWarps warps per CTA (few cells: spread them over the SMs).
+constexpr int kUnifWarps = 2;
+constexpr int kUnifBuf = 256;
+
+__device__ __forceinline__ void warp_span(bool active, double lj, double rj, double& lw, double& rw) {
+  lw = active ? lj : INFINITY;
+  rw = active ? rj : -INFINITY;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double l2 = __shfl_xor_sync(0xffffffffu, lw, o), r2 = __shfl_xor_sync(0xffffffffu, rw, o);
+    lw = l2 < lw ? l2 : lw;
+    rw = r2 > rw ? r2 : rw;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kUnifWarps) k_unif_propagate(const double* __restrict__ f, double mscale,
+                                                                   const double* __restrict__ cpts,
+                                                                   const double* __restrict__ cu, int64_t n,
+                                                                   double a, double h, int64_t d, double rad,
+                                                                   double* out) {
+  __shared__ double sm_all[kUnifWarps][kUnifBuf], sl_all[kUnifWarps][kUnifBuf], sh_all[kUnifWarps][kUnifBuf];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sm = sm_all[warp];
+  double* sl = sl_all[warp];  // c - rad
+  double* sh = sh_all[warp];  // c + rad
+  const int64_t j0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  if (j0 >= d) return;  // warp-uniform: no cell of this warp exists
+  const int64_t j = j0 + lane;
+  const bool active = j < d;
+  const double lj = active ? cell_left(j, a, h) : 0.0, rj = active ? cell_right(j, a, h, d) : 0.0;
+  double lw, rw;
+  warp_span(active, lj, rj, lw, rw);
+  const unsigned below = (1u << lane) - 1u;
+  // kUnifBuf sources per pass: each lane holds kUnifBuf / 32 of them in
+  // registers (independent loads in flight together; the next pass's loads
+  // issue before this pass's serial loop)
+  constexpr int K = kUnifBuf / 32;
+  double rf[K], rc[K];
+  auto load = [&](int64_t base) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t r = base + k * 32 + lane;
+      rf[k] = 0.0;
+      rc[k] = 0.0;
+      if (r < n) {
+        rf[k] = mscale == 1.0 ? f[r] : mscale * f[r];
+        rc[k] = cu ? cpts[r] + cu[r] : cpts[r];
+      }
     }
-    __syncthreads();
-    if (j < d) {
-      for (int r = 0; r < cnt; ++r) {
-        double lo = sc[r] - rad, hi = sc[r] + rad;
+  };
+  double acc = 0.0;
+  if (n > 0) load(0);
+  for (int64_t base = 0; base < n; base += kUnifBuf) {
+    int fill = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool rel = base + k * 32 + lane < n && !((rc[k] + rad) <= lw || (rc[k] - rad) >= rw);
+      const unsigned mask = __ballot_sync(0xffffffffu, rel);
+      if (rel) {
+        const int pos = fill + __popc(mask & below);
+        sm[pos] = rf[k];
+        sl[pos] = rc[k] - rad;
+        sh[pos] = rc[k] + rad;
+      }
+      fill += __popc(mask);
+    }
+    if (base + kUnifBuf < n) load(base + kUnifBuf);
+    __syncwarp();
+    if (active) {
+#pragma unroll 4
+      for (int q = 0; q < fill; ++q) {
+        double lo = sl[q], hi = sh[q];
         if (lo < lj) lo = lj;
         if (hi > rj) hi = rj;
         const double ov = hi - lo;
-        if (ov > 0.0) acc += sm[r] * ov;
+        if (ov > 0.0) acc += sm[q] * ov;
       }
     }
+    __syncwarp();
   }
-  if (j < d) out[j] = acc * (1.0 / ((2.0 * rad) * h));
+  if (active) out[j] = acc * (1.0 / ((2.0 * rad) * h));
 }
 
 // kernels.py:580-615, one thread per query, support points in ascending i
-__global__ void k_unif_moments_points(const double* __restrict__ y, int64_t n, const double* __restrict__ centers,
-                                      const double* __restrict__ w, const double* __restrict__ vals, int64_t m,
-                                      double a, double h, int64_t d, double rad, double* m0, double* m1, double* m2) {
-  __shared__ double sc[256], sw[256], sv[256];
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// (sources out of the warp's reach skipped as in k_unif_propagate: bitwise)
+__global__ void __launch_bounds__(32 * kUnifWarps) k_unif_moments_points(
+    const double* __restrict__ y, int64_t n, const double* __restrict__ centers, const double* __restrict__ w,
+    const double* __restrict__ vals, int64_t m, double a, double h, int64_t d, double rad, double* m0, double* m1,
+    double* m2) {
+  __shared__ double sl_all[kUnifWarps][kUnifBuf], sh_all[kUnifWarps][kUnifBuf], sw_all[kUnifWarps][kUnifBuf],
+      sv_all[kUnifWarps][kUnifBuf];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sl = sl_all[warp];  // centre - rad
+  double* sh = sh_all[warp];  // centre + rad
+  double* sw = sw_all[warp];
+  double* sv = sv_all[warp];
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  if (t0 >= n) return;  // warp-uniform
+  const int64_t t = t0 + lane;
   const bool active = t < n;
   const long long j = cell_index(active ? y[t] : 0.0, a, h, d);
   const double lj = cell_left(j, a, h), rj = cell_right(j, a, h, d);
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-  for (int64_t base = 0; base < m; base += 256) {
-    const int cnt = (int)(m - base < 256 ? m - base : 256);
-    __syncthreads();
-    for (int r = threadIdx.x; r < cnt; r += blockDim.x) {
-      sc[r] = centers[base + r];
-      sw[r] = w[base + r];
-      sv[r] = vals[base + r];
+  double lw, rw;
+  warp_span(active, lj, rj, lw, rw);
+  const unsigned below = (1u << lane) - 1u;
+  constexpr int K = kUnifBuf / 32;  // register-batched loads as in k_unif_propagate
+  double rc[K], rw_[K], rv[K];
+  auto load = [&](int64_t base) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t r = base + k * 32 + lane;
+      rc[k] = 0.0;
+      rw_[k] = 0.0;
+      rv[k] = 0.0;
+      if (r < m) {
+        rc[k] = centers[r];
+        rw_[k] = w[r];
+        rv[k] = vals[r];
+      }
     }
-    __syncthreads();
+  };
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  if (m > 0) load(0);
+  for (int64_t base = 0; base < m; base += kUnifBuf) {
+    int fill = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool rel = base + k * 32 + lane < m && !((rc[k] + rad) <= lw || (rc[k] - rad) >= rw);
+      const unsigned mask = __ballot_sync(0xffffffffu, rel);
+      if (rel) {
+        const int pos = fill + __popc(mask & below);
+        sl[pos] = rc[k] - rad;
+        sh[pos] = rc[k] + rad;
+        sw[pos] = rw_[k];
+        sv[pos] = rv[k];
+      }
+      fill += __popc(mask);
+    }
+    if (base + kUnifBuf < m) load(base + kUnifBuf);
+    __syncwarp();
     if (active) {
-      for (int r = 0; r < cnt; ++r) {
-        double lo = sc[r] - rad, hi = sc[r] + rad;
+#pragma unroll 4
+      for (int q = 0; q < fill; ++q) {
+        double lo = sl[q], hi = sh[q];
         if (lo < lj) lo = lj;
         if (hi > rj) hi = rj;
         const double ov = hi - lo;
         if (ov > 0.0) {
-          const double wov = sw[r] * ov, vi = sv[r];
+          const double wov = sw[q] * ov, vi = sv[q];
           acc0 += wov;
           const double wv = wov * vi;
           acc1 += wv;
@@ -247,6 +347,7 @@ __global__ void k_unif_moments_points(const double* __restrict__ y, int64_t n, c
         }
       }
     }
+    __syncwarp();
   }
   if (active) {
     const double inv = 1.0 / ((2.0 * rad) * h);
@@ -273,6 +374,43 @@ struct ZdCost0 {
     return f0[i] * (((pw * u) * u) + distortion);
   }
 };
+
+// ZeroDelay stage 0 in partial exhaustion: every candidate is a controller
+// value u0[j], and ZdCost0's moments depend on u alone, so they are computed
+// once per j (k_zd_mom_table, the same unif_moments_at_tab call) and every
+// (point, candidate) pair reads them: the same expression on the same
+// operands, bitwise equal to ZdCost0, at O(1) per candidate.
+struct ZdCost0Memo {
+  const double* y0;
+  const double* f0;
+  const double* S;  // [3][d0]: s0, s1, s2 of u0[j]
+  int64_t d0;
+  double pw;
+  __device__ __forceinline__ double at(double u, int64_t j, int64_t i) const {
+    const double s0 = S[j], s1 = S[d0 + j], s2 = S[2 * d0 + j];
+    const double y = y0[i];
+    const double distortion = (((s0 * y) * y) - ((2.0 * s1) * y)) + s2;
+    return f0[i] * (((pw * u) * u) + distortion);
+  }
+};
+
+__global__ void k_zd_mom_table(ZdCost0 c, const double* __restrict__ u0, int64_t d0, double* S) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d0) return;
+  const Mom3U s = unif_moments_at_tab(u0[j], c.v1, c.a1, c.h1, c.d1, 1.0, c.tab, c.tab + c.d1, c.tab + 2 * c.d1);
+  S[j] = s.s0;
+  S[d0 + j] = s.s1;
+  S[2 * d0 + j] = s.s2;
+}
+
+// candidate j of point i (the memoised functor reads its per-j table)
+template <class Cost>
+__device__ __forceinline__ double exh_cost(const Cost& c, const double* __restrict__ u, int64_t j, int64_t i) {
+  return c(u[j], i);
+}
+__device__ __forceinline__ double exh_cost(const ZdCost0Memo& c, const double* __restrict__ u, int64_t j, int64_t i) {
+  return c.at(u[j], j, i);
+}
 
 // any stage whose cost is quadratic in u with per-point moments (ZeroDelay m=1)
 struct QuadCost {
@@ -366,7 +504,7 @@ __global__ void k_gen_exh_eval(Cost cost, const double* __restrict__ u, const in
   // a value equal to its window predecessor has the same cost and never wins
   // the first-minimum: not evaluated (the reference's flatten_windows dedups
   // the same adjacent repeats, kernels.py:163-187)
-  if (j <= hi[i] && !(k > 0 && u[j] == u[j - 1])) costs[p * wmax + k] = cost(u[j], i);
+  if (j <= hi[i] && !(k > 0 && u[j] == u[j - 1])) costs[p * wmax + k] = exh_cost(cost, u, j, i);
 }
 
 __global__ void k_gen_exh_pick(const double* __restrict__ u, const int64_t* __restrict__ lo,
@@ -509,7 +647,7 @@ int zd_moments(const ucp_zd_problem* P, const double* u0, const double* yq, int6
   int rc;
   if ((rc = ws_get(ws, WS_MOM, sizeof(double) * 3 * (size_t)nq, &pm))) return rc;
   double* m0 = (double*)pm;
-  k_unif_moments_points<<<nblocks(nq, 128), 128, 0, st>>>(yq, nq, u0, P->fw0, P->y0, P->d0, P->a1, P->h1, P->d1,
+  k_unif_moments_points<<<nblocks(nq, 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(yq, nq, u0, P->fw0, P->y0, P->d0, P->a1, P->h1, P->d1,
                                                           1.0, m0, m0 + nq, m0 + 2 * nq);
   UCP_LAUNCHED("k_unif_moments_points");
   q->A = m0;
@@ -545,13 +683,13 @@ int inv_forward_density(const ucp_inv_problem* P, int m, const double* const* u,
   double* bufs[2] = {(double*)pa, (double*)pb};
   const double* one = (const double*)pone;
   // f = unif_propagate([1.0], [0.0], grid 0)
-  k_unif_propagate<<<nblocks(P->d[0], 128), 128, 0, st>>>(one, 1.0, one + 1, nullptr, 1, P->a[0], P->h[0], P->d[0],
+  k_unif_propagate<<<nblocks(P->d[0], 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(one, 1.0, one + 1, nullptr, 1, P->a[0], P->h[0], P->d[0],
                                                            1.0, bufs[0]);
   UCP_LAUNCHED("k_unif_propagate");
   int cur = 0;
   for (int mm = 0; mm < m; ++mm) {
     // f = unif_propagate(h_mm * f, pts_mm + u_mm, grid mm+1)
-    k_unif_propagate<<<nblocks(P->d[mm + 1], 128), 128, 0, st>>>(bufs[cur], P->h[mm], P->pts[mm], u[mm], P->d[mm],
+    k_unif_propagate<<<nblocks(P->d[mm + 1], 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(bufs[cur], P->h[mm], P->pts[mm], u[mm], P->d[mm],
                                                                  P->a[mm + 1], P->h[mm + 1], P->d[mm + 1], 1.0,
                                                                  bufs[cur ^ 1]);
     UCP_LAUNCHED("k_unif_propagate");
@@ -645,7 +783,7 @@ int ucp_unif_ball_sum(const double* x, int64_t n, const double* g, double a, dou
 int ucp_unif_propagate(const double* masses, const double* centers, int64_t n, double a, double h, int64_t d,
                        double rad, double* out, void* stream) {
   if (n < 0 || d < 2) return arg_fail("unif_propagate: bad sizes");
-  k_unif_propagate<<<nblocks(d, 128), 128, 0, as_stream(stream)>>>(masses, 1.0, centers, nullptr, n, a, h, d, rad,
+  k_unif_propagate<<<nblocks(d, 32 * kUnifWarps), 32 * kUnifWarps, 0, as_stream(stream)>>>(masses, 1.0, centers, nullptr, n, a, h, d, rad,
                                                                    out);
   UCP_LAUNCHED("k_unif_propagate");
   return UCP_OK;
@@ -656,7 +794,7 @@ int ucp_unif_moments_points(const double* y, int64_t n, const double* centers, c
                             double* m2, void* stream) {
   if (n < 0 || m < 0 || d < 2) return arg_fail("unif_moments_points: bad sizes");
   if (n == 0) return UCP_OK;
-  k_unif_moments_points<<<nblocks(n, 128), 128, 0, as_stream(stream)>>>(y, n, centers, w, vals, m, a, h, d, rad, m0,
+  k_unif_moments_points<<<nblocks(n, 32 * kUnifWarps), 32 * kUnifWarps, 0, as_stream(stream)>>>(y, n, centers, w, vals, m, a, h, d, rad, m0,
                                                                         m1, m2);
   UCP_LAUNCHED("k_unif_moments_points");
   return UCP_OK;
@@ -725,7 +863,17 @@ int ucp_zd_exhaustion(const ucp_zd_problem* P, int stage, const double* u0, cons
   if (stage == 0) {
     ZdCost0 c;
     if ((rc = zd_cost0_tab(P, u1, ws, st, &c))) return rc;
-    return launch_gen_exhaust(c, u0, win_lo, win_hi, wmax, 0, begin, n, out, err, ws, st);
+    void* ps;
+    if ((rc = ws_get(ws, WS_C5_MEMO, sizeof(double) * 3 * (size_t)P->d0, &ps))) return rc;
+    k_zd_mom_table<<<nblocks(P->d0, 128), 128, 0, st>>>(c, u0, P->d0, (double*)ps);
+    UCP_LAUNCHED("k_zd_mom_table");
+    ZdCost0Memo mc;
+    mc.y0 = P->y0;
+    mc.f0 = P->f0;
+    mc.S = (const double*)ps;
+    mc.d0 = P->d0;
+    mc.pw = P->power_weight;
+    return launch_gen_exhaust(mc, u0, win_lo, win_hi, wmax, 0, begin, n, out, err, ws, st);
   }
   QuadCost q;
   if ((rc = zd_moments(P, u0, P->y1 + begin, n, ws, st, &q))) return rc;
