@@ -211,6 +211,13 @@ typedef struct ucp_inv_problem {
   double h[UCP_INV_MAX_STAGES];
   int64_t d[UCP_INV_MAX_STAGES];
   const double* pts[UCP_INV_MAX_STAGES];
+  /* Optional (NULL: none): host array of M caller-assigned content keys, one
+   * per controller u[m], nonzero and never reused for different contents.
+   * With keys, the stock densities f_k (keyed by u[0..k-1]) and costs-to-go
+   * g_k (keyed by u[k..M-1]) of earlier calls on the same workspace and
+   * problem are reused instead of re-propagated: the same kernels on the same
+   * inputs, so results are unchanged.  Zero-initialise this field. */
+  const uint64_t* ukey;
 } ucp_inv_problem;
 int ucp_inv_cost(const ucp_inv_problem* P, int stage, const double* const* u, const double* u_flat,
                  int64_t n_cand, const int64_t* offsets, const double* y_seg, int64_t nseg,

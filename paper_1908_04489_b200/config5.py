@@ -20,7 +20,7 @@ from . import _lib
 from ._device import F64, I64, ptr, to_device_f64, to_device_i64
 from .device_problem import NO_ERROR, DeviceContext
 from .distributed import LOCAL, Sharding
-from .grids import ControllerSet
+from .grids import ControllerSet, content_key
 from .numerics import Gaussian, pdf
 from .problem import NumericError, Problem
 
@@ -42,7 +42,7 @@ class InvProblemC(ctypes.Structure):
 
     _fields_ = [("stages", c_i32), ("quadratic", c_i32), ("order_cost", c_dbl), ("holding_rate", c_dbl),
                 ("backlog_rate", c_dbl), ("a", c_dbl * MAX_STAGES), ("h", c_dbl * MAX_STAGES),
-                ("d", c_i64 * MAX_STAGES), ("pts", c_vp * MAX_STAGES)]
+                ("d", c_i64 * MAX_STAGES), ("pts", c_vp * MAX_STAGES), ("ukey", c_vp)]
 
 
 _PP = ctypes.POINTER
@@ -277,6 +277,7 @@ class Inventory(_DeviceSweeps, Problem):
         super().__init__(grids)
         self._device_arg = device
         self._dev = None
+        self.reuse = True  # reuse densities / costs-to-go of unchanged stages (result-identical)
 
     def default_grid_specs(self):
         return [(-3.0, 3.0, 601)] * self.stages
@@ -315,7 +316,16 @@ class Inventory(_DeviceSweeps, Problem):
         self._P = P
 
     def _uarray(self, ts):
+        """Device pointers of the controllers, and their content keys into
+        the problem struct (the library then reuses densities / costs-to-go
+        of unchanged stages across calls; no keys, no reuse)."""
         arr = (c_vp * MAX_STAGES)(*[ptr(t) for t in ts])
+        keys = [content_key(t) for t in ts]
+        if self.reuse and all(keys):
+            self._ukeys = (ctypes.c_uint64 * MAX_STAGES)(*keys)
+            self._P.ukey = ctypes.cast(self._ukeys, c_vp)
+        else:
+            self._P.ukey = None
         return arr
 
     def _abi_local(self, m, ts, lp, begin, end, buf, err):

@@ -668,31 +668,127 @@ int check_inv(const ucp_inv_problem* P, const double* const* u) {
 
 inline int inv_state(const ucp_inv_problem* P, int mm) { return mm < P->stages - 1 ? mm : P->stages - 1; }
 
-// Stock density at stage m (inventory.py:96-110) into *out (device, d[m]).
-int inv_forward_density(const ucp_inv_problem* P, int m, const double* const* u, ucp_workspace* ws,
-                        cudaStream_t st, const double** out) {
-  void *pa, *pb, *pone;
+// Reuse across calls when the caller keys its controllers (ucp_inv_problem.ukey):
+// *use = false without keys, during graph capture (host decisions would be
+// baked into the graph), or on a key of 0.  The slots are reset whenever the
+// problem or the cache buffers change.
+int inv_cache_prepare(const ucp_inv_problem* P, ucp_workspace* ws, cudaStream_t st, int64_t dmax, double** fb,
+                      double** gb, bool* use) {
+  *use = false;
+  if (!P->ukey) return UCP_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return UCP_OK;
+  }
+  const int M = P->stages;
+  for (int k = 0; k < M; ++k)
+    if (P->ukey[k] == 0) return UCP_OK;
+  void *pf, *pg;
   int rc;
+  if ((rc = ws_get(ws, WS_C5_FC, sizeof(double) * (size_t)(M + 1) * (size_t)dmax, &pf))) return rc;
+  if ((rc = ws_get(ws, WS_C5_GC, sizeof(double) * (size_t)(M + 1) * (size_t)dmax, &pg))) return rc;
+  ucp_inv_cache& c = ws->inv;
+  ucp_inv_problem key = *P;
+  key.ukey = nullptr;
+  if (!c.valid || c.fbuf != pf || c.gbuf != pg || memcmp(&c.prob, &key, sizeof key) != 0) {
+    c = ucp_inv_cache{};
+    c.prob = key;
+    c.fbuf = pf;
+    c.gbuf = pg;
+    c.valid = true;
+  }
+  *fb = (double*)pf;
+  *gb = (double*)pg;
+  *use = true;
+  return UCP_OK;
+}
+
+int64_t inv_dmax(const ucp_inv_problem* P) {
   int64_t dmax = 0;
   for (int k = 0; k < P->stages; ++k) dmax = P->d[k] > dmax ? P->d[k] : dmax;
-  if ((rc = ws_get(ws, WS_C5_F0, sizeof(double) * (size_t)dmax, &pa))) return rc;
-  if ((rc = ws_get(ws, WS_C5_F1, sizeof(double) * (size_t)dmax, &pb))) return rc;
+  return dmax;
+}
+
+// f_0 = unif_propagate([1.0], [0.0], grid 0)
+int inv_density0(const ucp_inv_problem* P, ucp_workspace* ws, cudaStream_t st, double* out) {
+  void* pone;
+  int rc;
   if ((rc = ws_get(ws, WS_C5_ONE, sizeof(double) * 2, &pone))) return rc;
   static const double one_zero[2] = {1.0, 0.0};
   UCP_CHECK(cudaMemcpyAsync(pone, one_zero, sizeof one_zero, cudaMemcpyHostToDevice, st));
-  double* bufs[2] = {(double*)pa, (double*)pb};
   const double* one = (const double*)pone;
-  // f = unif_propagate([1.0], [0.0], grid 0)
-  k_unif_propagate<<<nblocks(P->d[0], 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(one, 1.0, one + 1, nullptr, 1, P->a[0], P->h[0], P->d[0],
-                                                           1.0, bufs[0]);
+  k_unif_propagate<<<nblocks(P->d[0], 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(one, 1.0, one + 1, nullptr, 1,
+                                                                                   P->a[0], P->h[0], P->d[0], 1.0, out);
   UCP_LAUNCHED("k_unif_propagate");
+  return UCP_OK;
+}
+
+// f_{mm+1} = unif_propagate(h_mm * f_mm, pts_mm + u_mm, grid mm+1)
+int inv_density_step(const ucp_inv_problem* P, int mm, const double* const* u, const double* f, double* out,
+                      cudaStream_t st) {
+  k_unif_propagate<<<nblocks(P->d[mm + 1], 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(
+      f, P->h[mm], P->pts[mm], u[mm], P->d[mm], P->a[mm + 1], P->h[mm + 1], P->d[mm + 1], 1.0, out);
+  UCP_LAUNCHED("k_unif_propagate");
+  return UCP_OK;
+}
+
+// g_M = gamma(terminal state points), on grid inv_state(M)
+int inv_terminal(const ucp_inv_problem* P, double* out, cudaStream_t st) {
+  const int term = inv_state(P, P->stages);
+  k_inv_downstream<<<nblocks(P->d[term], 128), 128, 0, st>>>(P->pts[term], nullptr, P->d[term], nullptr, 0.0, 0.0, 0,
+                                                             0.0, P->quadratic, P->holding_rate, P->backlog_rate, out);
+  UCP_LAUNCHED("k_inv_downstream");
+  return UCP_OK;
+}
+
+// g_mm from g_{mm+1} (tg: scratch for g_{mm+1}'s interior-cell terms)
+int inv_downstream_step(const ucp_inv_problem* P, int mm, const double* const* u, const double* gnext, double* tg,
+                         double* out, cudaStream_t st) {
+  const int nx = inv_state(P, mm + 1);
+  k_unif_ball_terms<<<nblocks(P->d[nx], 256), 256, 0, st>>>(gnext, P->a[nx], P->h[nx], P->d[nx], tg);
+  UCP_LAUNCHED("k_unif_ball_terms");
+  k_inv_downstream<<<nblocks(P->d[mm], 128), 128, 0, st>>>(P->pts[mm], u[mm], P->d[mm], gnext, P->a[nx], P->h[nx],
+                                                           P->d[nx], P->order_cost, P->quadratic, P->holding_rate,
+                                                           P->backlog_rate, out, tg);
+  UCP_LAUNCHED("k_inv_downstream");
+  return UCP_OK;
+}
+
+// Stock density at stage m (inventory.py:96-110) into *out (device, d[m]).
+int inv_forward_density(const ucp_inv_problem* P, int m, const double* const* u, ucp_workspace* ws,
+                        cudaStream_t st, const double** out) {
+  int rc;
+  const int64_t dmax = inv_dmax(P);
+  double *F, *G;
+  bool use;
+  if ((rc = inv_cache_prepare(P, ws, st, dmax, &F, &G, &use))) return rc;
+  if (use) {
+    ucp_inv_cache& c = ws->inv;
+    int start = -1;
+    for (int k = m; k >= 0 && start < 0; --k)
+      if (c.fok[k] && std::equal(P->ukey, P->ukey + k, c.fkey[k])) start = k;
+    if (start < 0) {
+      if ((rc = inv_density0(P, ws, st, F))) return rc;
+      c.fok[0] = true;
+      start = 0;
+    }
+    for (int mm = start; mm < m; ++mm) {
+      if ((rc = inv_density_step(P, mm, u, F + (size_t)mm * dmax, F + (size_t)(mm + 1) * dmax, st))) return rc;
+      c.fok[mm + 1] = true;
+      std::copy(P->ukey, P->ukey + mm + 1, c.fkey[mm + 1]);
+    }
+    *out = F + (size_t)m * dmax;
+    return UCP_OK;
+  }
+  void *pa, *pb;
+  if ((rc = ws_get(ws, WS_C5_F0, sizeof(double) * (size_t)dmax, &pa))) return rc;
+  if ((rc = ws_get(ws, WS_C5_F1, sizeof(double) * (size_t)dmax, &pb))) return rc;
+  double* bufs[2] = {(double*)pa, (double*)pb};
+  if ((rc = inv_density0(P, ws, st, bufs[0]))) return rc;
   int cur = 0;
   for (int mm = 0; mm < m; ++mm) {
-    // f = unif_propagate(h_mm * f, pts_mm + u_mm, grid mm+1)
-    k_unif_propagate<<<nblocks(P->d[mm + 1], 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(bufs[cur], P->h[mm], P->pts[mm], u[mm], P->d[mm],
-                                                                 P->a[mm + 1], P->h[mm + 1], P->d[mm + 1], 1.0,
-                                                                 bufs[cur ^ 1]);
-    UCP_LAUNCHED("k_unif_propagate");
+    if ((rc = inv_density_step(P, mm, u, bufs[cur], bufs[cur ^ 1], st))) return rc;
     cur ^= 1;
   }
   *out = bufs[cur];
@@ -702,31 +798,42 @@ int inv_forward_density(const ucp_inv_problem* P, int m, const double* const* u,
 // g_{m+1} on the stage-(m+1) state grid (inventory.py:78-94), backwards from M.
 int inv_downstream(const ucp_inv_problem* P, int m, const double* const* u, ucp_workspace* ws, cudaStream_t st,
                    const double** out) {
-  void *pa, *pb;
   int rc;
-  int64_t dmax = 0;
-  for (int k = 0; k < P->stages; ++k) dmax = P->d[k] > dmax ? P->d[k] : dmax;
+  const int64_t dmax = inv_dmax(P);
+  const int M = P->stages;
+  void* ptg;
+  if ((rc = ws_get(ws, WS_C5_GT0, sizeof(double) * (size_t)dmax, &ptg))) return rc;
+  double* tg = (double*)ptg;
+  double *F, *G;
+  bool use;
+  if ((rc = inv_cache_prepare(P, ws, st, dmax, &F, &G, &use))) return rc;
+  if (use) {
+    ucp_inv_cache& c = ws->inv;
+    int start = -1;
+    for (int k = m + 1; k <= M && start < 0; ++k)
+      if (c.gok[k] && std::equal(P->ukey + k, P->ukey + M, c.gkey[k] + k)) start = k;
+    if (start < 0) {
+      if ((rc = inv_terminal(P, G + (size_t)M * dmax, st))) return rc;
+      c.gok[M] = true;
+      start = M;
+    }
+    for (int mm = start - 1; mm >= m + 1; --mm) {
+      if ((rc = inv_downstream_step(P, mm, u, G + (size_t)(mm + 1) * dmax, tg, G + (size_t)mm * dmax, st)))
+        return rc;
+      c.gok[mm] = true;
+      std::copy(P->ukey + mm, P->ukey + M, c.gkey[mm] + mm);
+    }
+    *out = G + (size_t)(m + 1) * dmax;
+    return UCP_OK;
+  }
+  void *pa, *pb;
   if ((rc = ws_get(ws, WS_C5_G0, sizeof(double) * (size_t)dmax, &pa))) return rc;
   if ((rc = ws_get(ws, WS_C5_G1, sizeof(double) * (size_t)dmax, &pb))) return rc;
   double* bufs[2] = {(double*)pa, (double*)pb};
-  const int M = P->stages;
-  const int term = inv_state(P, M);
   int cur = 0;
-  k_inv_downstream<<<nblocks(P->d[term], 128), 128, 0, st>>>(P->pts[term], nullptr, P->d[term], nullptr, 0.0, 0.0, 0,
-                                                             0.0, P->quadratic, P->holding_rate, P->backlog_rate,
-                                                             bufs[cur]);
-  UCP_LAUNCHED("k_inv_downstream");
-  void* ptg;
-  if ((rc = ws_get(ws, WS_C5_GT0, sizeof(double) * (size_t)dmax, &ptg))) return rc;
+  if ((rc = inv_terminal(P, bufs[cur], st))) return rc;
   for (int mm = M - 1; mm >= m + 1; --mm) {
-    const int nx = inv_state(P, mm + 1);
-    k_unif_ball_terms<<<nblocks(P->d[nx], 256), 256, 0, st>>>(bufs[cur], P->a[nx], P->h[nx], P->d[nx], (double*)ptg);
-    UCP_LAUNCHED("k_unif_ball_terms");
-    k_inv_downstream<<<nblocks(P->d[mm], 128), 128, 0, st>>>(P->pts[mm], u[mm], P->d[mm], bufs[cur], P->a[nx],
-                                                             P->h[nx], P->d[nx], P->order_cost, P->quadratic,
-                                                             P->holding_rate, P->backlog_rate, bufs[cur ^ 1],
-                                                             (const double*)ptg);
-    UCP_LAUNCHED("k_inv_downstream");
+    if ((rc = inv_downstream_step(P, mm, u, bufs[cur], tg, bufs[cur ^ 1], st))) return rc;
     cur ^= 1;
   }
   *out = bufs[cur];

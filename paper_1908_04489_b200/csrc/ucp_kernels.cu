@@ -14,6 +14,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <array>
 #include <atomic>
 #include <vector>
@@ -1266,6 +1267,20 @@ struct ucp_graph_entry {
 // synchronising calls (workspace growth / destruction) hold it exclusively.
 std::shared_mutex g_capture_mu;
 
+// Inventory density / cost-to-go reuse across calls (ucp_inv_problem.ukey):
+// slot k of the forward buffer holds f_k computed from controllers with keys
+// fkey[k][0..k-1]; slot k of the backward buffer g_k from gkey[k][k..M-1].
+struct ucp_inv_cache {
+  bool valid = false;
+  ucp_inv_problem prob{};  // the problem the slots belong to (ukey cleared)
+  const void* fbuf = nullptr;
+  const void* gbuf = nullptr;
+  bool fok[UCP_INV_MAX_STAGES + 1] = {false};
+  bool gok[UCP_INV_MAX_STAGES + 1] = {false};
+  uint64_t fkey[UCP_INV_MAX_STAGES + 1][UCP_INV_MAX_STAGES] = {};
+  uint64_t gkey[UCP_INV_MAX_STAGES + 1][UCP_INV_MAX_STAGES] = {};
+};
+
 struct ucp_workspace {
   void* buf[24] = {nullptr};
   size_t cap[24] = {0};
@@ -1274,12 +1289,13 @@ struct ucp_workspace {
   int64_t* h_total = nullptr;           // pinned
   cudaStream_t cap_stream = nullptr;    // private stream for CUDA-graph capture
   std::vector<ucp_graph_entry> graphs;  // one instantiated graph per block signature
+  ucp_inv_cache inv;
 };
 
 namespace {
 enum {
   WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS,
-  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_C5_TAB, WS_C5_GT0, WS_C5_GT1, WS_C5_MEMO, WS_NSLOTS
+  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_C5_TAB, WS_C5_GT0, WS_C5_GT1, WS_C5_MEMO, WS_C5_FC, WS_C5_GC, WS_NSLOTS
 };
 static_assert(WS_NSLOTS <= 24, "workspace slots");
 // fused moments below this many queries (above, k_moments' persistent CTAs

@@ -9,6 +9,7 @@ on the GPU from start to finish.
 """
 from __future__ import annotations
 
+import itertools
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -69,6 +70,21 @@ def _is_tensor(x) -> bool:
     return isinstance(x, torch.Tensor)
 
 
+_CONTENT_KEYS = itertools.count(1)
+
+
+def content_key(t) -> int:
+    """A nonzero 64-bit key for the CONTENTS of a controller's device tensor
+    (0: none): a serial stamped when the controller adopts or creates the
+    tensor, combined with the tensor's in-place version counter, so a key is
+    never shared by different contents (ucp_inv_problem.ukey)."""
+    serial = getattr(t, "_ucp_serial", 0)
+    version = t._version
+    if not serial or version >= 1 << 20 or serial >= 1 << 43:
+        return 0
+    return (serial << 20) | version
+
+
 class SampledController:
     """Immutable step-function controller: one float64 value per grid point.
 
@@ -96,6 +112,7 @@ class SampledController:
                 if not bool(ok.all()):
                     bad = int(torch.nonzero(~ok)[0, 0])
                     raise ValueError(f"controller value at grid point {bad} is not finite")
+            t._ucp_serial = next(_CONTENT_KEYS)
             object.__setattr__(self, "_dev", t)
             return
         vals = np.array(values.cpu() if _is_tensor(values) else values, dtype=np.float64)
@@ -126,6 +143,7 @@ class SampledController:
         dev = self._dev
         if dev is None or dev.device != torch.device(device):
             dev = torch.from_numpy(np.array(self.values)).to(device)
+            dev._ucp_serial = next(_CONTENT_KEYS)
             object.__setattr__(self, "_dev", dev)
         return dev
 

@@ -110,3 +110,50 @@ def test_uniform_kernels_vs_oracle(P, oracle_mod, seed):
         want = oracle_mod.unif_moments_points(q, x, w, vals, a, h, d, rad)
         for k in range(3):
             assert_bitwise(outs[k].cpu().numpy(), want[k], f"unif_moments_points m{k}")
+
+
+def test_inventory_reuse_across_calls_is_result_identical(P):
+    """Densities / costs-to-go reused across calls (content keys) give the
+    bits of the no-reuse path, in any call order, and an in-place change of a
+    controller tensor (version bump) is never served from the cache."""
+    rng = np.random.default_rng(7)
+    M, d = 5, 97
+    specs = [(-3.0, 3.0, d)] * M
+    keyed, plain = P.Inventory(stages=M, grids=specs), P.Inventory(stages=M, grids=specs)
+    plain.reuse = False
+    pts = keyed.grids[0].points
+    sets = [[np.maximum(0.0, 0.5 - 0.3 * pts + 0.2 * rng.uniform(-1, 1, d)) for _ in range(M)] for _ in range(3)]
+    cfg = P.SolverConfig()
+    # the keyed side reuses its controller objects (stable keys: cache hits)
+    ctrl = [[P.SampledController(keyed.grids[k], sets[s][k]) for k in range(M)] for s in range(3)]
+    from paper_1908_04489_b200 import _lib
+
+    launches = [0, 0]
+    for step in range(24):
+        pick = [int(rng.integers(3)) for _ in range(M)]  # stages drawn from different sets
+        us = [sets[pick[k]][k] for k in range(M)]
+        m = int(rng.integers(M))
+        Uk = P.ControllerSet(tuple(ctrl[pick[k]][k] for k in range(M)))
+        Up = _U(P, plain, us)
+        n0 = _lib.launch_count()
+        a = P.local_update_phase(keyed, m, Uk, cfg)
+        n1 = _lib.launch_count()
+        b = P.local_update_phase(plain, m, Up, cfg)
+        launches[0] += n1 - n0
+        launches[1] += _lib.launch_count() - n1
+        assert_bitwise(a, b, f"LU{m} {step}")
+        assert_bitwise(keyed.forward_density(m, Uk), plain.forward_density(m, Up), f"f{m} {step}")
+        if step % 4 == 0:
+            assert_bitwise(P.partial_exhaustion_phase(keyed, m, Uk, cfg),
+                           P.partial_exhaustion_phase(plain, m, Up, cfg), f"EX{m} {step}")
+    assert launches[0] < launches[1], launches  # reuse happened
+    # in-place change of stage 0's device values after they were cached
+    us = sets[0]
+    Uk = P.ControllerSet(tuple(ctrl[0]))
+    P.local_update_phase(keyed, M - 1, Uk, cfg)
+    t = Uk.device_values(0, torch.device("cuda"))
+    t.add_(0.125)
+    changed = [us[0] + 0.125] + list(us[1:])
+    for m in (M - 1, 1):
+        assert_bitwise(P.local_update_phase(keyed, m, Uk, cfg),
+                       P.local_update_phase(plain, m, _U(P, plain, changed), cfg), f"LU{m} after in-place change")

@@ -1,7 +1,7 @@
 """Kernel-time breakdown (CUPTI) of config-5 solves (ZeroDelay d=16384,
 Inventory M=3 d=4096), for ncu target selection and profiles/.
 
-    python tools/profile_config5.py
+    python tools/profile_config5.py [zd_16384,inv3_4096,inv8_601]
 """
 import json
 import sys
@@ -16,8 +16,10 @@ sys.path.insert(0, str(ROOT))
 import paper_1908_04489_b200 as P  # noqa: E402
 
 cases = {"zd_16384": lambda: P.ZeroDelay(grids=[(-5.0, 5.0, 16384), (-6.0, 6.0, 16384)]),
-         "inv3_4096": lambda: P.Inventory(stages=3, grids=[(-3.0, 3.0, 4096)] * 3)}
-for name, mk in cases.items():
+         "inv3_4096": lambda: P.Inventory(stages=3, grids=[(-3.0, 3.0, 4096)] * 3),
+         "inv8_601": lambda: P.Inventory(stages=8, grids=[(-3.0, 3.0, 601)] * 8)}
+pick = sys.argv[1].split(",") if len(sys.argv) > 1 else ["zd_16384", "inv3_4096"]
+for name, mk in ((k, cases[k]) for k in pick):
     P.solve(mk(), P.SolverConfig(max_rounds=1))
     torch.cuda.synchronize()
     agg = defaultdict(lambda: [0, 0.0])
