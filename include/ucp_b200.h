@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define UCP_ABI_VERSION 1
+#define UCP_ABI_VERSION 2
 
 enum ucp_status {
   UCP_OK = 0,

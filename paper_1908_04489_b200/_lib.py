@@ -97,8 +97,8 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.ucp_abi_version() != 1:
-        raise ImportError(f"libucp_b200 ABI {lib.ucp_abi_version()} != 1")
+    if lib.ucp_abi_version() != 2:
+        raise ImportError(f"libucp_b200 ABI {lib.ucp_abi_version()} != 2")
     _LIB = lib
     return lib
 

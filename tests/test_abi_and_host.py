@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
     L = _lib.load()
-    assert L.ucp_abi_version() == 1
+    assert L.ucp_abi_version() == 2
     assert L.ucp_status_string(1) == b"bad argument"
 
 
