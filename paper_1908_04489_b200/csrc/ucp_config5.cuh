@@ -647,8 +647,8 @@ int zd_moments(const ucp_zd_problem* P, const double* u0, const double* yq, int6
   int rc;
   if ((rc = ws_get(ws, WS_MOM, sizeof(double) * 3 * (size_t)nq, &pm))) return rc;
   double* m0 = (double*)pm;
-  k_unif_moments_points<<<nblocks(nq, 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(yq, nq, u0, P->fw0, P->y0, P->d0, P->a1, P->h1, P->d1,
-                                                          1.0, m0, m0 + nq, m0 + 2 * nq);
+  k_unif_moments_points<<<nblocks(nq, 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(
+      yq, nq, u0, P->fw0, P->y0, P->d0, P->a1, P->h1, P->d1, 1.0, m0, m0 + nq, m0 + 2 * nq);
   UCP_LAUNCHED("k_unif_moments_points");
   q->A = m0;
   q->B = m0 + nq;
@@ -890,8 +890,8 @@ int ucp_unif_ball_sum(const double* x, int64_t n, const double* g, double a, dou
 int ucp_unif_propagate(const double* masses, const double* centers, int64_t n, double a, double h, int64_t d,
                        double rad, double* out, void* stream) {
   if (n < 0 || d < 2) return arg_fail("unif_propagate: bad sizes");
-  k_unif_propagate<<<nblocks(d, 32 * kUnifWarps), 32 * kUnifWarps, 0, as_stream(stream)>>>(masses, 1.0, centers, nullptr, n, a, h, d, rad,
-                                                                   out);
+  k_unif_propagate<<<nblocks(d, 32 * kUnifWarps), 32 * kUnifWarps, 0, as_stream(stream)>>>(
+      masses, 1.0, centers, nullptr, n, a, h, d, rad, out);
   UCP_LAUNCHED("k_unif_propagate");
   return UCP_OK;
 }
@@ -901,8 +901,8 @@ int ucp_unif_moments_points(const double* y, int64_t n, const double* centers, c
                             double* m2, void* stream) {
   if (n < 0 || m < 0 || d < 2) return arg_fail("unif_moments_points: bad sizes");
   if (n == 0) return UCP_OK;
-  k_unif_moments_points<<<nblocks(n, 32 * kUnifWarps), 32 * kUnifWarps, 0, as_stream(stream)>>>(y, n, centers, w, vals, m, a, h, d, rad, m0,
-                                                                        m1, m2);
+  k_unif_moments_points<<<nblocks(n, 32 * kUnifWarps), 32 * kUnifWarps, 0, as_stream(stream)>>>(
+      y, n, centers, w, vals, m, a, h, d, rad, m0, m1, m2);
   UCP_LAUNCHED("k_unif_moments_points");
   return UCP_OK;
 }
