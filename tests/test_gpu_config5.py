@@ -157,3 +157,43 @@ def test_inventory_reuse_across_calls_is_result_identical(P):
     for m in (M - 1, 1):
         assert_bitwise(P.local_update_phase(keyed, m, Uk, cfg),
                        P.local_update_phase(plain, m, _U(P, plain, changed), cfg), f"LU{m} after in-place change")
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 33, 255, 257, 1000])
+def test_uniform_source_compaction_edges(P, oracle_mod, n):
+    """k_unif_propagate / k_unif_moments_points skip sources out of a warp's
+    reach: source counts around the 32-lane and 256-source batch boundaries,
+    clustered / far-away / infinite / NaN centres, bitwise vs the oracle."""
+    from paper_1908_04489_b200 import _lib, config5
+    from paper_1908_04489_b200._device import ptr, stream_ptr
+
+    config5._bind()
+    rng = np.random.default_rng(n)
+    a, b, d = -2.0, 2.0, 301
+    h = (b - a) / (d - 1)
+    x = np.concatenate([rng.uniform(-0.1, 0.1, n // 2), rng.uniform(a - 6, b + 6, n - n // 2)])
+    rng.shuffle(x)
+    if n >= 31:
+        x[3], x[7], x[11], x[30] = np.inf, -np.inf, np.nan, 50.0
+    masses = np.abs(rng.normal(0, 1, n))
+    w, vals = np.abs(rng.normal(0, 1, n)), rng.normal(0, 3, n)
+    q = np.concatenate([np.linspace(a - 0.5, b + 0.5, 77), [a, b, a - 3.0, b + 3.0]])
+    dev = torch.device("cuda", 0)
+    keep = []
+
+    def T(z):
+        t = torch.from_numpy(np.ascontiguousarray(z, dtype=np.float64)).to(dev)
+        keep.append(t)
+        return t
+
+    s = stream_ptr(dev)
+    for rad in (1.0, 0.05):
+        out = torch.empty(d, dtype=torch.float64, device=dev)
+        _lib.call("ucp_unif_propagate", ptr(T(masses)), ptr(T(x)), n, a, h, d, rad, ptr(out), s)
+        assert_bitwise(out.cpu().numpy(), oracle_mod.unif_propagate(masses, x, a, h, d, rad), f"propagate n={n}")
+        outs = [torch.empty(q.size, dtype=torch.float64, device=dev) for _ in range(3)]
+        _lib.call("ucp_unif_moments_points", ptr(T(q)), q.size, ptr(T(x)), ptr(T(w)), ptr(T(vals)), n, a, h, d,
+                  rad, *(ptr(o) for o in outs), s)
+        want = oracle_mod.unif_moments_points(q, x, w, vals, a, h, d, rad)
+        for k in range(3):
+            assert_bitwise(outs[k].cpu().numpy(), want[k], f"unif_moments_points m{k} n={n}")
