@@ -193,7 +193,7 @@ __global__ void k_unif_ball_sum(const double* __restrict__ x, const double* __re
 // the same order, bitwise equal, with the loop shortened to the sources in
 // reach.  kUnifWarps warps per CTA (few cells: spread them over the SMs).
 constexpr int kUnifWarps = 2;
-constexpr int kUnifBuf = 256;
+constexpr int kUnifBuf = 512;
 
 __device__ __forceinline__ void warp_span(bool active, double lj, double rj, double& lw, double& rw) {
   lw = active ? lj : INFINITY;
