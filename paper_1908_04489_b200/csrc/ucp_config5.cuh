@@ -59,6 +59,29 @@ __device__ __forceinline__ Mom3U unif_moments_at(double x, const double* __restr
   return r;
 }
 
+// Interior-cell run of one table (unif_ball_at_tab): the additions stay in
+// ascending order, while an L1 prefetch runs kPfCells ahead of the loads (a
+// lone warp per scheduler otherwise waits one L2 round trip per unrolled
+// batch: long-scoreboard stalls on the first add of each batch).  The
+// three-table moments loop is left to the compiler: the same prefetching
+// made the ZeroDelay probes slower.
+constexpr int kPfCells = 128;
+__device__ __forceinline__ void prefetch_l1(const double* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+__device__ __forceinline__ double sum_run(double acc, const double* __restrict__ t, long long j0, long long j1) {
+  long long j = j0;
+  for (; j + 15 <= j1; j += 16) {
+    prefetch_l1(t + (j + kPfCells <= j1 ? j + kPfCells : j1));
+    double v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = __ldg(t + j + k);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc += v[k];
+  }
+  for (; j <= j1; ++j) acc += __ldg(t + j);
+  return acc;
+}
+
 // The same moments with the interior cells' terms read from tables: a cell
 // at least two cells inside the window [cell(x - rad), cell(x + rad)]
 // overlaps it completely (its bounds are the neighbours' shared edges,
@@ -151,7 +174,7 @@ __device__ __forceinline__ double unif_ball_at_tab(double x, const double* __res
   if (jlo <= jhi) {
     const long long e0 = jlo + 1 < jhi ? jlo + 1 : jhi;
     for (long long j = jlo; j <= e0; ++j) edge(j);
-    for (long long j = jlo + 2; j <= jhi - 2; ++j) acc += __ldg(tg + j);
+    acc = sum_run(acc, tg, jlo + 2, jhi - 2);
     for (long long j = (jhi - 1 > jlo + 2 ? jhi - 1 : jlo + 2); j <= jhi; ++j) edge(j);
   }
   return acc * (1.0 / (2.0 * rad));
