@@ -44,3 +44,30 @@ def test_reference_arm_contract():
     assert d["impl"] == "reference" and d["unit"] == "evals/s" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["value"] == d["value"]
+
+
+def _run_torchrun(world, *args):
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
+                        "--gpus", str(world), *args], cwd=str(ROOT), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]  # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_bench_line_contract_two_ranks():
+    """The driver's N>1 launch (torchrun, one rank per GPU) on a one-GPU box: gloo, both
+    ranks on cuda:0 — plumbing only (barriers, max-over-ranks timing, one JSON line)."""
+    d = _run_torchrun(2, "--steps", "1", "--warmup", "3", "--log2d", "12", "--no-cpu-baseline",
+                      "--backend", "gloo", "--same-device")
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert d["time_to_converge"]["J"] == 0.16692114286407383  # sharded C1 solve, bitwise the reference
+
