@@ -123,7 +123,12 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 struct WalkGrid {
   double a, h, b, q;  // b = a + h*(d-1); q = exp(-h*h)   (kernels.py:411-412)
   int64_t d;
+  // Suffix bounds for the walk's no-op tail (nullptr: walk every node):
+  // vsuf[j >> kVsufShift] >= |v_j'| for every j' >= (j >> kVsufShift) << kVsufShift,
+  // +inf when any v_j' in that suffix is not finite (see walk_tail_noop).
+  const double* vsuf;
 };
+constexpr int kVsufShift = 8;  // 256 nodes per suffix block
 
 struct Mom3 {
   double t0, t1, t2;
@@ -149,6 +154,7 @@ WalkGrid make_walk_grid(double a, double h, int64_t d) {
   g.d = d;
   g.b = a + h * (double)(d - 1);
   g.q = ucp_exp_tab((-h) * h, h_exp_tab);  // same port as the device: bitwise glibc
+  g.vsuf = nullptr;
   return g;
 }
 
@@ -176,6 +182,27 @@ template <int kMode>
 __device__ __forceinline__ double2 walk_ld2(const double* v, int j) {
   if (kMode == 2) return *reinterpret_cast<const double2*>(v + j);
   return __ldg(reinterpret_cast<const double2*>(v + j));
+}
+
+// Result-invariant early end of a walk (throughput mode only).  Past the
+// Gaussian's peak (ratio <= 1; q < 1 keeps every later ratio <= 1) the
+// computed pdf never grows (fl is monotone and pdf*ratio <= pdf), so with
+// wpc = fl(h*pdf) and vm >= |v_j'| for every remaining node, monotonicity of
+// rounding bounds every remaining addend exactly:
+//   acc0 += wp' <= wpc,  |acc1 += wv'| <= fl(wpc*vm),  acc2 += fl(wv'*v') <= fl(fl(wpc*vm)*vm).
+// An addend t with |t| < |acc| * 2^-56 (< half the smaller ulp around acc,
+// acc normal) leaves acc unchanged under round-to-nearest, so once all three
+// bounds are below their thresholds no remaining node changes a bit and the
+// walk may stop.  vm = +inf (a non-finite v ahead) or NaN never passes.
+__device__ __forceinline__ bool walk_tail_noop(double pdf, double ratio, double h, double vm, double acc0,
+                                               double acc1, double acc2) {
+  const double e = 0x1p-56, tiny = 0x1p-960;
+  const double wpc = h * pdf;
+  const double b1 = wpc * vm;
+  const double b2 = b1 * vm;
+  const double a1 = fabs(acc1);
+  return ratio <= 1.0 && acc0 > tiny && a1 > tiny && acc2 > tiny && wpc < acc0 * e && b1 < a1 * e &&
+         b2 < acc2 * e;
 }
 
 template <int kMode>
@@ -246,7 +273,14 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
         j += 4;
       }
     } else {
+      const double* __restrict__ vsuf = g.vsuf;
+      int it = 0;
       for (; j + 3 <= jint; j += 4) {
+        if (vsuf && (++it & 15) == 0 &&
+            walk_tail_noop(pdf, ratio, h, __ldg(vsuf + (j >> kVsufShift)), acc0, acc1, acc2)) {
+          j = je + 1;  // every remaining node (incl. a half-weight last one) is a no-op
+          break;
+        }
         const double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
         const double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
         UCP_WALK_STEP_V(h, p0.x);
@@ -520,6 +554,42 @@ __global__ void k_segmented_argmin(const double* __restrict__ costs, const int64
 // repeats collapsed (identical values give identical costs, and the
 // first-occurrence argmin returns the same value -- the reference's own
 // flatten_windows dedups, kernels.py:163-187).
+// Suffix bounds of |v| per 256-node block for walk_tail_noop: one CTA
+// (d <= 2^31 nodes; ~8 B/node read once, negligible beside the walks that use it).
+// vsuf[b] = max |v_j| over j >= 256 b, +inf once any such v_j is not finite.
+__global__ void __launch_bounds__(1024) k_vsuf(const double* __restrict__ v, int64_t d, double* vsuf) {
+  __shared__ double seg[1024];
+  const int64_t nb = (d + (1 << kVsufShift) - 1) >> kVsufShift;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t b = warp; b < nb; b += 32) {  // block maxima, one warp per block
+    double m = 0.0;
+    for (int64_t j = (b << kVsufShift) + lane; j < d && j < ((b + 1) << kVsufShift); j += 32) {
+      double a = fabs(v[j]);
+      m = (a <= 1.7976931348623157e308) ? fmax(m, a) : INFINITY;  // NaN / inf -> inf
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) vsuf[b] = m;
+  }
+  __syncthreads();
+  const int64_t per = (nb + 1023) / 1024;
+  const int64_t b0 = threadIdx.x * per, b1 = b0 + per < nb ? b0 + per : nb;
+  double m = 0.0;
+  for (int64_t b = b1 - 1; b >= b0; --b) m = fmax(m, vsuf[b]);
+  seg[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {  // inclusive suffix max over segments
+    double x = threadIdx.x + o < 1024 ? seg[threadIdx.x + o] : 0.0;
+    __syncthreads();
+    seg[threadIdx.x] = fmax(seg[threadIdx.x], x);
+    __syncthreads();
+  }
+  m = threadIdx.x + 1 < 1024 ? seg[threadIdx.x + 1] : 0.0;  // max over later segments
+  for (int64_t b = b1 - 1; b >= b0; --b) {
+    m = fmax(m, vsuf[b]);
+    vsuf[b] = m;
+  }
+}
+
 __global__ void k_ex_count(const double* __restrict__ u, const int64_t* __restrict__ lo,
                            const int64_t* __restrict__ hi, int64_t begin, int64_t n, int64_t* counts) {
   pdl_wait();
@@ -1295,7 +1365,7 @@ struct ucp_workspace {
 namespace {
 enum {
   WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS,
-  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_C5_TAB, WS_C5_GT0, WS_C5_GT1, WS_C5_MEMO, WS_C5_FC, WS_C5_GC, WS_NSLOTS
+  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_C5_TAB, WS_C5_GT0, WS_C5_GT1, WS_C5_MEMO, WS_C5_FC, WS_C5_GC, WS_VSUF, WS_NSLOTS
 };
 static_assert(WS_NSLOTS <= 24, "workspace slots");
 // fused moments below this many queries (above, k_moments' persistent CTAs
@@ -1418,6 +1488,23 @@ void allow_smem(K* kernel) {  // opt in to >48 KiB dynamic shared memory (walk k
     }                                                                                             \
   } while (0)
 
+// Throughput-mode stage-0 walks over v1 end at their no-op tail
+// (walk_tail_noop, result-invariant): build the suffix bounds of v1 on the
+// stream first.  UCP_TAIL_EXIT=0 walks every node.
+const bool g_tail_exit = [] {
+  const char* e = getenv("UCP_TAIL_EXIT");
+  return !(e && e[0] == '0');
+}();
+int attach_vsuf(WalkGrid* g, const double* v1, int64_t n_walks, ucp_workspace* ws, cudaStream_t st) {
+  if (!g_tail_exit || walk_latency_mode(n_walks)) return UCP_OK;
+  void* p;
+  if (int rc = ws_get(ws, WS_VSUF, sizeof(double) * (size_t)((g->d >> kVsufShift) + 1), &p)) return rc;
+  k_vsuf<<<1, 1024, 0, st>>>(v1, g->d, (double*)p);
+  UCP_LAUNCHED("k_vsuf");
+  g->vsuf = (const double*)p;
+  return UCP_OK;
+}
+
 int check_aligned(const void* v) {
   if (reinterpret_cast<uintptr_t>(v) & 15u) return arg_fail("controller arrays must be 16-byte aligned");
   return UCP_OK;
@@ -1484,6 +1571,7 @@ int ucp_workspace_reserve(ucp_workspace* ws, int64_t d0, int64_t d1, int64_t max
   if ((rc = ws_get(ws, WS_COUNT, sizeof(int64_t) * (size_t)(dm + 1), &p))) return rc;
   if ((rc = ws_get(ws, WS_CAND_PT, sizeof(int32_t) * (size_t)max_cand, &p))) return rc;
   if ((rc = ws_get(ws, WS_CAND_J, sizeof(int32_t) * (size_t)max_cand, &p))) return rc;
+  if ((rc = ws_get(ws, WS_VSUF, sizeof(double) * (size_t)((d1 >> kVsufShift) + 1), &p))) return rc;
   return UCP_OK;
 }
 
@@ -1591,6 +1679,7 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
     if ((rc = ws_get(ws, WS_COST, sizeof(double) * 3 * (size_t)n, &pc))) return rc;
     if (int rc_ = check_aligned(u1)) return rc_;
     WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
+    if ((rc = attach_vsuf(&g, u1, 3 * n, ws, st))) return rc;
     UCP_WALK_LAUNCH_PDL(k_lu0_probe, 3 * n, nblocks(3 * n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
                                                      (double*)pc, kNoBatch);
     UCP_LAUNCHED("k_lu0_probe");
@@ -1679,6 +1768,7 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
   UCP_LAUNCHED("k_ex_fill");
   if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
+  if ((rc = attach_vsuf(&g, u1, total, ws, st))) return rc;
   UCP_WALK_LAUNCH(k_ex0_eval, total, nblocks(total, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, counts + n,
                                                   (const int32_t*)ppt, (const int32_t*)pj, (double*)pc, kNoBatch);
   UCP_LAUNCHED("k_ex0_eval");

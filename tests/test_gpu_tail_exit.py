@@ -1,0 +1,31 @@
+"""The walk's no-op tail exit (walk_tail_noop in csrc/ucp_kernels.cu) is
+result-invariant: every phase output of the bench snapshot and J are bitwise
+equal with UCP_TAIL_EXIT=1 (default) and 0 (every node walked, the reference's
+loop).  2^17 points: both stage-0 phases run the throughput-mode walk."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _run(flag, out):
+    env = dict(os.environ, UCP_TAIL_EXIT=flag)
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "tail_exit_ab.py"), "--log2d", "17", "--out", str(out)],
+                       cwd=str(ROOT), env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return np.load(out)
+
+
+def test_tail_exit_bitwise(tmp_path):
+    a = _run("0", tmp_path / "full.npz")
+    b = _run("1", tmp_path / "exit.npz")
+    assert set(a.files) == set(b.files) == {"local0", "local1", "exh0", "exh1", "J"}
+    for k in a.files:
+        assert a[k].tobytes() == b[k].tobytes(), k
+    assert b["J"][0] > 0
