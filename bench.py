@@ -451,14 +451,33 @@ def run_ours(args):
                "path": "public API: SampledController from pinned host arrays -> 4 device sweeps + objective "
                        "-> new controllers copied back to pinned host buffers, J to host"}
 
-    # roofline: every kernel family, and the dominant one
+    # executed walk nodes: the no-op tail exit (csrc walk_tail_noop) visits fewer nodes than
+    # the reference's windows, so the roofline counts what the kernels actually walked --
+    # one untimed, instrumented pass of the two stage-0 phases on this rank's shard
+    ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+    visited = {}
+    for key, kind in (("lu0", "local"), ("ex0", "exhaustion")):
+        ctr.zero_()
+        torch.cuda.synchronize()
+        _lib.call("ucp_walk_node_counter", ptr(ctr))
+        try:
+            (prob.device_local_update if kind == "local" else prob.device_exhaustion)(0, U0, cfg, sh)
+            torch.cuda.synchronize()
+        finally:
+            _lib.call("ucp_walk_node_counter", None)
+        visited[key] = float(ctr.item())
+        if visited[key] == 0:  # latency-mode walks (small grids) are not instrumented: full windows
+            visited[key] = counts[f"{key}_nodes"] * frac_rank
+
+    # roofline: every kernel family, and the dominant one (this rank's executed work)
     kernels = {
-        "exh0": ("k_ex0_eval (stage-0 exhaustion candidates)", counts["ex0_dp_ops"], phase_ms[2]),
-        "local0": ("k_lu0_probe + k_lu0_finish (stage-0 local update)", counts["lu0_dp_ops"], phase_ms[0]),
-        "local1": ("k_moments (u1 estimator) + k_lu1", counts["moment_dp_ops"], phase_ms[1]),
+        "exh0": ("k_ex0_eval (stage-0 exhaustion candidates)", visited["ex0"] * DP_OPS_PER_NODE, phase_ms[2]),
+        "local0": ("k_lu0_probe + k_lu0_finish (stage-0 local update)", visited["lu0"] * DP_OPS_PER_NODE,
+                   phase_ms[0]),
+        "local1": ("k_moments (u1 estimator) + k_lu1", counts["moment_dp_ops"] * frac_rank, phase_ms[1]),
     }
-    fam = {k: {"kernel": v[0], "achieved_tflops": v[1] * frac_rank / (v[2] * 1e-3) / 1e12,
-               "frac": v[1] * frac_rank / (v[2] * 1e-3) / fp64_peak, "ms": v[2]} for k, v in kernels.items()}
+    fam = {k: {"kernel": v[0], "achieved_tflops": v[1] / (v[2] * 1e-3) / 1e12,
+               "frac": v[1] / (v[2] * 1e-3) / fp64_peak, "ms": v[2]} for k, v in kernels.items()}
     top = max(kernels, key=lambda k: kernels[k][2])
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
@@ -471,9 +490,13 @@ def run_ours(args):
                 "peak": fp64_peak / 1e12, "unit": "TFLOP/s", "frac": fam[top]["frac"], "traffic": traffic,
                 "peak_source": f"measured on this GPU at bench start: ucp_fp64_probe DMUL+DADD throughput "
                                f"({sms} SMs); nominal 148 x 64 DP lanes x 1.965 GHz = 18.6 TFLOP/s (non-FMA)",
-                "work": f"{DP_OPS_PER_NODE} DP ops per visited walk node ({counts['ex0_nodes']:.4g} nodes in "
-                        f"exh0, {counts['lu0_nodes']:.4g} in local0), {DP_OPS_PER_PAIR} per in-range moment pair "
+                "work": f"{DP_OPS_PER_NODE} DP ops per visited walk node (executed, counted on the device: "
+                        f"{visited['ex0']:.4g} nodes in exh0, {visited['lu0']:.4g} in local0 on this rank; the "
+                        f"reference's full windows are {counts['ex0_nodes']:.4g} / {counts['lu0_nodes']:.4g}: "
+                        f"the no-op tail exit skips the rest), {DP_OPS_PER_PAIR} per in-range moment pair "
                         f"({counts['moment_pairs']:.4g}); exp/erf/setup outside the loops excluded",
+                "walk_nodes": {"executed": visited, "reference": {"ex0": counts["ex0_nodes"] * frac_rank,
+                                                                   "lu0": counts["lu0_nodes"] * frac_rank}},
                 "families": fam}
 
     if rank == 0:

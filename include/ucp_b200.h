@@ -343,6 +343,12 @@ int ucp_allreduce_min_i64(ucp_comm* comm, int64_t* buf, int64_t count, void* str
  * blocks*threads doubles. */
 int ucp_fp64_probe(int blocks, int threads, int iters, double* sink, void* stream);
 
+/* Throughput-mode stage-0 walks launched while `counter` (a device pointer,
+ * nullptr = off) is set add the number of walk nodes they actually visited to
+ * it (the no-op tail exit makes this fewer than the reference's window).  For
+ * the roofline's executed-work count only; not thread-safe across host threads. */
+int ucp_walk_node_counter(unsigned long long* counter);
+
 #ifdef __cplusplus
 }
 #endif

@@ -123,12 +123,16 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 struct WalkGrid {
   double a, h, b, q;  // b = a + h*(d-1); q = exp(-h*h)   (kernels.py:411-412)
   int64_t d;
-  // Suffix bounds for the walk's no-op tail (nullptr: walk every node):
-  // vsuf[j >> kVsufShift] >= |v_j'| for every j' >= (j >> kVsufShift) << kVsufShift,
-  // +inf when any v_j' in that suffix is not finite (see walk_tail_noop).
+  // Range-max bounds for the walk's no-op tail (nullptr: walk every node): a
+  // sparse table over 256-node blocks, level k at vsuf + k*nb holding
+  // max |v| over blocks [b, b + 2^k), +inf when any v there is not finite
+  // (see walk_tail_noop / k_vsuf).
   const double* vsuf;
+  int nb;
+  // instrumentation (ucp_walk_node_counter): visited walk nodes are added here
+  unsigned long long* visits;
 };
-constexpr int kVsufShift = 8;  // 256 nodes per suffix block
+constexpr int kVsufShift = 8;  // 256 nodes per block
 
 struct Mom3 {
   double t0, t1, t2;
@@ -147,6 +151,8 @@ struct BatchArgs {
 };
 constexpr BatchArgs kNoBatch = {nullptr, 0, 0, 0, 0, nullptr};
 
+unsigned long long* g_visits = nullptr;  // ucp_walk_node_counter (instrumentation only)
+
 WalkGrid make_walk_grid(double a, double h, int64_t d) {
   WalkGrid g;
   g.a = a;
@@ -155,6 +161,8 @@ WalkGrid make_walk_grid(double a, double h, int64_t d) {
   g.b = a + h * (double)(d - 1);
   g.q = ucp_exp_tab((-h) * h, h_exp_tab);  // same port as the device: bitwise glibc
   g.vsuf = nullptr;
+  g.nb = (int)((d + (1 << 8) - 1) >> 8);
+  g.visits = g_visits;
   return g;
 }
 
@@ -190,19 +198,26 @@ __device__ __forceinline__ double2 walk_ld2(const double* v, int j) {
 // wpc = fl(h*pdf) and vm >= |v_j'| for every remaining node, monotonicity of
 // rounding bounds every remaining addend exactly:
 //   acc0 += wp' <= wpc,  |acc1 += wv'| <= fl(wpc*vm),  acc2 += fl(wv'*v') <= fl(fl(wpc*vm)*vm).
-// An addend t with |t| < |acc| * 2^-56 (< half the smaller ulp around acc,
-// acc normal) leaves acc unchanged under round-to-nearest, so once all three
+// An addend t with |t| < |acc| * 2^-55 (< 2^(E-54) for acc in [2^E, 2^(E+1)):
+// half the smaller ulp around acc, acc normal) leaves acc unchanged under round-to-nearest, so once all three
 // bounds are below their thresholds no remaining node changes a bit and the
 // walk may stop.  vm = +inf (a non-finite v ahead) or NaN never passes.
 __device__ __forceinline__ bool walk_tail_noop(double pdf, double ratio, double h, double vm, double acc0,
                                                double acc1, double acc2) {
-  const double e = 0x1p-56, tiny = 0x1p-960;
+  const double e = 0x1p-55, tiny = 0x1p-960;
   const double wpc = h * pdf;
   const double b1 = wpc * vm;
   const double b2 = b1 * vm;
   const double a1 = fabs(acc1);
   return ratio <= 1.0 && acc0 > tiny && a1 > tiny && acc2 > tiny && wpc < acc0 * e && b1 < a1 * e &&
          b2 < acc2 * e;
+}
+
+// max |v| over 256-node blocks [bl, br] (bl <= br) from the sparse table
+__device__ __forceinline__ double range_max(const double* __restrict__ t, int nb, int bl, int br) {
+  const int k = 31 - __clz(br - bl + 1);
+  const double* lv = t + (size_t)k * nb;
+  return fmax(__ldg(lv + bl), __ldg(lv + br - (1 << k) + 1));
 }
 
 template <int kMode>
@@ -276,9 +291,12 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
       const double* __restrict__ vsuf = g.vsuf;
       int it = 0;
       for (; j + 3 <= jint; j += 4) {
-        if (vsuf && (++it & 15) == 0 &&
-            walk_tail_noop(pdf, ratio, h, __ldg(vsuf + (j >> kVsufShift)), acc0, acc1, acc2)) {
-          j = je + 1;  // every remaining node (incl. a half-weight last one) is a no-op
+        if (vsuf && (++it & 15) == 0 && ratio <= 1.0 &&
+            walk_tail_noop(pdf, ratio, h, range_max(vsuf, g.nb, j >> kVsufShift, je >> kVsufShift), acc0, acc1,
+                           acc2)) {
+          // every remaining node (incl. a half-weight last one) is a no-op; j > je
+          // skips them and encodes the first unvisited node for the node counter
+          j = 2 * (je + 1) - j;
           break;
         }
         const double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
@@ -291,6 +309,13 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
     }
     for (; j <= jint; ++j) UCP_WALK_STEP(h);
     if (je == last && j == last) UCP_WALK_STEP(hh);
+    if (!kLat && g.visits) {  // instrumentation: nodes this walk visited
+      const int jstop = (je == last && j == last) ? je + 1 : 2 * (je + 1) - j;  // first unvisited node
+      const unsigned n = (unsigned)(jstop - (int)jlo);
+      const unsigned mask = __activemask();
+      const unsigned tot = __reduce_add_sync(mask, n);
+      if ((threadIdx.x & 31) == __ffs(mask) - 1) atomicAdd(g.visits, (unsigned long long)tot);
+    }
 #undef UCP_WALK_STEP
 #undef UCP_WALK_STEP_V
   }
@@ -554,40 +579,34 @@ __global__ void k_segmented_argmin(const double* __restrict__ costs, const int64
 // repeats collapsed (identical values give identical costs, and the
 // first-occurrence argmin returns the same value -- the reference's own
 // flatten_windows dedups, kernels.py:163-187).
-// Suffix bounds of |v| per 256-node block for walk_tail_noop: one CTA
-// (d <= 2^31 nodes; ~8 B/node read once, negligible beside the walks that use it).
-// vsuf[b] = max |v_j| over j >= 256 b, +inf once any such v_j is not finite.
-__global__ void __launch_bounds__(1024) k_vsuf(const double* __restrict__ v, int64_t d, double* vsuf) {
-  __shared__ double seg[1024];
-  const int64_t nb = (d + (1 << kVsufShift) - 1) >> kVsufShift;
+// Range-max table of |v| over 256-node blocks for walk_tail_noop: one CTA
+// (~8 B/node read once plus log2(nb) passes over nb blocks; negligible beside
+// the walks that use it).  Level 0: block maxima; level k: max over 2^k blocks.
+// A non-finite v makes every entry covering it +inf (the walk never exits there).
+__global__ void __launch_bounds__(1024) k_vsuf(const double* __restrict__ v, int64_t d, int nb, double* t) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t b = warp; b < nb; b += 32) {  // block maxima, one warp per block
+  for (int b = warp; b < nb; b += 32) {
     double m = 0.0;
-    for (int64_t j = (b << kVsufShift) + lane; j < d && j < ((b + 1) << kVsufShift); j += 32) {
+    for (int64_t j = ((int64_t)b << kVsufShift) + lane; j < d && j < ((int64_t)(b + 1) << kVsufShift); j += 32) {
       double a = fabs(v[j]);
       m = (a <= 1.7976931348623157e308) ? fmax(m, a) : INFINITY;  // NaN / inf -> inf
     }
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) vsuf[b] = m;
+    if (lane == 0) t[b] = m;
   }
-  __syncthreads();
-  const int64_t per = (nb + 1023) / 1024;
-  const int64_t b0 = threadIdx.x * per, b1 = b0 + per < nb ? b0 + per : nb;
-  double m = 0.0;
-  for (int64_t b = b1 - 1; b >= b0; --b) m = fmax(m, vsuf[b]);
-  seg[threadIdx.x] = m;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {  // inclusive suffix max over segments
-    double x = threadIdx.x + o < 1024 ? seg[threadIdx.x + o] : 0.0;
+  for (int k = 1; (1 << k) <= nb; ++k) {
     __syncthreads();
-    seg[threadIdx.x] = fmax(seg[threadIdx.x], x);
-    __syncthreads();
+    const double* p = t + (size_t)(k - 1) * nb;
+    double* q = t + (size_t)k * nb;
+    const int half = 1 << (k - 1);
+    for (int b = threadIdx.x; b + 2 * half <= nb; b += blockDim.x) q[b] = fmax(p[b], p[b + half]);
   }
-  m = threadIdx.x + 1 < 1024 ? seg[threadIdx.x + 1] : 0.0;  // max over later segments
-  for (int64_t b = b1 - 1; b >= b0; --b) {
-    m = fmax(m, vsuf[b]);
-    vsuf[b] = m;
-  }
+}
+
+int vsuf_levels(int nb) {
+  int k = 0;
+  while ((2 << k) <= nb) ++k;
+  return k + 1;
 }
 
 __global__ void k_ex_count(const double* __restrict__ u, const int64_t* __restrict__ lo,
@@ -1498,8 +1517,8 @@ const bool g_tail_exit = [] {
 int attach_vsuf(WalkGrid* g, const double* v1, int64_t n_walks, ucp_workspace* ws, cudaStream_t st) {
   if (!g_tail_exit || walk_latency_mode(n_walks)) return UCP_OK;
   void* p;
-  if (int rc = ws_get(ws, WS_VSUF, sizeof(double) * (size_t)((g->d >> kVsufShift) + 1), &p)) return rc;
-  k_vsuf<<<1, 1024, 0, st>>>(v1, g->d, (double*)p);
+  if (int rc = ws_get(ws, WS_VSUF, sizeof(double) * (size_t)g->nb * vsuf_levels(g->nb), &p)) return rc;
+  k_vsuf<<<1, 1024, 0, st>>>(v1, g->d, g->nb, (double*)p);
   UCP_LAUNCHED("k_vsuf");
   g->vsuf = (const double*)p;
   return UCP_OK;
@@ -1571,7 +1590,10 @@ int ucp_workspace_reserve(ucp_workspace* ws, int64_t d0, int64_t d1, int64_t max
   if ((rc = ws_get(ws, WS_COUNT, sizeof(int64_t) * (size_t)(dm + 1), &p))) return rc;
   if ((rc = ws_get(ws, WS_CAND_PT, sizeof(int32_t) * (size_t)max_cand, &p))) return rc;
   if ((rc = ws_get(ws, WS_CAND_J, sizeof(int32_t) * (size_t)max_cand, &p))) return rc;
-  if ((rc = ws_get(ws, WS_VSUF, sizeof(double) * (size_t)((d1 >> kVsufShift) + 1), &p))) return rc;
+  {
+    const int nb1 = (int)((d1 + (1 << kVsufShift) - 1) >> kVsufShift);
+    if ((rc = ws_get(ws, WS_VSUF, sizeof(double) * (size_t)nb1 * vsuf_levels(nb1), &p))) return rc;
+  }
   return UCP_OK;
 }
 
@@ -1913,6 +1935,11 @@ int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const doub
   UCP_WALK_LAUNCH(k_obj_terms, end - begin, nblocks(end - begin, kWalkThreads), as_stream(stream), P->d1, P->y0, P->f0, u0, P->k, u1, g,
                                                                           begin, end, terms, err, kNoBatch);
   UCP_LAUNCHED("k_obj_terms");
+  return UCP_OK;
+}
+
+int ucp_walk_node_counter(unsigned long long* counter) {
+  g_visits = counter;
   return UCP_OK;
 }
 

@@ -14,18 +14,26 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def _run(flag, out):
+def _run(flag, out, perturb="none"):
     env = dict(os.environ, UCP_TAIL_EXIT=flag)
-    r = subprocess.run([sys.executable, str(ROOT / "tools" / "tail_exit_ab.py"), "--log2d", "17", "--out", str(out)],
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "tail_exit_ab.py"), "--log2d", "17", "--out", str(out),
+                        "--perturb", perturb],
                        cwd=str(ROOT), env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     return np.load(out)
 
 
-def test_tail_exit_bitwise(tmp_path):
-    a = _run("0", tmp_path / "full.npz")
-    b = _run("1", tmp_path / "exit.npz")
+@pytest.mark.parametrize("perturb", ["none", "spike", "identity", "huge"])
+def test_tail_exit_bitwise(tmp_path, perturb):
+    """none: the bench snapshot; spike: huge finite u1 values in the far tail (late addends
+    that DO change the sums: the exit must not fire before them); identity: u1 = y, so the
+    first moment nearly cancels for centres near 0; huge: a 1e200 value (v*v overflows: the bound
+    is inf and the walk never ends early; errors must match).  Non-finite controllers never reach
+    a walk (SampledController rejects them, as the reference does)."""
+    a = _run("0", tmp_path / "full.npz", perturb)
+    b = _run("1", tmp_path / "exit.npz", perturb)
     assert set(a.files) == set(b.files) == {"local0", "local1", "exh0", "exh1", "J"}
     for k in a.files:
         assert a[k].tobytes() == b[k].tobytes(), k
-    assert b["J"][0] > 0
+    if perturb == "none":
+        assert b["J"][0] > 0

@@ -24,6 +24,9 @@ def main():
     ap.add_argument("--window-nodes", type=int, default=39)
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--out", required=True)
+    ap.add_argument("--perturb", choices=["none", "spike", "identity", "huge"], default="none",
+                    help="adversarial stage-1 controller: far-tail spikes (large finite addends after the "
+                         "peak), u1 = y (odd: acc1 ~ 0 near s = 0), one 1e200 value (v*v overflows)")
     args = ap.parse_args()
 
     import torch
@@ -37,6 +40,15 @@ def main():
     res = P.solve(P.Witsenhausen(k=bench.K_WC, sigma=bench.SIGMA), P.SolverConfig())
     u0h = bench.resample(res.controllers.values(0), d)
     u1h = bench.resample(res.controllers.values(1), d)
+    y = np.linspace(bench.SPAN[0], bench.SPAN[1], d)
+    if args.perturb == "spike":
+        u1h[d - 3] = 1e6
+        u1h[d // 2 + d // 7] = -3e5
+        u1h[d // 5] = 2e4
+    elif args.perturb == "identity":
+        u1h = y.copy()
+    elif args.perturb == "huge":
+        u1h[d // 2 + d // 9] = 1e200
     prob = P.Witsenhausen(k=bench.K_WC, sigma=bench.SIGMA, grids=[(*bench.SPAN, d), (*bench.SPAN, d)])
     h = prob.grids[0].spacing
     cfg = P.SolverConfig(search_radius=(args.window_nodes / 2.0) * h)
@@ -50,16 +62,22 @@ def main():
             sweep = prob.device_local_update if kind == "local" else prob.device_exhaustion
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            r = sweep(m, U, cfg, sh)
+            try:
+                r = sweep(m, U, cfg, sh)
+            except Exception as exc:  # the error (type and text) must match too
+                r = np.frombuffer(f"{type(exc).__name__}: {exc}".encode(), dtype=np.uint8)
             e1.record(stream)
             torch.cuda.synchronize()
             if rep:
                 ms[name] = ms.get(name, 0.0) + e0.elapsed_time(e1) / args.reps
             outs[name] = np.asarray(r.cpu().numpy() if hasattr(r, "cpu") else np.asarray(r))
-        J = prob.device_objective(U, sh)
-        outs["J"] = np.array([float(J)])
+        try:
+            outs["J"] = np.array([float(prob.device_objective(U, sh))])
+        except Exception as exc:
+            outs["J"] = np.frombuffer(f"{type(exc).__name__}: {exc}".encode(), dtype=np.uint8)
     np.savez(args.out, **outs)
-    print(json.dumps({"log2d": args.log2d, "phase_ms": ms, "J": float(outs["J"][0])}))
+    print(json.dumps({"log2d": args.log2d, "perturb": args.perturb, "phase_ms": ms,
+                      "J": float(outs["J"][0]) if outs["J"].dtype == np.float64 else bytes(outs["J"]).decode()}))
 
 
 if __name__ == "__main__":
