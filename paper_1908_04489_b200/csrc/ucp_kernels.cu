@@ -289,9 +289,19 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
       }
     } else {
       const double* __restrict__ vsuf = g.vsuf;
-      int it = 0;
-      for (; j + 3 <= jint; j += 4) {
-        if (vsuf && (++it & 15) == 0 && ratio <= 1.0 &&
+      // 64-node chunks with a counter-free inner loop; the tail check runs
+      // between chunks (any check point is result-invariant)
+      while (j + 63 <= jint) {
+#pragma unroll 2
+        for (int c = 0; c < 16; ++c, j += 4) {
+          const double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
+          const double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
+          UCP_WALK_STEP_V(h, p0.x);
+          UCP_WALK_STEP_V(h, p0.y);
+          UCP_WALK_STEP_V(h, p1.x);
+          UCP_WALK_STEP_V(h, p1.y);
+        }
+        if (vsuf && ratio <= 1.0 && j <= jint &&
             walk_tail_noop(pdf, ratio, h, range_max(vsuf, g.nb, j >> kVsufShift, je >> kVsufShift), acc0, acc1,
                            acc2)) {
           // every remaining node (incl. a half-weight last one) is a no-op; j > je
@@ -299,6 +309,8 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
           j = 2 * (je + 1) - j;
           break;
         }
+      }
+      for (; j + 3 <= jint; j += 4) {
         const double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
         const double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
         UCP_WALK_STEP_V(h, p0.x);
