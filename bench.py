@@ -42,10 +42,20 @@ METRIC = "marginal-cost evals/sec & time-to-converge (s), Witsenhausen k=0.2 σ=
 K_WC, SIGMA = 0.2, 5.0
 SPAN = (-25.0, 25.0)
 C1_D = 2000
+C1_SOLVES = 7
+PAPER_SOLVES = 3
+C4_SWEEPS = 3
 DP_OPS_PER_NODE = 8  # kernels.py:430-439: 3 mul + 3 add accumulate, 2 mul recurrence
-# kernels.py:466-482 per in-range pair: sub, 2 compares, 2 mul, exp (12 DP on the glibc
-# FMA3 path), *factor, *INV, != 0, *w, 3 add, 2 mul
-DP_OPS_PER_PAIR = 27
+# kernels.py:466-482 per in-cutoff pair: sub, 2 compares, 2 mul (-0.5*diff*diff), exp (12 DP
+# instructions in the device port of glibc's __exp_fma: 8 FMA + 1 sub + 1 add + 2 mul),
+# *factor, *INV, != 0, *w, 3 add, 2 mul (wp*x, (wp*x)*x) = 26; out of the cutoff: sub +
+# compares = 3
+DP_OPS_PER_PAIR = 26
+DP_OPS_PER_PAIR_OUT = 3
+# FP64-pipe instructions k_moments executes per in-cutoff pair (ncu
+# sm__sass_thread_inst_executed_op_fp64_pred_on.sum = 6.634e11 over 2.875e10 in-cutoff pairs at 2^18,
+# profiles/r2_fp64_inst_2p18.csv)
+DP_INST_PER_PAIR_EXEC = 23.07
 
 
 def parse():
@@ -192,26 +202,42 @@ def cpu_step_seconds(orc, p, u0, u1, d, r, target_s, cand_per_point=1.0):
     n_obj = int(np.clip(per * node_rate / W, 16, d))
     rng = np.random.default_rng(0)
     pick = lambda n: np.sort(rng.choice(d, n, replace=False)).astype(np.int64)  # noqa: E731
-    times = {}
-    t = time.perf_counter()
-    orc.local_update_phase(p, 0, u0, u1, cfg, points=pick(n_lu0))
-    times["local0"] = (time.perf_counter() - t) * d / n_lu0
-    t = time.perf_counter()
-    orc.local_update_phase(p, 1, u0, u1, cfg, points=pick(n_lu1))
-    times["local1"] = (time.perf_counter() - t) * d / n_lu1
-    t = time.perf_counter()
-    orc.partial_exhaustion_phase(p, 0, u0, u1, cfg, points=pick(n_ex0))
-    times["exh0"] = (time.perf_counter() - t) * d / n_ex0
-    t = time.perf_counter()
-    orc.partial_exhaustion_phase(p, 1, u0, u1, cfg, points=pick(n_ex1))
-    times["exh1"] = (time.perf_counter() - t) * d / n_ex1
-    t = time.perf_counter()
-    idx = pick(n_obj)
-    p.cost_batch(0, u0[idx], idx, u0, u1)
-    times["objective"] = (time.perf_counter() - t) * d / n_obj
-    sample = (f"points sampled per phase: local0={n_lu0}, local1={n_lu1}, exh0={n_ex0}, exh1={n_ex1}, "
-              f"objective={n_obj} of {d}; time extrapolated x d/n")
-    return sum(times.values()), times, thr, sample
+    times, outs = {}, {}
+
+    def run(name, n, fn):
+        idx = pick(n)
+        if name != "objective":  # the grid ends are the edge cases of every phase
+            idx[0], idx[-1] = 0, d - 1
+            idx = np.unique(idx)
+        t = time.perf_counter()
+        outs[name] = (idx, fn(idx))
+        times[name] = (time.perf_counter() - t) * d / idx.size
+
+    run("local0", n_lu0, lambda i: orc.local_update_phase(p, 0, u0, u1, cfg, points=i))
+    run("local1", n_lu1, lambda i: orc.local_update_phase(p, 1, u0, u1, cfg, points=i))
+    run("exh0", n_ex0, lambda i: orc.partial_exhaustion_phase(p, 0, u0, u1, cfg, points=i))
+    run("exh1", n_ex1, lambda i: orc.partial_exhaustion_phase(p, 1, u0, u1, cfg, points=i))
+    run("objective", n_obj, lambda i: p.cost_batch(0, u0[i], i, u0, u1))
+    sample = (f"points sampled per phase: " + ", ".join(f"{k}={v[0].size}" for k, v in outs.items())
+              + f" of {d}; time extrapolated x d/n")
+    return sum(times.values()), times, thr, sample, outs
+
+
+def parity_vs_oracle(outs, gpu, J, orc, h):
+    """Bitwise mismatches of the GPU step against the oracle's outputs on the
+    sampled points (the cpu_baseline leg's own results): the four phases, the
+    objective integrand, and J re-summed from the device integrand by the
+    oracle's serial trapezoid (kernels.py:136-144)."""
+    par = {}
+    for name, (idx, want) in outs.items():
+        got = gpu[name][idx]
+        par[name] = int(np.count_nonzero(got.view(np.uint64) != np.ascontiguousarray(want, np.float64).view(np.uint64)))
+    par["J_from_terms"] = int(np.float64(orc.trapezoid_sum(gpu["objective"], h)).view(np.uint64)
+                              != np.float64(J).view(np.uint64))
+    par["points"] = {name: int(idx.size) for name, (idx, _) in outs.items()}
+    par["what"] = ("bitwise mismatches, GPU step vs the oracle (reference-order C restatement, pinned to the "
+                   "reference's goldens) on the cpu_baseline sample points, grid ends included")
+    return par
 
 
 def c1_oracle_solve(orc):
@@ -241,7 +267,7 @@ def run_reference(args):
         cpu_step_seconds(orc, p, u0, u1, d, r, per_step / 4, cpp)
     steps, last = [], None
     for _ in range(args.steps):
-        tot, times, thr, sample = cpu_step_seconds(orc, p, u0, u1, d, r, per_step, cpp)
+        tot, times, thr, sample, _ = cpu_step_seconds(orc, p, u0, u1, d, r, per_step, cpp)
         steps.append(tot)
         last = (times, thr, sample)
     sec = float(np.mean(steps))
@@ -285,6 +311,9 @@ def run_ours(args):
     dev = torch.device("cuda", local_rank)
     if world > 1:
         if args.backend == "nccl":
+            # communicator init lines (ranks, NVLS/P2P transport) in the log, so every rank is checkable
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(args.backend)
@@ -295,33 +324,44 @@ def run_ours(args):
     sh = P.from_process_group() if world > 1 else P.LOCAL
     d = 1 << args.log2d
 
-    # time-to-converge at the default grid (C1) on the GPU(s); it also gives the snapshot
-    # one round on a throw-away problem first: lazy module loading and the first
-    # launch of every kernel the solve uses are one-time process costs
+    # time-to-converge at the default grid (C1) on the GPU(s); it also gives the snapshot.
+    # One round on a throw-away problem first (lazy module loading and the first launch
+    # of every kernel are one-time process costs), then C1_SOLVES solves, each of a fresh
+    # problem (new device context, graph captures included) as a user would run them:
+    # median, min and max reported.  At N>1 the small solves run as replicas on every rank
+    # (a d=2000 phase is latency-bound: sharding it only adds collectives).
     warm = P.Witsenhausen(k=K_WC, sigma=SIGMA)
-    P.solve(warm, P.SolverConfig(max_rounds=1), sharding=sh)
-    c1p = P.Witsenhausen(k=K_WC, sigma=SIGMA)
-    c1p.objective(c1p.identity_controllers())  # context creation
-    gc.collect()  # no collector pass (or context teardown) inside a timed region
-    torch.cuda.synchronize()
-    t = time.perf_counter()
-    res = P.solve(c1p, P.SolverConfig(), sharding=sh)
-    torch.cuda.synchronize()
-    c1 = {"config": f"d={C1_D} default SolverConfig, identity init", "wall_s": time.perf_counter() - t,
+    P.solve(warm, P.SolverConfig(max_rounds=1))
+
+    def timed_solves(make, n):
+        walls, res = [], None
+        for _ in range(n):
+            pr = make()
+            pr.objective(pr.identity_controllers())  # context creation (allocations) outside the clock
+            gc.collect()  # no collector pass (or context teardown) inside a timed region
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            res = P.solve(pr, P.SolverConfig())
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t)
+            del pr
+        return res, {"wall_s": float(np.median(walls)), "wall_s_min": min(walls), "wall_s_max": max(walls),
+                     "solves": n, "walls_s": [round(w, 5) for w in walls]}
+
+    res, c1w = timed_solves(lambda: P.Witsenhausen(k=K_WC, sigma=SIGMA), C1_SOLVES)
+    c1 = {"config": f"d={C1_D} default SolverConfig, identity init; median of {C1_SOLVES} solves of fresh "
+                    "problems" + (" (replica on every rank)" if world > 1 else ""), **c1w,
           "rounds": res.total_rounds, "J": res.final_objective, "termination": res.termination}
     u0h, u1h = resample(res.controllers.values(0), d), resample(res.controllers.values(1), d)
     # the paper's grid size (d=14000): the reference needs 1,437 s on 8 cores
-    pp = P.Witsenhausen(k=K_WC, sigma=SIGMA, grids=[(*SPAN, 14000), (*SPAN, 14000)])
-    gc.collect()
-    torch.cuda.synchronize()
-    t = time.perf_counter()
-    rp = P.solve(pp, P.SolverConfig(), sharding=sh)
-    torch.cuda.synchronize()
-    paper = {"config": "d=14000 (paper size) default SolverConfig, identity init",
-             "wall_s": time.perf_counter() - t, "rounds": rp.total_rounds, "J": rp.final_objective,
+    rp, pw = timed_solves(lambda: P.Witsenhausen(k=K_WC, sigma=SIGMA, grids=[(*SPAN, 14000), (*SPAN, 14000)]),
+                          PAPER_SOLVES)
+    paper = {"config": f"d=14000 (paper size) default SolverConfig, identity init; median of {PAPER_SOLVES} "
+                       "solves" + (" (replica on every rank)" if world > 1 else ""), **pw,
+             "rounds": rp.total_rounds, "J": rp.final_objective,
              "termination": rp.termination, "reference_cpu_s": 1437.4,
              "reference_cpu": "numba reference, 8-core Xeon (SURVEY.md Appendix B)"}
-    del pp, rp
+    del rp
     # config 4: 64 independent instances (k in [0.05, 1], sigma in {3, 5, 7}) at d=2000 to
     # convergence -- the batched engine (one kernel over (instance, point) per step);
     # instances k % world per rank ("replicas only")
@@ -329,21 +369,26 @@ def run_ours(args):
     # first launches of the batched kernels and the engine for this shape (a
     # reusable resource, cached per shape like a workspace)
     P.solve_many([P.Witsenhausen(k=k, sigma=s_) for k, s_ in sweep], P.SolverConfig(max_rounds=1), sharding=sh)
-    sprobs = [P.Witsenhausen(k=k, sigma=s_) for k, s_ in sweep]
-    gc.collect()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t = time.perf_counter()
-    sres = P.solve_many(sprobs, P.SolverConfig(), sharding=sh)
-    torch.cuda.synchronize()
-    swall = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(swall, op=dist.ReduceOp.MAX)
-    swall = float(swall.item())
+    swalls = []
+    for _ in range(C4_SWEEPS):
+        sprobs = [P.Witsenhausen(k=k, sigma=s_) for k, s_ in sweep]
+        gc.collect()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        sres = P.solve_many(sprobs, P.SolverConfig(), sharding=sh)
+        torch.cuda.synchronize()
+        sw = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(sw, op=dist.ReduceOp.MAX)
+        swalls.append(float(sw.item()))
+    swall = float(np.median(swalls))
     config4 = {"config": "64 Witsenhausen instances, k = 0.05 + 0.95 i/63, sigma = (3, 5, 7)[i % 3], d=2000, "
-                         "default SolverConfig, to convergence; instances k % world per rank",
-               "wall_s": swall, "solves_per_s": 64 / swall, "engine": "batched (csrc/ucp_batch.cuh)",
+                         f"default SolverConfig, to convergence; instances k % world per rank; median of "
+                         f"{C4_SWEEPS} sweeps (max over ranks each)",
+               "wall_s": swall, "wall_s_min": min(swalls), "wall_s_max": max(swalls),
+               "solves_per_s": 64 / swall, "engine": "batched (csrc/ucp_batch.cuh)",
                "rounds_max": max(r.total_rounds for r in sres if r is not None),
                "reference_cpu_s_per_instance": 7.5,
                "reference_cpu": "oracle port on 16 cores, profiles/r1_sweep_c4.json"}
@@ -469,16 +514,40 @@ def run_ours(args):
         if visited[key] == 0:  # latency-mode walks (small grids) are not instrumented: full windows
             visited[key] = counts[f"{key}_nodes"] * frac_rank
 
-    # roofline: every kernel family, and the dominant one (this rank's executed work)
+    # the step's outputs on the host (one untimed step on the same snapshot): the
+    # parity check against the oracle's results on the cpu_baseline sample points
+    outs_dev, J_dev = step(U0)
+    gpu_out = {name: o.cpu().numpy() for (name, _, _), o in zip(PHASES, outs_dev)}
+    gpu_out["objective"] = prob.device_objective_terms(U0, sh).cpu().numpy()
+
+    # roofline: every kernel family, and the dominant one.  Two work counts per
+    # family (this rank's share): "algorithmic" = SURVEY.md §8(d)'s per-unit figure
+    # over the reference's full windows / all pairs; "executed" = what the kernels
+    # actually ran (walk nodes counted on the device: the no-op tail exit skips the
+    # rest; moment pairs inside the cutoff, FP64 instructions per pair from ncu).
+    # Two denominators: the nominal FP64 issue rate SMs x 64 x the SM clock sampled
+    # during the timed region (§8(d)), and the DMUL/DADD probe measured above.
+    clk_mhz = clk.get("sm_mhz") or 1965.0
+    p_nominal = sms * 64 * clk_mhz * 1e6
+    mom_pairs = counts["moment_pairs"] * frac_rank
+    mom_all = float(d) * float(d) * frac_rank
     kernels = {
-        "exh0": ("k_ex0_eval (stage-0 exhaustion candidates)", visited["ex0"] * DP_OPS_PER_NODE, phase_ms[2]),
-        "local0": ("k_lu0_probe + k_lu0_finish (stage-0 local update)", visited["lu0"] * DP_OPS_PER_NODE,
-                   phase_ms[0]),
-        "local1": ("k_moments (u1 estimator) + k_lu1", counts["moment_dp_ops"] * frac_rank, phase_ms[1]),
+        "exh0": ("k_ex0_eval (stage-0 exhaustion candidates)", phase_ms[2],
+                 counts["ex0_nodes"] * frac_rank * DP_OPS_PER_NODE, visited["ex0"] * DP_OPS_PER_NODE),
+        "local0": ("k_lu0_probe + k_lu0_finish (stage-0 local update)", phase_ms[0],
+                   counts["lu0_nodes"] * frac_rank * DP_OPS_PER_NODE, visited["lu0"] * DP_OPS_PER_NODE),
+        "local1": ("k_moments (u1 estimator) + k_lu1", phase_ms[1],
+                   mom_pairs * DP_OPS_PER_PAIR + (mom_all - mom_pairs) * DP_OPS_PER_PAIR_OUT,
+                   mom_pairs * DP_INST_PER_PAIR_EXEC),
     }
-    fam = {k: {"kernel": v[0], "achieved_tflops": v[1] / (v[2] * 1e-3) / 1e12,
-               "frac": v[1] / (v[2] * 1e-3) / fp64_peak, "ms": v[2]} for k, v in kernels.items()}
-    top = max(kernels, key=lambda k: kernels[k][2])
+    fam = {}
+    for k, (kname, ms_k, alg, exe) in kernels.items():
+        s_k = ms_k * 1e-3
+        fam[k] = {"kernel": kname, "ms": ms_k, "ops_algorithmic": alg, "ops_executed": exe,
+                  "tflops_algorithmic": alg / s_k / 1e12, "tflops_executed": exe / s_k / 1e12,
+                  "frac_algorithmic": alg / s_k / p_nominal, "frac_executed": exe / s_k / p_nominal,
+                  "frac_algorithmic_probe": alg / s_k / fp64_peak, "frac_executed_probe": exe / s_k / fp64_peak}
+    top = max(kernels, key=lambda k: kernels[k][1])
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
@@ -486,22 +555,30 @@ def run_ours(args):
             traffic = json.loads(prof.read_text()).get(f"dram_bytes_per_launch_2p{args.log2d}", {}).get(top)
         except Exception:
             traffic = None
-    roofline = {"bound": "fp64", "kernel": kernels[top][0], "achieved": fam[top]["achieved_tflops"],
-                "peak": fp64_peak / 1e12, "unit": "TFLOP/s", "frac": fam[top]["frac"], "traffic": traffic,
-                "peak_source": f"measured on this GPU at bench start: ucp_fp64_probe DMUL+DADD throughput "
-                               f"({sms} SMs); nominal 148 x 64 DP lanes x 1.965 GHz = 18.6 TFLOP/s (non-FMA)",
-                "work": f"{DP_OPS_PER_NODE} DP ops per visited walk node (executed, counted on the device: "
-                        f"{visited['ex0']:.4g} nodes in exh0, {visited['lu0']:.4g} in local0 on this rank; the "
-                        f"reference's full windows are {counts['ex0_nodes']:.4g} / {counts['lu0_nodes']:.4g}: "
-                        f"the no-op tail exit skips the rest), {DP_OPS_PER_PAIR} per in-range moment pair "
-                        f"({counts['moment_pairs']:.4g}); exp/erf/setup outside the loops excluded",
+    roofline = {"bound": "fp64", "kernel": kernels[top][0], "achieved": fam[top]["tflops_algorithmic"],
+                "peak": p_nominal / 1e12, "unit": "TFLOP/s", "frac": fam[top]["frac_algorithmic"],
+                "frac_executed": fam[top]["frac_executed"],
+                "frac_algorithmic_probe": fam[top]["frac_algorithmic_probe"],
+                "frac_executed_probe": fam[top]["frac_executed_probe"], "traffic": traffic,
+                "peak_source": f"nominal FP64 issue rate {sms} SMs x 64 DP lanes x {clk_mhz:.0f} MHz (median SM "
+                               f"clock sampled during the timed region; SURVEY.md §8(d)); probe = ucp_fp64_probe "
+                               f"DMUL+DADD throughput measured on this GPU at bench start: "
+                               f"{fp64_peak / 1e12:.3f} T instr/s",
+                "work": f"achieved/frac = algorithmic work (SURVEY.md §8(d)): {DP_OPS_PER_NODE} DP ops per node of "
+                        f"the reference's full clamped walk windows ({counts['ex0_nodes']:.4g} nodes in exh0, "
+                        f"{counts['lu0_nodes']:.4g} in local0); frac_executed counts the nodes the kernels walked "
+                        f"(device counter: {visited['ex0']:.4g} / {visited['lu0']:.4g} on this rank; the no-op tail "
+                        f"exit skips the rest, result-invariant). Moments: {DP_OPS_PER_PAIR} DP ops per in-cutoff "
+                        f"pair + {DP_OPS_PER_PAIR_OUT} per out-of-cutoff pair algorithmic, {DP_INST_PER_PAIR_EXEC} "
+                        f"FP64 instructions per in-cutoff pair executed (ncu, profiles/README.md); exp/erf/setup "
+                        f"outside the loops excluded",
                 "walk_nodes": {"executed": visited, "reference": {"ex0": counts["ex0_nodes"] * frac_rank,
                                                                    "lu0": counts["lu0_nodes"] * frac_rank}},
                 "families": fam}
 
     if rank == 0:
         value = counts["evals"] / (ms_step * 1e-3)
-        cpu = None
+        cpu, parity = None, None
         if not args.no_cpu_baseline and world == 1:
             from oracle import oracle as orc
 
@@ -509,16 +586,28 @@ def run_ours(args):
             orc.set_threads(os.cpu_count() or 1)
             p = orc.OracleWitsenhausen(k=K_WC, sigma=SIGMA, grid0=(*SPAN, d), grid1=(*SPAN, d),
                                        f0=prob._f0, fw0=prob._fw0)
-            sec, times, thr, sample = cpu_step_seconds(orc, p, u0h, u1h, d, cfg.radius_for(prob.grids[0]),
-                                                       args.cpu_seconds, counts["cand0"] / d)
+            sec, times, thr, sample, orc_out = cpu_step_seconds(orc, p, u0h, u1h, d, cfg.radius_for(prob.grids[0]),
+                                                                args.cpu_seconds, counts["cand0"] / d)
             cpu = {"value": counts["evals"] / sec, "unit": "evals/s", "cores": thr, "kind": "port",
                    "sample": sample, "step_s_extrapolated": sec, "phase_s": times,
                    "host": orc.host_cpu_description()}
+            parity = parity_vs_oracle(orc_out, gpu_out, J_dev, orc, prob.grids[0].spacing)
+        elif not args.no_cpu_baseline:
+            # N>1: the same check on a smaller sample (parity only; the CPU baseline is an N=1 figure)
+            from oracle import oracle as orc
+
+            orc.build()
+            orc.set_threads(os.cpu_count() or 1)
+            p = orc.OracleWitsenhausen(k=K_WC, sigma=SIGMA, grid0=(*SPAN, d), grid1=(*SPAN, d),
+                                       f0=prob._f0, fw0=prob._fw0)
+            *_, orc_out = cpu_step_seconds(orc, p, u0h, u1h, d, cfg.radius_for(prob.grids[0]),
+                                           min(args.cpu_seconds, 3.0), counts["cand0"] / d)
+            parity = parity_vs_oracle(orc_out, gpu_out, J_dev, orc, prob.grids[0].spacing)
         line = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(args, d, counts),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
+            "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "phase_ms": dict(zip(["local0", "local1", "exh0", "exh1", "objective"], phase_ms.round(3).tolist())),
             "time_to_converge": c1, "time_to_converge_paper_size": paper, "config4_sweep": config4,
             "gpu": torch.cuda.get_device_name(dev),

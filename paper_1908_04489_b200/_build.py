@@ -14,7 +14,10 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libucp_b200.so"
 SOURCES = [CSRC / "ucp_kernels.cu"]
-HEADERS = [CSRC / "ucp_libm.h", CSRC / "ucp_exp_data.h", CSRC / "ucp_config5.cuh", PKG.parent / "include" / "ucp_b200.h"]
+# every file ucp_kernels.cu includes: an edit to any of them rebuilds the library
+HEADERS = sorted(CSRC.glob("*.h")) + sorted(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "ucp_b200.h"]
+# stress build (tests/test_gpu_stress.py): schedule jitter + device index checks
+STRESS_LIB = PKG / "libucp_b200_stress.so"
 
 NVCC_FLAGS = [
     "-O3",
@@ -34,17 +37,18 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def stale() -> bool:
-    if not LIB.exists():
+def stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
-    return any(p.stat().st_mtime > t for p in SOURCES + HEADERS)
+    t = lib.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in SOURCES + HEADERS + [Path(__file__)])
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not stale():
-        return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, *(str(s) for s in SOURCES), "-o", str(LIB) + ".tmp"]
+def build(force: bool = False, verbose: bool = False, lib: Path = LIB, defines: tuple = ()) -> Path:
+    """nvcc the library to ``lib`` (``defines``: extra -D macros for variant builds)."""
+    if not force and not stale(lib):
+        return lib
+    cmd = [nvcc(), *NVCC_FLAGS, *(f"-D{x}" for x in defines), *(str(s) for s in SOURCES), "-o", str(lib) + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -52,10 +56,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{res.stdout}\n{res.stderr}")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(str(LIB) + ".tmp", LIB)
-    return LIB
+    os.replace(str(lib) + ".tmp", lib)
+    return lib
+
+
+def build_stress(force: bool = False) -> Path:
+    return build(force=force, lib=STRESS_LIB, defines=("UCP_STRESS",))
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--stress" in sys.argv:
+        print(build_stress(force="--force" in sys.argv))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB)

@@ -110,12 +110,13 @@ __global__ void __launch_bounds__(kCandThreads) k_bex_fill(const double* __restr
     for (unsigned c = 0; c < blockIdx.x; ++c) base += chunk_tot[(int64_t)slot * gridDim.x + c];
     s_base = base;
   }
-  __syncthreads();
+  UCP_SYNC();
   const int64_t i = (int64_t)blockIdx.x * kCandThreads + threadIdx.x;
   const int64_t c = i < d0 ? counts[(int64_t)slot * d0 + i] : 0;
   int64_t pos, agg;
   Scan(tmp).ExclusiveSum(c, pos, agg);
   pos += s_base;
+  UCP_DCHECK(pos + c <= B.sslot);
   if (i < d0) {
     offs[i] = pos;
     const int64_t j0 = lo[i];

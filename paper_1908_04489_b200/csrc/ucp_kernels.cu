@@ -35,6 +35,45 @@
 
 namespace {
 
+// Stress build (-DUCP_STRESS; tools/stress_build.py, tests/test_gpu_stress.py):
+// compute-sanitizer is closed on this pool, so races are shaken out by
+// delaying a pseudo-random eighth of the threads (up to ~2 us, seeded by the
+// clock) around every barrier, mbarrier wait, bulk-copy issue and work-queue
+// fetch, and index invariants are checked with device traps.  Results must
+// stay bitwise equal to the oracle under any schedule.  Both macros compile
+// to nothing in the production build.
+#ifdef UCP_STRESS
+__device__ __forceinline__ void ucp_jitter(unsigned site) {
+  unsigned x = (unsigned)clock64() ^ (threadIdx.x * 0x9E3779B9u) ^ (blockIdx.x * 0x85EBCA6Bu) ^
+               (blockIdx.y * 0x27D4EB2Fu) ^ (site * 0xC2B2AE35u);
+  x ^= x >> 15;
+  x *= 0x2C1B3C6Du;
+  x ^= x >> 12;
+  x *= 0x297A2D39u;
+  x ^= x >> 15;
+  if ((x & 7u) == 0u) __nanosleep((x >> 16) & 2047u);
+}
+#define UCP_JITTER() ucp_jitter(__LINE__)
+#define UCP_DCHECK(cond)                                                                        \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("UCP_DCHECK failed: %s at %s:%d (block %d,%d thread %d)\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);                               \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define UCP_JITTER() ((void)0)
+#define UCP_DCHECK(cond) ((void)0)
+#endif
+// __syncthreads with the stress build's jitter on both sides
+#define UCP_SYNC()      \
+  do {                  \
+    UCP_JITTER();       \
+    __syncthreads();    \
+    UCP_JITTER();       \
+  } while (0)
+
 constexpr double kGaussCut = 12.0;  // kernels.py:55 GAUSS_CUT
 // Walk kernels (one serial Gaussian walk per thread): 128-thread CTAs, at
 // least 12 resident per SM (<= 42 registers) so 12 warps per scheduler hide
@@ -321,6 +360,7 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
     }
     for (; j <= jint; ++j) UCP_WALK_STEP(h);
     if (je == last && j == last) UCP_WALK_STEP(hh);
+    UCP_DCHECK(jlo >= 0 && je <= last && j >= jint + 1 && j <= je + 1 + (int)(je - jlo + 1));
     if (!kLat && g.visits) {  // instrumentation: nodes this walk visited
       const int jstop = (je == last && j == last) ? je + 1 : 2 * (je + 1) - j;  // first unvisited node
       const unsigned n = (unsigned)(jstop - (int)jlo);
@@ -370,7 +410,7 @@ __device__ __forceinline__ void flag_min(int64_t* slot, int64_t i) {
     extern __shared__ __align__(16) double ucp_sv_[];               \
     for (int r_ = threadIdx.x; r_ < (int)(D); r_ += blockDim.x)    \
       ucp_sv_[r_] = V[r_];                                          \
-    __syncthreads();                                                \
+    UCP_SYNC();                                                \
     V = ucp_sv_;                                                    \
   }
 
@@ -607,7 +647,7 @@ __global__ void __launch_bounds__(1024) k_vsuf(const double* __restrict__ v, int
     if (lane == 0) t[b] = m;
   }
   for (int k = 1; (1 << k) <= nb; ++k) {
-    __syncthreads();
+    UCP_SYNC();
     const double* p = t + (size_t)(k - 1) * nb;
     double* q = t + (size_t)k * nb;
     const int half = 1 << (k - 1);
@@ -646,6 +686,7 @@ __global__ void k_ex_fill(const double* __restrict__ u, const int64_t* __restric
   int64_t i = begin + t;
   int64_t pos = offs[t];
   int64_t j0 = lo[i];
+  UCP_DCHECK(j0 >= 0 && j0 <= hi[i] && offs[t + 1] - pos >= 1);
   double prev = u[j0];
   cand_pt[pos] = (int32_t)i;
   cand_j[pos] = (int32_t)j0;
@@ -659,6 +700,7 @@ __global__ void k_ex_fill(const double* __restrict__ u, const int64_t* __restric
     }
     prev = x;
   }
+  UCP_DCHECK(pos == offs[t + 1]);
 }
 
 // Warp-per-point form of k_ex_fill (same candidates, same order): lane l of
@@ -688,6 +730,7 @@ __global__ void k_ex_fill_warp(const double* __restrict__ u, const int64_t* __re
     }
     pos += __popc(mask);
   }
+  UCP_DCHECK(pos == offs[t + 1]);
 }
 
 template <int kMode, bool kBatch = false>
@@ -737,6 +780,7 @@ __global__ void k_ex_argmin(const double* __restrict__ u, const double* __restri
     err += b * B.serr;
   }
   int64_t lo = offs[t], hi = offs[t + 1];
+  UCP_DCHECK(hi > lo);
   int64_t best = lo;
   double bv = costs[lo];
   bool ok = finite(bv);
@@ -778,7 +822,7 @@ __global__ void k_x1_prepare(const double* __restrict__ y0, const double* __rest
   }
   __shared__ int snan;
   if (threadIdx.x == 0) snan = 0;
-  __syncthreads();
+  UCP_SYNC();
   int64_t i = (int64_t)blockIdx.x * kTile + threadIdx.x;
   double x = 0.0, mn = INFINITY, mx = -INFINITY;
   if (i < d0) {
@@ -793,13 +837,13 @@ __global__ void k_x1_prepare(const double* __restrict__ y0, const double* __rest
   }
   smin[threadIdx.x] = mn;
   smax[threadIdx.x] = mx;
-  __syncthreads();
+  UCP_SYNC();
   for (int s = kTile / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) {
       smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + s]);
       smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
     }
-    __syncthreads();
+    UCP_SYNC();
   }
   if (threadIdx.x == 0)
     tile_mm[blockIdx.x] = snan ? make_double2(-INFINITY, INFINITY) : make_double2(smin[0], smax[0]);
@@ -827,9 +871,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra UCP_MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+  UCP_JITTER();  // a late reader: the refill of the other buffer must not overtake it
 }
 // global -> shared bulk copy completing on `bar` (bytes % 16 == 0, 16-B aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  UCP_JITTER();
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
@@ -890,7 +936,7 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
     mbar_init(&sbar[1], 1);
     mbar_init_fence();
   }
-  __syncthreads();
+  UCP_SYNC();
   uint32_t phase0 = 0, phase1 = 0;  // completions seen per barrier (parity), CTA-uniform
   const double2* xw0 = xw;
   const double2* tails0 = tails;
@@ -908,6 +954,7 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
       slot = r / per;
       qb = 1 + r % per;
     }
+    UCP_DCHECK(slot >= 0 && slot < nslots && qb >= 0 && qb < nqb);
     xw = xw0 + slot * ntiles * kTile;
     tails = tails0 + slot * m;
     tile_mm = tile_mm0 + slot * ntiles;
@@ -928,14 +975,14 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
       ymin = fmin(ymin, __shfl_xor_sync(0xffffffffu, ymin, off));
       ymax = fmax(ymax, __shfl_xor_sync(0xffffffffu, ymax, off));
     }
-    __syncthreads();
+    UCP_SYNC();
     if ((threadIdx.x & 31) == 0) {
       s_ymin[threadIdx.x >> 5] = ymin;
       s_ymax[threadIdx.x >> 5] = ymax;
     }
     if (at_left) atomicOr(&s_left, 1);
     if (at_right) atomicOr(&s_right, 1);
-    __syncthreads();
+    UCP_SYNC();
     ymin = s_ymin[0];
     ymax = s_ymax[0];
     for (int r = 1; r < kQT / 32; ++r) {
@@ -967,6 +1014,7 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
       }
       while (tile < ntiles) {
         const int64_t nxt = next_tile(tile + 1);
+        UCP_DCHECK(nxt > tile && nxt <= ntiles);
         if (cur == 0) {
           mbar_wait(&sbar[0], phase0);
           phase0 ^= 1u;
@@ -1004,7 +1052,7 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
             }
           }
         }
-        __syncthreads();
+        UCP_SYNC();
         cur ^= 1;
         tile = nxt;
       }
@@ -1013,12 +1061,12 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
       for (int64_t tile = next_tile(0); tile < ntiles; tile = next_tile(tile + 1)) {
         const int64_t base = tile * kTile;
         const int cnt = (int)(m - base < kTile ? m - base : kTile);
-        __syncthreads();
+        UCP_SYNC();
         for (int r = threadIdx.x; r < kTile; r += kQT) {
           sxw[r] = xw[base + r];
           slr[r] = r < cnt ? tails[base + r] : make_double2(0.0, 0.0);
         }
-        __syncthreads();
+        UCP_SYNC();
         // kernels.py:466-482 in order; the exp() of kMomUnroll pairs is
         // evaluated ahead (independent) and used only where the reference
         // evaluates it.  Padding slots (x = +inf, tails 0) give wp == 0.
@@ -1048,7 +1096,7 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
           }
         }
       }
-      __syncthreads();
+      UCP_SYNC();
       fence_proxy_async_smem();  // generic writes to sbuf[0] before later bulk copies into it
     }
     if (active) {
@@ -1056,9 +1104,12 @@ k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ 
       o1[t] = acc1;
       o2[t] = acc2;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) s_work = gridDim.x + atomicAdd(work_counter, 1);
-    __syncthreads();
+    UCP_SYNC();
+    if (threadIdx.x == 0) {
+      UCP_JITTER();
+      s_work = gridDim.x + atomicAdd(work_counter, 1);
+    }
+    UCP_SYNC();
   }
 }
 
@@ -1088,9 +1139,11 @@ static_assert(kFProd % kFQ == 0, "producer threads keep one query each");
 constexpr size_t kFSmem = 2 * 3 * kTile * kFQ * sizeof(double);  // 96 KiB at kFQ = 8: two CTAs per SM
 
 __device__ __forceinline__ void named_sync(int id, int count) {
+  UCP_JITTER();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 __device__ __forceinline__ void named_arrive(int id, int count) {
+  UCP_JITTER();
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
@@ -1141,7 +1194,7 @@ k_mom_fused(const double* __restrict__ yq, int64_t n, const double* __restrict__
       s_ymax = hi;
     }
   }
-  __syncthreads();
+  UCP_SYNC();
   const bool has_left = s_left != 0, has_right = s_right != 0;
   const double ymin = s_ymin, ymax = s_ymax;
   const int64_t ntiles = (m + kTile - 1) / kTile;

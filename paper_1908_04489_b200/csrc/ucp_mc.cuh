@@ -197,13 +197,13 @@ __device__ __forceinline__ double mc_block_sum(double v, double* warp_sums) {
   for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) warp_sums[warp] = v;
-  __syncthreads();
+  UCP_SYNC();
   double s = 0.0;
   if (threadIdx.x == 0) {
     s = warp_sums[0];
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) s = __dadd_rn(s, warp_sums[w]);
   }
-  __syncthreads();
+  UCP_SYNC();
   return s;
 }
 

@@ -268,6 +268,29 @@ class Witsenhausen(Problem):
         _lib.call("ucp_trapezoid_sum", ptr(terms), g.d, g.spacing, jbits.data_ptr(), None, D.stream)
         return jbits
 
+    def device_objective_terms(self, U: ControllerSet, sharding: Sharding = LOCAL) -> torch.Tensor:
+        """The objective's per-point integrand c_i = C0(u0_i, y_i) (problem.py:119-126)
+        as a device tensor of d0 doubles -- the values the serial trapezoid sums.
+        Non-finite terms are reported like device_objective's."""
+        D = self.device_context()
+        res = torch.full((1,), NO_ERROR, dtype=I64, device=D.device)
+        self.check_controllers(U)
+        g = self.grids[0]
+        u0, u1 = self._uv(U)
+        bounds = self._plan(0, U, sharding)
+        begin, end = sharding.shard(bounds)
+        buf = sharding.padded_buffer(bounds, D.device)
+        _lib.call("ucp_wc_objective_terms", ctypes.byref(D.P), ptr(u0), ptr(u1), begin, end,
+                  sharding.rank_ptr(buf, bounds), res.data_ptr(), D.stream)
+        terms = sharding.gather(buf, bounds, g.d)
+        sharding.allreduce_min_(res)
+        bad = int(D.errors.flush(sharding, extra=res)[0])
+        if bad != NO_ERROR:
+            raise NumericError(
+                f"{self.name}: non-finite objective integrand at stage 0, grid point {bad} "
+                f"(y={g.points[bad]!r}, u={U.values(0)[bad]!r})")
+        return terms
+
     def device_objective(self, U: ControllerSet, sharding: Sharding = LOCAL, deferred=()) -> float:
         """problem.py:110-127 on the device.  ``deferred`` objectives (from
         device_objective_deferred) are read in the same synchronisation."""
