@@ -134,6 +134,7 @@ class DeviceContext:
         self.ws = ws
         self.errors = ErrorLog(self.device, prob)
         self.windows: dict = {}
+        self.plans: dict = {}  # ((stage, radius), world) -> shard bounds (multi-rank sweeps)
 
     def __del__(self):
         try:

@@ -47,49 +47,82 @@ class Sharding:
         """Shard boundaries (world+1 ints).  With ``weights`` (int64 per-point
         work estimates, identical on every rank because they derive from the
         same snapshot) the cumulative work is split evenly; otherwise equal
-        point counts.  Boundaries never change a result bit."""
+        point counts.  Boundaries never change a result bit.  (Reads the cuts
+        back: the solver queues ``plan_cuts`` instead and reads them with a
+        synchronisation it makes anyway.)"""
         d = int(d)
         if self.world == 1:
             return (0, d)
         if weights is None:
-            c = self.chunk(d)
-            return tuple(min(r * c, d) for r in range(self.world)) + (d,)
+            return self.equal_plan(d)
+        return self.plan_from_cuts(d, self.plan_cuts(weights).cpu().tolist())
+
+    def equal_plan(self, d: int) -> tuple:
+        c = self.chunk(d)
+        return tuple(min(r * c, d) for r in range(self.world)) + (d,)
+
+    def plan_cuts(self, weights: torch.Tensor) -> torch.Tensor:
+        """The world-1 interior cuts of the weight-balanced plan, on the
+        weights' device (no synchronisation)."""
         cum = torch.cumsum(weights.to(torch.int64), 0)
         targets = (cum[-1] * torch.arange(1, self.world, device=cum.device, dtype=torch.int64)) // self.world
-        cuts = torch.searchsorted(cum, targets, right=True).cpu().tolist()
+        return torch.searchsorted(cum, targets, right=True)
+
+    def plan_from_cuts(self, d: int, cuts) -> tuple:
         out = [0]
         for c in cuts:
             out.append(min(max(int(c), out[-1]), d))
-        out.append(d)
+        out.append(int(d))
         return tuple(out)
 
     def shard(self, bounds: tuple) -> tuple[int, int]:
         return bounds[self.rank], bounds[self.rank + 1]
 
-    @staticmethod
-    def cmax(bounds: tuple) -> int:
-        return max(1, max(bounds[r + 1] - bounds[r] for r in range(len(bounds) - 1)))
-
     def padded_buffer(self, bounds: tuple, device) -> torch.Tensor:
-        """world slots of cmax doubles; rank r's points land in slot r."""
-        return torch.empty(self.cmax(bounds) * self.world, dtype=torch.float64, device=device)
+        """The phase output in the natural layout (grid point i at index i),
+        padded to chunk*world doubles so an equal-split plan all-gathers in place."""
+        d = bounds[-1]
+        return torch.empty(max(self.chunk(d) * self.world, 1), dtype=torch.float64, device=device)
 
     def rank_ptr(self, buf: torch.Tensor, bounds: tuple) -> int:
-        """Base pointer such that base[i] (i in this rank's shard) is its slot entry."""
-        return buf.data_ptr() + 8 * (self.rank * self.cmax(bounds) - bounds[self.rank])
+        """Base pointer such that base[i] (i in this rank's shard) is its output slot."""
+        return buf.data_ptr()
 
     def gather(self, buf: torch.Tensor, bounds: tuple, d: int) -> torch.Tensor:
-        """All-gather the slots and return the contiguous length-d vector."""
+        """All-gather every rank's shard of ``buf`` (natural layout) in place and
+        return the contiguous length-d vector: no compaction copy.  Equal-split
+        plans use one all_gather_into_tensor; work-balanced (uneven) plans one
+        uneven all_gather (NCCL: grouped broadcasts straight into place)."""
         if self.world == 1:
             return buf[:d]
-        self.allgather_(buf)
-        c = self.cmax(bounds)
-        if all(bounds[r] == r * c for r in range(self.world)):
-            return buf[:d]  # equal split: slots are already contiguous
-        slots = buf.view(self.world, c)
-        return torch.cat([slots[r, : bounds[r + 1] - bounds[r]] for r in range(self.world)])
+        if tuple(bounds) == self.equal_plan(d):
+            self.allgather_(buf)
+            return buf[:d]
+        self.allgather_uneven_(buf, bounds)
+        return buf[:d]
 
     # -- collectives -------------------------------------------------------
+    def allgather_uneven_(self, buf: torch.Tensor, bounds: tuple) -> None:
+        """buf[bounds[r]:bounds[r+1]] of rank r to every rank, in place."""
+        import torch.distributed as dist
+
+        b, e = self.shard(bounds)
+        if dist.get_backend(self.group) == "gloo":
+            # gloo has no uneven all-gather: pad each shard to the longest on the
+            # host (CPU-collective plumbing for tests; NCCL in production)
+            cm = max(1, max(bounds[r + 1] - bounds[r] for r in range(self.world)))
+            host = buf.cpu()
+            slots = torch.zeros(cm * self.world, dtype=host.dtype)
+            slots[self.rank * cm:self.rank * cm + (e - b)] = host[b:e]
+            dist.all_gather_into_tensor(slots, slots[self.rank * cm:(self.rank + 1) * cm].clone(), group=self.group)
+            for r in range(self.world):
+                host[bounds[r]:bounds[r + 1]] = slots[r * cm:r * cm + bounds[r + 1] - bounds[r]]
+            if buf.is_cuda:
+                buf.copy_(host)
+            return
+        outs = [buf[bounds[r]:bounds[r + 1]] for r in range(self.world)]
+        dist.all_gather(outs, buf[b:e], group=self.group)
+
     def allgather_(self, buf: torch.Tensor) -> None:
         """In-place all-gather of each rank's chunk of ``buf`` (no-op for one rank)."""
         if self.world == 1:

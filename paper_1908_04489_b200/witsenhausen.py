@@ -150,14 +150,17 @@ class Witsenhausen(Problem):
 
     # ------------------------------------------------ solver sweeps (device)
     # ---- work-balanced shards (multi-GPU) --------------------------------
-    def _plan(self, m: int, U: ControllerSet, sharding: Sharding, stage0_scale=None) -> tuple:
-        """Shard boundaries for a stage-m phase: split the estimated work
-        (walk nodes for stage 0, in-range support points for stage 1) evenly
-        across ranks.  Estimates come from the shared snapshot, so every rank
-        computes the same boundaries; results do not depend on them."""
-        d = self.grids[m].d
-        if sharding.world == 1 or d < BALANCE_MIN_POINTS:
-            return sharding.plan(d)
+    # Plans are cached per (stage, weighting) and refreshed at the objective's
+    # synchronisation (device_objective): the cuts are computed on the device
+    # from that snapshot and read back in the same copy as J, so a phase never
+    # waits on the host for its plan.  A phase uses the plan of the latest
+    # objective snapshot (the first use per problem computes it directly).
+    # Boundaries never change a result bit, only the balance.
+    def _plan_weights(self, key, U: ControllerSet) -> torch.Tensor:
+        """Per-point work estimates of plan ``key`` = (stage, scaled): walk nodes
+        for stage 0 (times the window width for exhaustion), in-range support
+        points for stage 1.  Every rank derives them from the same snapshot."""
+        m, scaled = key
         D = self.device_context()
         u0, _ = self._uv(U)
         g1 = self.grids[1]
@@ -166,12 +169,39 @@ class Witsenhausen(Problem):
             span = torch.clamp(torch.minimum(s + 12.0, torch.full_like(s, g1.b))
                                - torch.maximum(s - 12.0, torch.full_like(s, g1.a)), min=0.0)
             w = (span / g1.spacing).to(torch.int64) + 1
-            if stage0_scale is not None:
-                w = w * stage0_scale
-        else:
-            xs = torch.sort(D.y0 + u0).values
-            w = (torch.searchsorted(xs, D.y1 + 12.0, right=True) - torch.searchsorted(xs, D.y1 - 12.0)) + 1
-        return sharding.plan(d, w)
+            if scaled is not None:
+                lo, hi = D.window(self, 0, scaled)
+                w = w * (hi - lo + 1)
+            return w
+        xs = torch.sort(D.y0 + u0).values
+        return (torch.searchsorted(xs, D.y1 + 12.0, right=True) - torch.searchsorted(xs, D.y1 - 12.0)) + 1
+
+    def _plan(self, m: int, U: ControllerSet, sharding: Sharding, radius=None) -> tuple:
+        """Shard boundaries for a stage-m phase (``radius``: stage-0 exhaustion
+        windows of that radius weight the walks)."""
+        d = self.grids[m].d
+        if sharding.world == 1 or d < BALANCE_MIN_POINTS:
+            return sharding.equal_plan(d) if sharding.world > 1 else (0, d)
+        key = (m, radius if m == 0 else None)
+        cache = self.device_context().plans
+        if (key, sharding.world) not in cache:  # first use: computed now (one read-back)
+            cache[(key, sharding.world)] = sharding.plan(d, self._plan_weights(key, U))
+        return cache[(key, sharding.world)]
+
+    def _queue_plan_refresh(self, U: ControllerSet, sharding: Sharding):
+        """Device cuts of every cached plan for snapshot U (no synchronisation);
+        returns (keys, int64 tensor) for _apply_plan_refresh."""
+        keys = [k for k in self.device_context().plans if k[1] == sharding.world]
+        if not keys or sharding.world == 1:
+            return [], None
+        cuts = torch.cat([sharding.plan_cuts(self._plan_weights(k, U)) for k, _ in keys])
+        return keys, cuts
+
+    def _apply_plan_refresh(self, keys, host_cuts, sharding: Sharding) -> None:
+        n = sharding.world - 1
+        cache = self.device_context().plans
+        for q, key in enumerate(keys):
+            cache[key] = sharding.plan_from_cuts(self.grids[key[0][0]].d, host_cuts[q * n:(q + 1) * n])
 
     def device_local_update(self, m: int, U: ControllerSet, cfg, sharding: Sharding = LOCAL):
         """One local-update sweep of stage m (solver.py:179-203); returns a CUDA tensor."""
@@ -193,7 +223,7 @@ class Witsenhausen(Problem):
         g = self.grids[m]
         u0, u1 = self._uv(U)
         lo, hi = D.window(self, m, cfg.radius_for(g))
-        bounds = self._plan(m, U, sharding, stage0_scale=(hi - lo + 1) if m == 0 else None)
+        bounds = self._plan(m, U, sharding, radius=cfg.radius_for(g) if m == 0 else None)
         begin, end = sharding.shard(bounds)
         buf = sharding.padded_buffer(bounds, D.device)
         err = D.errors.slot("exhaustion", m, sharding)
@@ -297,10 +327,16 @@ class Witsenhausen(Problem):
         D = self.device_context()
         res = torch.full((1,), NO_ERROR, dtype=I64, device=D.device)
         jbits = self._queue_objective(U, sharding, res)
+        keys, cuts = self._queue_plan_refresh(U, sharding)
         # one synchronisation: the pending phase-error rows (deferred objectives
-        # among them, in queue order) and every J travel together
-        extra = torch.cat([res, jbits] + [p[0] for p in deferred])
+        # among them, in queue order), every J and the refreshed shard plans
+        # travel together
+        extra = torch.cat([res, jbits] + [p[0] for p in deferred] + ([cuts] if keys else []))
         host = D.errors.flush(sharding, extra=extra)
+        if keys:
+            nj = 2 + len(deferred)
+            self._apply_plan_refresh(keys, host[nj:], sharding)
+            host = host[:nj]
         bad = int(host[0])
         if bad != NO_ERROR:
             g = self.grids[0]

@@ -281,3 +281,45 @@ def test_config5_sharded_solve_bitwise_world2():
             assert J == ref.final_objective, (name, r)
             for m, u in enumerate(us):
                 assert np.array_equal(u.view(np.uint64), np.asarray(ref.controllers.values(m)).view(np.uint64))
+
+
+# --------------------- no host synchronisation inside a multi-rank phase
+@pytest.mark.gpu
+def test_sharded_phases_do_not_synchronise(monkeypatch):
+    """Rank 0 of a 2-rank work-balanced plan (collectives stubbed: this is about
+    the host side): once a solve has cached the plans, every phase -- plan,
+    sweep, gather -- queues its work without one host<->device synchronisation
+    (torch sync debug mode "error" raises on any).  The plans are refreshed
+    from the objective's own read-back (Witsenhausen.device_objective)."""
+    import paper_1908_04489_b200 as P
+    from paper_1908_04489_b200 import witsenhausen
+
+    class Stub(P.Sharding):
+        def allgather_(self, buf):
+            pass
+
+        def allgather_uneven_(self, buf, bounds):
+            pass
+
+        def allreduce_min_(self, t):
+            pass
+
+    monkeypatch.setattr(witsenhausen, "BALANCE_MIN_POINTS", 1024)
+    sh = Stub(rank=0, world=2)
+    d = 4096
+    prob = P.Witsenhausen(grids=[(-25.0, 25.0, d)] * 2)
+    cfg = P.SolverConfig(max_rounds=1)
+    res = P.solve(prob, cfg, sharding=sh)  # fills and refreshes the plan cache
+    plans = prob.device_context().plans
+    assert {k[0] for k in plans} == {(0, None), (0, cfg.radius_for(prob.grids[0])), (1, None)}
+    assert all(b != sh.equal_plan(d) for b in plans.values())  # uneven: the balanced path
+    U = res.controllers
+    torch.cuda.synchronize()
+    torch.cuda.set_sync_debug_mode("error")
+    try:
+        for m in (0, 1):
+            prob.device_local_update(m, U, cfg, sh)
+            prob.device_exhaustion(m, U, cfg, sh)
+    finally:
+        torch.cuda.set_sync_debug_mode("default")
+    prob.flush_errors(sh)

@@ -87,3 +87,37 @@ def test_batch_numeric_error_is_the_single_solves(P):
     with pytest.raises(P.NumericError) as want:
         P.solve(probs[1], P.SolverConfig(max_rounds=2), bad)
     assert str(got.value) == str(want.value)
+
+
+def _same_as_oracle(r, want):
+    """A SolveResult vs oracle.solve's (u0, u1, J, rounds, termination), bitwise."""
+    u0, u1, J, rounds, term = want
+    assert r.termination == term
+    assert np.float64(r.final_objective).view(np.uint64) == np.float64(J).view(np.uint64)
+    assert len(r.rounds) == len(rounds)
+    for got, (idx, after_exh, gl, ge, nl, ne, after_local) in zip(r.rounds, rounds):
+        assert (got.round_index, got.local_iters, got.exhaustion_iters) == (idx, nl, ne)
+        g = np.array([got.objective, got.objective_after_local, got.local_gain, got.exhaustion_gain])
+        w = np.array([after_exh, after_local, gl, ge])
+        assert np.array_equal(g.view(np.uint64), w.view(np.uint64)), (idx, g, w)
+    for m, w in enumerate((u0, u1)):
+        assert np.array_equal(np.asarray(r.controllers.values(m)).view(np.uint64), w.view(np.uint64)), m
+
+
+@pytest.mark.parametrize("d", [201, 301])
+def test_batch_vs_oracle_sweep(P, oracle_mod, d):
+    """The batched engine against the oracle (not against itself): every
+    (k, sigma) of k in {0.05, 0.2, 0.6, 1.0} x sigma in {3, 5, 7} solved to
+    convergence in ONE solve_batch, each instance's trajectory (controllers,
+    J, every RoundReport) bitwise the oracle's sequential solve
+    (reference solver.py:234-290)."""
+    from paper_1908_04489_b200.batch import solve_batch
+
+    ks = [(k, s) for k in (0.05, 0.2, 0.6, 1.0) for s in (3.0, 5.0, 7.0)]
+    probs = [P.Witsenhausen(k=k, sigma=s, grids=[(-25.0, 25.0, d)] * 2) for k, s in ks]
+    got = solve_batch(probs, P.SolverConfig())
+    assert len({r.total_rounds for r in got}) > 1  # schedules diverge between instances
+    for (k, s), pr, r in zip(ks, probs, got):
+        p = oracle_mod.OracleWitsenhausen(k=k, sigma=s, grid0=(-25.0, 25.0, d), grid1=(-25.0, 25.0, d),
+                                          f0=pr._f0, fw0=pr._fw0)
+        _same_as_oracle(r, oracle_mod.solve(p, oracle_mod.OracleConfig()))

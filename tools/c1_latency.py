@@ -91,5 +91,33 @@ def main():
                               rounds_ms[int(np.argmax(walls))]}), flush=True)
 
 
+def profile_fresh(n=5):
+    """cProfile of n fresh-problem solves vs n re-solves of one problem: where
+    the fresh solves' extra host time goes (top functions by own time)."""
+    import cProfile
+    import pstats
+
+    torch.cuda.set_device(0)
+    P.solve(P.Witsenhausen(), P.SolverConfig(max_rounds=1))
+    same = P.Witsenhausen()
+    P.solve(same, P.SolverConfig())
+    for mode in ("fresh", "same"):
+        pr_ = cProfile.Profile()
+        for _ in range(n):
+            pr = same if mode == "same" else P.Witsenhausen()
+            pr.objective(pr.identity_controllers())
+            gc.collect()
+            torch.cuda.synchronize()
+            pr_.enable()
+            P.solve(pr, P.SolverConfig())
+            torch.cuda.synchronize()
+            pr_.disable()
+        print(f"==== {mode}: {n} solves, top 25 by own time", flush=True)
+        pstats.Stats(pr_).sort_stats("tottime").print_stats(25)
+
+
 if __name__ == "__main__":
-    main()
+    if "--profile" in sys.argv:
+        profile_fresh()
+    else:
+        main()
