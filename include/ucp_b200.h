@@ -76,6 +76,12 @@ int64_t ucp_launch_count(void);
 /* Scratch memory for the sweeps; grows on first use, reused afterwards. */
 int ucp_workspace_create(ucp_workspace** ws);
 int ucp_workspace_destroy(ucp_workspace* ws);
+/* Hand a workspace to a new owner (the Python side pools them across
+ * problems): synchronises the device (the next owner may use another stream),
+ * drops the content-keyed Inventory caches and marks the captured block graphs
+ * stale -- never replayed as they are, only reused through
+ * cudaGraphExecUpdate by a capture of the same shape. */
+int ucp_workspace_recycle(ucp_workspace* ws);
 /* Pre-size scratch for grids of d0/d1 points and up to max_cand exhaustion
  * candidates so later calls never allocate. */
 int ucp_workspace_reserve(ucp_workspace* ws, int64_t d0, int64_t d1, int64_t max_cand);
@@ -96,6 +102,14 @@ int ucp_trapezoid_sum(const double* samples, int64_t n, double spacing, double* 
 /* kernels.segmented_argmin (kernels.py:147-160). */
 int ucp_segmented_argmin(const double* costs, const int64_t* offsets, int64_t nseg,
                          int64_t* out, void* stream);
+/* kernels.flatten_windows, numba variant (kernels.py:163-187, dedup of later
+ * duplicates within each window, window order kept).  Point i's window is
+ * values[lo[i]..hi[i]] (0 <= lo[i] <= hi[i] < d).  offsets: n+1 entries (its
+ * last one is the kept total); flat: capacity sum(hi-lo+1) doubles, or NULL
+ * to compute only the offsets.  Asynchronous: read offsets[n] to size the
+ * result. */
+int ucp_flatten_windows(const double* values, int64_t d, const int64_t* lo, const int64_t* hi, int64_t n,
+                        double* flat, int64_t* offsets, ucp_workspace* ws, void* stream);
 /* Device libm port, exposed for parity tests: out[i] = exp(x[i]) (which=0),
  * erf(x[i]) (which=1) or the reference's phi_cdf(x[i]) (which=2). */
 int ucp_device_libm(int which, const double* x, int64_t n, double* out, void* stream);

@@ -50,6 +50,7 @@ SIGNATURES = {
     "ucp_launch_count": (c_i64, []),
     "ucp_workspace_create": (c_int, [ctypes.POINTER(c_vp)]),
     "ucp_workspace_destroy": (c_int, [c_vp]),
+    "ucp_workspace_recycle": (c_int, [c_vp]),
     "ucp_workspace_reserve": (c_int, [c_vp, c_i64, c_i64, c_i64]),
     "ucp_gauss_moments_grid": (c_int, [c_vp, c_i64, c_vp, c_dbl, c_dbl, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "ucp_gauss_moments_points": (c_int, [c_vp, c_i64, c_vp, c_vp, c_i64, c_dbl, c_dbl, c_i64, c_vp, c_vp,
@@ -57,6 +58,7 @@ SIGNATURES = {
     "ucp_trapezoid_sum": (c_int, [c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp]),
     "ucp_segmented_argmin": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "ucp_device_libm": (c_int, [c_int, c_vp, c_i64, c_vp, c_vp]),
+    "ucp_flatten_windows": (c_int, [c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "ucp_wc_stage0_cost": (c_int, [ctypes.POINTER(WcProblem), c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64,
                                    c_vp, c_vp]),
     "ucp_wc_stage1_cost": (c_int, [ctypes.POINTER(WcProblem), c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp,

@@ -190,7 +190,8 @@ struct BatchArgs {
 };
 constexpr BatchArgs kNoBatch = {nullptr, 0, 0, 0, 0, nullptr};
 
-unsigned long long* g_visits = nullptr;  // ucp_walk_node_counter (instrumentation only)
+// ucp_walk_node_counter (instrumentation only); read once per walk grid
+std::atomic<unsigned long long*> g_visits{nullptr};
 
 WalkGrid make_walk_grid(double a, double h, int64_t d) {
   WalkGrid g;
@@ -201,7 +202,7 @@ WalkGrid make_walk_grid(double a, double h, int64_t d) {
   g.q = ucp_exp_tab((-h) * h, h_exp_tab);  // same port as the device: bitwise glibc
   g.vsuf = nullptr;
   g.nb = (int)((d + (1 << 8) - 1) >> 8);
-  g.visits = g_visits;
+  g.visits = g_visits.load(std::memory_order_acquire);
   return g;
 }
 
@@ -624,6 +625,31 @@ __global__ void k_segmented_argmin(const double* __restrict__ costs, const int64
     }
   }
   out[s] = best;
+}
+
+// kernels.flatten_windows, numba variant (kernels.py:163-187): the window
+// values[lo[i]..hi[i]] of point i in order, a value dropped when an earlier
+// value of the same window equals it (NaN never equals: always kept).  One
+// thread per point; counts (kFill = false) then a scan, then the fill.
+template <bool kFill>
+__global__ void k_flatten_windows(const double* __restrict__ values, const int64_t* __restrict__ lo,
+                                  const int64_t* __restrict__ hi, int64_t n, int64_t* counts,
+                                  const int64_t* __restrict__ offsets, double* flat) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t l = lo[i], r = hi[i];
+  int64_t pos = kFill ? offsets[i] : 0;
+  for (int64_t j = l; j <= r; ++j) {
+    const double v = values[j];
+    bool dup = false;
+    for (int64_t t = l; t < j && !dup; ++t) dup = values[t] == v;
+    if (!dup) {
+      if (kFill) flat[pos] = v;
+      ++pos;
+    }
+  }
+  if (!kFill) counts[i] = pos;
+  UCP_DCHECK(!kFill || pos == offsets[i + 1]);
 }
 
 // ---- exhaustion, stage 0 (solver.py:206-223) -------------------------------
@@ -1409,9 +1435,12 @@ __global__ void k_fp64_probe(int iters, double* sink) {
 }  // namespace
 
 // ============================================================ workspace
+constexpr int kGraphKeyWords = 21;
 struct ucp_graph_entry {
-  std::array<uint64_t, 20> key;
+  std::array<uint64_t, kGraphKeyWords> key;
   cudaGraphExec_t exec;
+  int64_t kernels;  // kernel nodes per replay (the launch counter)
+  bool stale;       // recycled workspace: reusable only through cudaGraphExecUpdate
 };
 
 // CUDA-graph captures (ThreadLocal mode) run concurrently in the host threads
@@ -1461,7 +1490,18 @@ const int64_t kFusedMaxQueries = [] {
 // warp-per-point candidate fill below this many points (one thread per point above)
 constexpr int64_t kWarpFillMaxPoints = 1 << 16;
 // sync-free exhaustion when the candidate upper bound fits (16 B per candidate)
-constexpr int64_t kSyncFreeMaxCand = (int64_t)1 << 27;
+// (an eighth of the device memory, read once; at least 2^27 candidates, and
+// under 2^31 so candidate positions fit the kernels' int32 point indices):
+// C3's 2^22-point, 39-node sweep (1.6e8 candidates, 2.6 GB) stays sync-free.
+int64_t sync_free_max_cand() {
+  static const int64_t cap = [] {
+    size_t free_b = 0, total_b = 0;
+    int64_t c = (int64_t)1 << 27;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) c = std::max(c, (int64_t)(total_b / 8 / 16));
+    return std::min(c, ((int64_t)1 << 31) - 1);
+  }();
+  return cap;
+}
 
 int ws_get(ucp_workspace* ws, int slot, size_t bytes, void** out) {
   if (ws->cap[slot] < bytes) {
@@ -1528,12 +1568,12 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
 
 // Walk launches below one full wave of resident CTAs run the latency-mode walk.
 bool walk_latency_mode(int64_t n_walks) {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = 148;
-  }
+  static const int sms = [] {  // initialised once, thread-safe (function-local static)
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      n = 148;
+    return n;
+  }();
   return n_walks < (int64_t)sms * kWalkMinBlocks * kWalkThreads;
 }
 
@@ -1641,6 +1681,16 @@ int ucp_workspace_destroy(ucp_workspace* ws) {
   return UCP_OK;
 }
 
+int ucp_workspace_recycle(ucp_workspace* ws) {
+  if (!ws) return arg_fail("null workspace");
+  std::unique_lock<std::shared_mutex> lk(g_capture_mu);
+  // the next owner may queue on another stream: nothing in flight may still use the buffers
+  UCP_CHECK(cudaDeviceSynchronize());
+  for (auto& g : ws->graphs) g.stale = true;
+  ws->inv = ucp_inv_cache{};
+  return UCP_OK;
+}
+
 int ucp_workspace_reserve(ucp_workspace* ws, int64_t d0, int64_t d1, int64_t max_cand) {
   if (!ws) return arg_fail("null workspace");
   void* p;
@@ -1701,6 +1751,32 @@ int ucp_segmented_argmin(const double* costs, const int64_t* offsets, int64_t ns
   if (nseg == 0) return UCP_OK;
   k_segmented_argmin<<<nblocks(nseg, 128), 128, 0, as_stream(stream)>>>(costs, offsets, nseg, out);
   UCP_LAUNCHED("k_segmented_argmin");
+  return UCP_OK;
+}
+
+int ucp_flatten_windows(const double* values, int64_t d, const int64_t* lo, const int64_t* hi, int64_t n,
+                        double* flat, int64_t* offsets, ucp_workspace* ws, void* stream) {
+  if (n < 0 || d < 1 || !values || !lo || !hi || !offsets || !ws) return arg_fail("flatten_windows: bad arguments");
+  cudaStream_t st = as_stream(stream);
+  UCP_CHECK(cudaMemsetAsync(offsets, 0, sizeof(int64_t) * (size_t)(n + 1), st));
+  if (n == 0) return UCP_OK;
+  // counts land in offsets[1..n]; an inclusive scan in place makes them offsets
+  k_flatten_windows<false><<<nblocks(n, 128), 128, 0, st>>>(values, lo, hi, n, offsets + 1, nullptr, nullptr);
+  UCP_LAUNCHED("k_flatten_windows<count>");
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, offsets + 1, offsets + 1, n, st);
+  if (ws->scan_cap < tmp_bytes) {
+    std::unique_lock<std::shared_mutex> lk(g_capture_mu);
+    if (ws->scan_tmp) UCP_CHECK(cudaFree(ws->scan_tmp));
+    UCP_CHECK(cudaMalloc(&ws->scan_tmp, tmp_bytes));
+    ws->scan_cap = tmp_bytes;
+  }
+  UCP_CHECK(cub::DeviceScan::InclusiveSum(ws->scan_tmp, tmp_bytes, offsets + 1, offsets + 1, n, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (flat) {
+    k_flatten_windows<true><<<nblocks(n, 128), 128, 0, st>>>(values, lo, hi, n, nullptr, offsets, flat);
+    UCP_LAUNCHED("k_flatten_windows<fill>");
+  }
   return UCP_OK;
 }
 
@@ -1834,7 +1910,7 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
   // bound and let the kernels read the true count: no host round trip, so a
   // whole block of phases stays queued on the stream.  Otherwise read it back.
   int64_t total;
-  if (cand_bound > 0 && cand_bound <= kSyncFreeMaxCand) {
+  if (cand_bound > 0 && cand_bound <= sync_free_max_cand()) {
     total = cand_bound;
   } else {
     UCP_CHECK(cudaMemcpyAsync(ws->h_total, counts + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -1938,13 +2014,13 @@ int ucp_wc_run_block_graph(const ucp_wc_problem* P, int kind, int iters, double*
   // captured iteration never allocates (and proves the launch sequence)
   if ((rc = block_iteration(P, kind, u0, u1, lp, lo, hi, cand_bound0, scratch, err6, ws, st))) return rc;
   if (iters == 1) return UCP_OK;
-  const bool graphable = kind == 0 || (cand_bound0 > 0 && cand_bound0 <= kSyncFreeMaxCand);
+  const bool graphable = kind == 0 || (cand_bound0 > 0 && cand_bound0 <= sync_free_max_cand());
   if (!graphable) {  // exhaustion that must read its candidate count back: stay eager
     for (int it = 1; it < iters; ++it)
       if ((rc = block_iteration(P, kind, u0, u1, lp, lo, hi, cand_bound0, scratch, err6, ws, st))) return rc;
     return UCP_OK;
   }
-  std::array<uint64_t, 20> key{};
+  std::array<uint64_t, kGraphKeyWords> key{};
   key[0] = (uint64_t)kind;
   key[1] = (uint64_t)(uintptr_t)P;
   key[2] = (uint64_t)(uintptr_t)u0;
@@ -1961,9 +2037,15 @@ int ucp_wc_run_block_graph(const ucp_wc_problem* P, int kind, int iters, double*
     const double* lv = reinterpret_cast<const double*>(lp);
     for (int k = 0; k < 8; ++k) key[12 + k] = ucp_asu64(lv[k]);
   }
+  // captured walk grids bake in the node-counter pointer
+  key[20] = (uint64_t)(uintptr_t)g_visits.load(std::memory_order_acquire);
   cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;
   for (auto& g : ws->graphs)
-    if (g.key == key) exec = g.exec;
+    if (!g.stale && g.key == key) {
+      exec = g.exec;
+      kernels = g.kernels;
+    }
   if (!exec) {
     if (!ws->cap_stream) UCP_CHECK(cudaStreamCreateWithFlags(&ws->cap_stream, cudaStreamNonBlocking));
     std::shared_lock<std::shared_mutex> lk(g_capture_mu);
@@ -1976,15 +2058,48 @@ int ucp_wc_run_block_graph(const ucp_wc_problem* P, int kind, int iters, double*
       return rc;
     }
     if (ec != cudaSuccess) return cuda_fail(ec, "cudaStreamEndCapture");
-    ec = cudaGraphInstantiate(&exec, graph, 0);
+    // kernel nodes of one iteration (the launch counter adds them per replay)
+    size_t nn = 0;
+    cudaGraphGetNodes(graph, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+    for (size_t q = 0; q < nn; ++q) {
+      cudaGraphNodeType t;
+      if (cudaGraphNodeGetType(nodes[q], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++kernels;
+    }
+    // a recycled workspace's graph of the same shape (a previous problem's)
+    // takes the new parameters by an in-place update, far cheaper than a new
+    // instantiation; otherwise instantiate
+    for (size_t q = 0; q < ws->graphs.size() && !exec;) {
+      auto& g = ws->graphs[q];
+      if (!g.stale || g.key[0] != key[0] || g.kernels != kernels) {
+        ++q;
+        continue;
+      }
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(g.exec, graph, &info) == cudaSuccess) {
+        g.key = key;
+        g.stale = false;
+        exec = g.exec;
+      } else {  // not updatable (another shape): drop it (recycling synchronised: not in flight)
+        cudaGetLastError();
+        cudaGraphExecDestroy(g.exec);
+        ws->graphs.erase(ws->graphs.begin() + (std::ptrdiff_t)q);
+      }
+    }
+    if (!exec) {
+      ec = cudaGraphInstantiate(&exec, graph, 0);
+      if (ec != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return cuda_fail(ec, "cudaGraphInstantiate");
+      }
+      ws->graphs.push_back({key, exec, kernels, false});
+    }
     cudaGraphDestroy(graph);
-    if (ec != cudaSuccess) return cuda_fail(ec, "cudaGraphInstantiate");
-    ws->graphs.push_back({key, exec});
   }
-  // kernel launches of one iteration == the graph's nodes (for the counter)
   for (int it = 1; it < iters; ++it) {
     UCP_CHECK(cudaGraphLaunch(exec, st));
-    g_launches.fetch_add(kind == 0 ? 6 : 10, std::memory_order_relaxed);
+    g_launches.fetch_add(kernels, std::memory_order_relaxed);
   }
   return UCP_OK;
 }
@@ -2004,7 +2119,7 @@ int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const doub
 }
 
 int ucp_walk_node_counter(unsigned long long* counter) {
-  g_visits = counter;
+  g_visits.store(counter, std::memory_order_release);
   return UCP_OK;
 }
 

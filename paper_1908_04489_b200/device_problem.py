@@ -4,9 +4,9 @@ synchronisation point with the reference's exception) and a generic device
 context used by the config-5 problems."""
 from __future__ import annotations
 
-import weakref
-
 import ctypes
+import threading
+import weakref
 
 import numpy as np
 import torch
@@ -123,14 +123,43 @@ def _phase_error(problem, kind, m, row):
 
 
 
+# Released workspaces, per device, for the next problem (ucp_workspace_recycle):
+# a fresh problem -- e.g. every solve of a parameter sweep -- reuses grown
+# scratch buffers and updates the previous problem's captured block graphs in
+# place instead of allocating and instantiating anew.
+_POOL: dict = {}
+_POOL_LOCK = threading.Lock()
+POOL_MAX = 2  # workspaces kept per device
+
+
+def _pool_take(index: int):
+    with _POOL_LOCK:
+        free = _POOL.get(index)
+        return free.pop() if free else None
+
+
+def _pool_give(lib, index: int, ws) -> None:
+    """Recycle ws into the pool (or destroy it when the pool is full).  Runs
+    from __del__, in whatever thread the collector picks: the library takes
+    its capture lock for the device synchronisation."""
+    with _POOL_LOCK:
+        free = _POOL.setdefault(index, [])
+        if len(free) < POOL_MAX and lib.ucp_workspace_recycle(ws) == 0:
+            free.append(ws)
+            return
+    lib.ucp_workspace_destroy(ws)
+
+
 class DeviceContext:
     """Workspace, error log and cached window bounds of one device problem."""
 
     def __init__(self, prob, device=None):
         self.lib = _lib.load()
         self.device = require_cuda(device)
-        ws = ctypes.c_void_p()
-        _lib.call("ucp_workspace_create", ctypes.byref(ws))
+        ws = _pool_take(self.device.index)
+        if ws is None:
+            ws = ctypes.c_void_p()
+            _lib.call("ucp_workspace_create", ctypes.byref(ws))
         self.ws = ws
         self.errors = ErrorLog(self.device, prob)
         self.windows: dict = {}
@@ -139,10 +168,11 @@ class DeviceContext:
     def __del__(self):
         try:
             if self.ws:
-                # synchronises the device itself, under the library's capture
-                # lock (a bare device sync here -- the GC may run this in any
-                # thread -- would invalidate another thread's graph capture)
-                self.lib.ucp_workspace_destroy(self.ws)
+                # recycle/destroy synchronise the device themselves, under the
+                # library's capture lock (a bare device sync here -- the GC may
+                # run this in any thread -- would invalidate another thread's
+                # graph capture)
+                _pool_give(self.lib, self.device.index, self.ws)
         except Exception:  # interpreter shutdown
             pass
 

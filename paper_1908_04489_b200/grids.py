@@ -79,8 +79,15 @@ def content_key(t) -> int:
     tensor, combined with the tensor's in-place version counter, so a key is
     never shared by different contents (ucp_inv_problem.ukey)."""
     serial = getattr(t, "_ucp_serial", 0)
-    version = t._version
-    if not serial or version >= 1 << 20 or serial >= 1 << 43:
+    if not serial:
+        return 0
+    try:
+        if t.is_inference():  # no version counter: writes cannot be seen, so no reuse
+            return 0
+        version = t._version
+    except RuntimeError:
+        return 0
+    if version >= 1 << 20 or serial >= 1 << 43:
         return 0
     return (serial << 20) | version
 
@@ -106,7 +113,12 @@ class SampledController:
             t = values.detach()
             if t.dtype != torch.float64 or t.dim() != 1 or t.numel() != grid.d:
                 raise ValueError(f"controller needs {grid.d} values, got shape {tuple(t.shape)}")
-            t = t.contiguous()
+            # a caller's tensor is copied (the reference copies its input too,
+            # grids.py:76-85): later writes to it -- including ones the version
+            # counter does not see (.data, DLPack, raw pointers) -- can neither
+            # change this immutable controller nor a content-keyed cache entry;
+            # the library's own sweep outputs are adopted as they are
+            t = t.contiguous() if _trusted_device else t.clone(memory_format=torch.contiguous_format)
             if not _trusted_device:
                 ok = torch.isfinite(t)
                 if not bool(ok.all()):

@@ -18,17 +18,29 @@ from ._device import F64, I64, ptr, require_cuda, stream_ptr, to_device_f64, to_
 
 __all__ = [
     "BACKEND",
+    "NUMBA_ENABLED",
     "GAUSS_CUT",
     "set_workers",
     "max_workers",
     "trapezoid_sum",
+    "flatten_windows",
     "segmented_argmin",
     "gauss_moments_grid",
     "gauss_moments_points",
+    "unif_moments_grid",
+    "unif_ball_sum",
+    "unif_propagate",
+    "unif_moments_points",
+    "implementations",
     "device_libm",
 ]
 
 BACKEND = "b200"
+# No numba here; every kernel follows the numba backend's semantics (bitwise its
+# results, flatten_windows' dedup included), which is what the reference's tests
+# gate on NUMBA_ENABLED -- NUMBA_SEMANTICS says so without claiming numba.
+NUMBA_ENABLED = False
+NUMBA_SEMANTICS = True
 GAUSS_CUT = 12.0
 _TLS = threading.local()  # one scratch workspace per (host thread, device)
 
@@ -106,6 +118,79 @@ def segmented_argmin(costs, offsets):
     _lib.call("ucp_segmented_argmin", ptr(cd), ptr(od), nseg, ptr(out), stream_ptr(dev))
     out = out[:nseg]
     return out if keep else out.cpu().numpy()
+
+
+def flatten_windows(values, lo, hi):
+    """Flat candidates and offsets of every window values[lo[i]..hi[i]]
+    (kernels.py:163-187, numba variant: a value equal to an earlier one of the
+    same window is dropped, window order kept)."""
+    dev, keep = _device_of(values, lo, hi)
+    vd, lod, hid = to_device_f64(values, dev), to_device_i64(lo, dev), to_device_i64(hi, dev)
+    n = lod.numel()
+    if hid.numel() != n:
+        raise ValueError("lo and hi disagree")
+    width = (hid - lod + 1).clamp(min=0)
+    if n and bool(((width > 0) & ((lod < 0) | (hid >= vd.numel()))).any()):
+        raise ValueError("window bounds outside the values")
+    cap = int(width.sum().item()) if n else 0
+    flat = torch.empty(max(cap, 1), dtype=F64, device=dev)
+    offsets = torch.empty(n + 1, dtype=I64, device=dev)
+    _lib.call("ucp_flatten_windows", ptr(vd), vd.numel(), ptr(lod), ptr(hid), n, ptr(flat), ptr(offsets),
+              _workspace(dev), stream_ptr(dev))
+    total = int(offsets[n].item())
+    return _out(flat[:total], keep), _out(offsets, keep)
+
+
+def _unif(name, n_out, n, *args, dev, keep, length=None):
+    from .config5 import _bind
+
+    _bind()
+    outs = [torch.empty(max(length if length is not None else n, 1), dtype=F64, device=dev) for _ in range(n_out)]
+    _lib.call(name, *args, *(ptr(o) for o in outs), stream_ptr(dev))
+    outs = [o[:length if length is not None else n] for o in outs]
+    return tuple(_out(o, keep) for o in outs) if n_out > 1 else _out(outs[0], keep)
+
+
+def unif_moments_grid(x, v, a, h, d, rad):
+    """Uniform-noise moments of a clamped step function v at centres x (kernels.py:488-525)."""
+    dev, keep = _device_of(x, v)
+    xd, vd = to_device_f64(x, dev), to_device_f64(v, dev)
+    return _unif("ucp_unif_moments_grid", 3, xd.numel(), ptr(xd), xd.numel(), ptr(vd), float(a), float(h), int(d),
+                 float(rad), dev=dev, keep=keep)
+
+
+def unif_ball_sum(x, g, a, h, d, rad):
+    """Ball average of g over [x - rad, x + rad] (kernels.py:528-555)."""
+    dev, keep = _device_of(x, g)
+    xd, gd = to_device_f64(x, dev), to_device_f64(g, dev)
+    return _unif("ucp_unif_ball_sum", 1, xd.numel(), ptr(xd), xd.numel(), ptr(gd), float(a), float(h), int(d),
+                 float(rad), dev=dev, keep=keep)
+
+
+def unif_propagate(masses, centers, a, h, d, rad):
+    """Density on the d grid cells of masses spread uniformly around centres (kernels.py:558-577)."""
+    dev, keep = _device_of(masses, centers)
+    md, cd = to_device_f64(masses, dev), to_device_f64(centers, dev)
+    return _unif("ucp_unif_propagate", 1, md.numel(), ptr(md), ptr(cd), md.numel(), float(a), float(h), int(d),
+                 float(rad), dev=dev, keep=keep, length=int(d))
+
+
+def unif_moments_points(y, centers, w, vals, a, h, d, rad):
+    """Cell-overlap moments over scattered support points (kernels.py:580-615)."""
+    dev, keep = _device_of(y, centers, w, vals)
+    yd, cd = to_device_f64(y, dev), to_device_f64(centers, dev)
+    wd, vd = to_device_f64(w, dev), to_device_f64(vals, dev)
+    return _unif("ucp_unif_moments_points", 3, yd.numel(), ptr(yd), yd.numel(), ptr(cd), ptr(wd), ptr(vd), cd.numel(),
+                 float(a), float(h), int(d), float(rad), dev=dev, keep=keep)
+
+
+def implementations() -> dict:
+    """The heavy kernels by name, as ``(device_impl, None)`` (kernels.py:640-658
+    returns ``(numba_impl_or_None, numpy_impl)``; this backend has one
+    implementation per kernel, bitwise the numba one)."""
+    names = ["gauss_moments_grid", "gauss_moments_points", "unif_moments_grid", "unif_ball_sum",
+             "unif_propagate", "unif_moments_points"]
+    return {name: (globals()[name], None) for name in names}
 
 
 def device_libm(which: str, x):
