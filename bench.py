@@ -332,6 +332,7 @@ def run_ours(args):
     # (a d=2000 phase is latency-bound: sharding it only adds collectives).
     warm = P.Witsenhausen(k=K_WC, sigma=SIGMA)
     P.solve(warm, P.SolverConfig(max_rounds=1))
+    del warm  # its workspace goes to the pool every later problem draws from
 
     def timed_solves(make, n):
         walls, res = [], None
