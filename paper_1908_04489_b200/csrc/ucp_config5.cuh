@@ -380,6 +380,195 @@ __global__ void __launch_bounds__(32 * kUnifWarps) k_unif_moments_points(
   }
 }
 
+// Producer/consumer form of k_unif_propagate (kPlanes = 1) and
+// k_unif_moments_points (kPlanes = 3): the reference's per-output loops are
+// serial add chains (kernels.py:562-576, 593-613), and one thread per output
+// leaves them latency-bound (one warp per scheduler at d = 4096 / 16384,
+// every source costing the whole clamp/overlap/product dependency chain).
+// Here a CTA owns 32 outputs ("queries": cells j for propagate, points y_t
+// for moments).  8 producer warps scan the sources in ascending order,
+// compact the ones that can touch the CTA's cell span (ballot + per-warp
+// counts: order kept) into a shared-memory ring, and evaluate 32-source
+// stages of per-(source, query) terms -- mass*ov, or wov, wov*v, (wov*v)*v
+// for ov > 0, +0.0 otherwise -- while one consumer warp per accumulator adds
+// the previous stage's terms serially, lane = query.  Every query's
+// accumulator receives exactly the reference's addends in the reference's
+// order plus +0.0 for sources that do not overlap its own cell; an
+// accumulator that starts at +0.0 is never -0.0 (round-to-nearest gives +0.0
+// for exact cancellation), so those additions leave its bits unchanged:
+// bitwise equal.  Sources out of the CTA's span have ov <= 0 for all its
+// cells (as in k_unif_propagate's warp compaction; NaN centres stay in).
+// Two stages, named barriers (FULL: producers arrive, consumers wait; EMPTY:
+// the reverse; PROD among producers), a stage with nrows = -1 ends the run.
+constexpr int kPcQ = 32;            // queries (outputs) per CTA
+constexpr int kPcRows = 32;         // sources per stage
+constexpr int kPcProdWarps = 8;
+constexpr int kPcProd = 32 * kPcProdWarps;
+constexpr int kPcRing = 512;        // pending relevant sources (>= kPcRows - 1 + kPcProd)
+template <int kPlanes>
+__host__ __device__ constexpr int pc_threads() { return 32 * (kPlanes + kPcProdWarps); }
+template <int kPlanes>
+constexpr size_t pc_smem() {
+  return sizeof(double) * ((size_t)2 * kPlanes * kPcRows * kPcQ + (size_t)(kPlanes == 3 ? 4 : 3) * kPcRing);
+}
+
+template <int kPlanes>
+__global__ void __launch_bounds__(pc_threads<kPlanes>()) k_unif_pc(
+    const double* __restrict__ yq, int64_t n, const double* __restrict__ cpts, const double* __restrict__ cu,
+    const double* __restrict__ w, double wscale, const double* __restrict__ vals, int64_t m, double a, double h,
+    int64_t d, double rad, double* o0, double* o1, double* o2) {
+  static_assert(kPlanes == 1 || kPlanes == 3, "planes");
+  constexpr int kThreads = pc_threads<kPlanes>();
+  constexpr int kFull = 1, kEmpty = 3, kProdBar = 5;
+  extern __shared__ __align__(16) double pc_smem_[];
+  double* st = pc_smem_;                                   // [2][kPlanes][kPcRows][kPcQ]
+  double* rl = st + 2 * kPlanes * kPcRows * kPcQ;          // ring: centre - rad
+  double* rh = rl + kPcRing;                               //       centre + rad
+  double* rw = rh + kPcRing;                               //       weight / mass
+  double* rv = rw + kPcRing;                               //       value (kPlanes == 3)
+  __shared__ int s_wc[kPcProdWarps];
+  __shared__ int s_nrows[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t t0 = (int64_t)blockIdx.x * kPcQ;
+  if (warp >= kPlanes) {
+    // ------------------------------------------------------------ producers
+    const int pt = tid - 32 * kPlanes, pw = pt >> 5;
+    const int64_t tq = t0 + lane < n ? t0 + lane : n - 1;  // this thread's query (clamped)
+    const long long j = yq ? cell_index(yq[tq], a, h, d) : (long long)tq;
+    const double lj = cell_left(j, a, h), rj = cell_right(j, a, h, d);
+    double lc = lj, rc = rj;  // the CTA's span (every producer warp covers all 32 queries)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double l2 = __shfl_xor_sync(0xffffffffu, lc, o), r2 = __shfl_xor_sync(0xffffffffu, rc, o);
+      lc = l2 < lc ? l2 : lc;
+      rc = r2 > rc ? r2 : rc;
+    }
+    const unsigned below = (1u << lane) - 1u;
+    int head = 0, pend = 0, k = 0;
+    auto stage = [&](int nrows) {
+      const int buf = k & 1;
+      if (k >= 2) named_sync(kEmpty + buf, kThreads);  // consumers are done with stage k - 2
+      double* s = st + (size_t)buf * kPlanes * kPcRows * kPcQ;
+      for (int r = pw; r < nrows; r += kPcProdWarps) {  // row r, query lane
+        const int pos = (head + r) & (kPcRing - 1);
+        double lo = rl[pos], hi = rh[pos];
+        if (lo < lj) lo = lj;
+        if (hi > rj) hi = rj;
+        const double ov = hi - lo;
+        double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+        if (ov > 0.0) {
+          e0 = rw[pos] * ov;
+          if (kPlanes == 3) {
+            const double v = rv[pos];
+            e1 = e0 * v;
+            e2 = e1 * v;
+          }
+        }
+        s[r * kPcQ + lane] = e0;
+        if (kPlanes == 3) {
+          s[(kPcRows + r) * kPcQ + lane] = e1;
+          s[(2 * kPcRows + r) * kPcQ + lane] = e2;
+        }
+      }
+      if (pt == 0) s_nrows[buf] = nrows;
+      named_arrive(kFull + buf, kThreads);
+      ++k;
+    };
+    for (int64_t base = 0; base < m; base += kPcProd) {
+      const int64_t r = base + pt;
+      bool rel = false;
+      double cl = 0.0, ch = 0.0;
+      if (r < m) {
+        const double c = cu ? cpts[r] + cu[r] : cpts[r];
+        cl = c - rad;
+        ch = c + rad;
+        rel = !(ch <= lc || cl >= rc);
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, rel);
+      if (lane == 0) s_wc[pw] = __popc(mask);
+      named_sync(kProdBar, kPcProd);
+      int before = 0, total = 0;
+#pragma unroll
+      for (int q = 0; q < kPcProdWarps; ++q) {
+        const int c = s_wc[q];
+        before += q < pw ? c : 0;
+        total += c;
+      }
+      if (rel) {
+        const int pos = (head + pend + before + __popc(mask & below)) & (kPcRing - 1);
+        rl[pos] = cl;
+        rh[pos] = ch;
+        rw[pos] = wscale == 1.0 ? w[r] : wscale * w[r];
+        if (kPlanes == 3) rv[pos] = vals[r];
+      }
+      named_sync(kProdBar, kPcProd);  // ring entries visible; s_wc free again
+      pend += total;
+      UCP_DCHECK(pend < kPcRing);
+      while (pend >= kPcRows) {
+        stage(kPcRows);
+        head = (head + kPcRows) & (kPcRing - 1);
+        pend -= kPcRows;
+      }
+    }
+    if (pend > 0) stage(pend);
+    stage(-1);  // end marker
+    if (k >= 2) named_sync(kEmpty + ((k - 2) & 1), kThreads);  // the consumers' last EMPTY arrival
+  } else {
+    // ------------------------------------------------------------ consumers
+    const int plane = warp;
+    double acc = 0.0;
+    for (int k = 0;; ++k) {
+      const int buf = k & 1;
+      named_sync(kFull + buf, kThreads);
+      const int nrows = s_nrows[buf];
+      if (nrows < 0) break;
+      const double* s = st + ((size_t)buf * kPlanes + plane) * kPcRows * kPcQ + lane;
+#pragma unroll 8
+      for (int r = 0; r < nrows; ++r) acc += s[r * kPcQ];
+      named_arrive(kEmpty + buf, kThreads);
+    }
+    const int64_t t = t0 + lane;
+    if (t < n) {
+      const double inv = 1.0 / ((2.0 * rad) * h);
+      (plane == 0 ? o0 : plane == 1 ? o1 : o2)[t] = acc * inv;
+    }
+  }
+}
+
+// launch helpers (dynamic shared memory opt-in once per kernel and device);
+// -DUCP_UNIF_PC=0 builds the one-thread-per-output kernels instead (A/B)
+#ifndef UCP_UNIF_PC
+#define UCP_UNIF_PC 1
+#endif
+int launch_unif_propagate(const double* f, double mscale, const double* cpts, const double* cu, int64_t n, double a,
+                          double h, int64_t d, double rad, double* out, cudaStream_t st) {
+  if (!UCP_UNIF_PC) {
+    k_unif_propagate<<<nblocks(d, 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(f, mscale, cpts, cu, n, a, h, d, rad, out);
+    UCP_LAUNCHED("k_unif_propagate");
+    return UCP_OK;
+  }
+  smem_opt_in(reinterpret_cast<const void*>(k_unif_pc<1>), pc_smem<1>());
+  k_unif_pc<1><<<nblocks(d, kPcQ), pc_threads<1>(), pc_smem<1>(), st>>>(nullptr, d, cpts, cu, f, mscale, nullptr, n,
+                                                                        a, h, d, rad, out, nullptr, nullptr);
+  UCP_LAUNCHED("k_unif_pc<1>");
+  return UCP_OK;
+}
+int launch_unif_moments_points(const double* y, int64_t n, const double* centers, const double* w,
+                               const double* vals, int64_t m, double a, double h, int64_t d, double rad, double* m0,
+                               double* m1, double* m2, cudaStream_t st) {
+  if (!UCP_UNIF_PC) {
+    k_unif_moments_points<<<nblocks(n, 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(y, n, centers, w, vals, m, a, h, d,
+                                                                                   rad, m0, m1, m2);
+    UCP_LAUNCHED("k_unif_moments_points");
+    return UCP_OK;
+  }
+  smem_opt_in(reinterpret_cast<const void*>(k_unif_pc<3>), pc_smem<3>());
+  k_unif_pc<3><<<nblocks(n, kPcQ), pc_threads<3>(), pc_smem<3>(), st>>>(y, n, centers, nullptr, w, 1.0, vals, m, a, h,
+                                                                        d, rad, m0, m1, m2);
+  UCP_LAUNCHED("k_unif_pc<3>");
+  return UCP_OK;
+}
+
 // ------------------------------------------------------- cost functors
 // zero_delay.py:69-76: C0(u, y_i) = f0_i (pw u^2 + E[(y - u1(x1))^2]), x1 = u + w
 struct ZdCost0 {
@@ -670,9 +859,9 @@ int zd_moments(const ucp_zd_problem* P, const double* u0, const double* yq, int6
   int rc;
   if ((rc = ws_get(ws, WS_MOM, sizeof(double) * 3 * (size_t)nq, &pm))) return rc;
   double* m0 = (double*)pm;
-  k_unif_moments_points<<<nblocks(nq, 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(
-      yq, nq, u0, P->fw0, P->y0, P->d0, P->a1, P->h1, P->d1, 1.0, m0, m0 + nq, m0 + 2 * nq);
-  UCP_LAUNCHED("k_unif_moments_points");
+  if ((rc = launch_unif_moments_points(yq, nq, u0, P->fw0, P->y0, P->d0, P->a1, P->h1, P->d1, 1.0, m0, m0 + nq,
+                                       m0 + 2 * nq, st)))
+    return rc;
   q->A = m0;
   q->B = m0 + nq;
   q->C = m0 + 2 * nq;
@@ -741,19 +930,14 @@ int inv_density0(const ucp_inv_problem* P, ucp_workspace* ws, cudaStream_t st, d
   static const double one_zero[2] = {1.0, 0.0};
   UCP_CHECK(cudaMemcpyAsync(pone, one_zero, sizeof one_zero, cudaMemcpyHostToDevice, st));
   const double* one = (const double*)pone;
-  k_unif_propagate<<<nblocks(P->d[0], 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(one, 1.0, one + 1, nullptr, 1,
-                                                                                   P->a[0], P->h[0], P->d[0], 1.0, out);
-  UCP_LAUNCHED("k_unif_propagate");
-  return UCP_OK;
+  return launch_unif_propagate(one, 1.0, one + 1, nullptr, 1, P->a[0], P->h[0], P->d[0], 1.0, out, st);
 }
 
 // f_{mm+1} = unif_propagate(h_mm * f_mm, pts_mm + u_mm, grid mm+1)
 int inv_density_step(const ucp_inv_problem* P, int mm, const double* const* u, const double* f, double* out,
                       cudaStream_t st) {
-  k_unif_propagate<<<nblocks(P->d[mm + 1], 32 * kUnifWarps), 32 * kUnifWarps, 0, st>>>(
-      f, P->h[mm], P->pts[mm], u[mm], P->d[mm], P->a[mm + 1], P->h[mm + 1], P->d[mm + 1], 1.0, out);
-  UCP_LAUNCHED("k_unif_propagate");
-  return UCP_OK;
+  return launch_unif_propagate(f, P->h[mm], P->pts[mm], u[mm], P->d[mm], P->a[mm + 1], P->h[mm + 1], P->d[mm + 1], 1.0,
+                               out, st);
 }
 
 // g_M = gamma(terminal state points), on grid inv_state(M)
@@ -913,10 +1097,7 @@ int ucp_unif_ball_sum(const double* x, int64_t n, const double* g, double a, dou
 int ucp_unif_propagate(const double* masses, const double* centers, int64_t n, double a, double h, int64_t d,
                        double rad, double* out, void* stream) {
   if (n < 0 || d < 2) return arg_fail("unif_propagate: bad sizes");
-  k_unif_propagate<<<nblocks(d, 32 * kUnifWarps), 32 * kUnifWarps, 0, as_stream(stream)>>>(
-      masses, 1.0, centers, nullptr, n, a, h, d, rad, out);
-  UCP_LAUNCHED("k_unif_propagate");
-  return UCP_OK;
+  return launch_unif_propagate(masses, 1.0, centers, nullptr, n, a, h, d, rad, out, as_stream(stream));
 }
 
 int ucp_unif_moments_points(const double* y, int64_t n, const double* centers, const double* w, const double* vals,
@@ -924,10 +1105,7 @@ int ucp_unif_moments_points(const double* y, int64_t n, const double* centers, c
                             double* m2, void* stream) {
   if (n < 0 || m < 0 || d < 2) return arg_fail("unif_moments_points: bad sizes");
   if (n == 0) return UCP_OK;
-  k_unif_moments_points<<<nblocks(n, 32 * kUnifWarps), 32 * kUnifWarps, 0, as_stream(stream)>>>(
-      y, n, centers, w, vals, m, a, h, d, rad, m0, m1, m2);
-  UCP_LAUNCHED("k_unif_moments_points");
-  return UCP_OK;
+  return launch_unif_moments_points(y, n, centers, w, vals, m, a, h, d, rad, m0, m1, m2, as_stream(stream));
 }
 
 // ---------------------------------------------------------------- ZeroDelay

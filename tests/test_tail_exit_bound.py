@@ -36,10 +36,11 @@ def test_absorption_lemma():
         assert bits(acc + t) == bits(acc)
 
 
-def walk(s, a, h, v, exit_rule):
+def walk(s, a, h, v, exit_rule, chunk=256):
     """Stage-0 walk over nodes a + j*h within s +- 12 (interior weight h, half
     weight at the grid ends), in the reference's order; with exit_rule the
-    walk stops between 64-node chunks once the bounds of walk_tail_noop pass."""
+    walk stops between ``chunk``-node chunks (the kernel's 4 x UCP_WALK_CHUNK4)
+    once the bounds of walk_tail_noop pass."""
     d = len(v)
     q = math.exp(-h * h)
     jlo = max(0, math.ceil(((s - 12.0) - a) / h))
@@ -52,7 +53,7 @@ def walk(s, a, h, v, exit_rule):
     ratio = math.exp(-h * (tt + 0.5 * h))
     visited = 0
     for j in range(jlo, jhi + 1):
-        if exit_rule and (j - jlo) % 64 == 0 and j > jlo and ratio <= 1.0:
+        if exit_rule and (j - jlo) % chunk == 0 and j > jlo and ratio <= 1.0:
             vm = max(abs(x) for x in v[j:jhi + 1])
             wpc = h * pdf
             b1 = wpc * vm
@@ -72,8 +73,9 @@ def walk(s, a, h, v, exit_rule):
     return acc0, acc1, acc2, visited
 
 
+@pytest.mark.parametrize("chunk", [64, 256])
 @pytest.mark.parametrize("kind", ["smooth", "spikes", "odd", "huge"])
-def test_tail_exit_walk_bitwise(kind):
+def test_tail_exit_walk_bitwise(kind, chunk):
     rng = random.Random(["smooth", "spikes", "odd", "huge"].index(kind) + 11)
     a, h, d = -25.0, 50.0 / 2047, 2048
     xs = [a + j * h for j in range(d)]
@@ -89,7 +91,7 @@ def test_tail_exit_walk_bitwise(kind):
     saved = 0
     for s in [a + rng.random() * 50.0 for _ in range(60)] + [0.0, -25.0, 25.0, 13.0]:
         full = walk(s, a, h, v, False)
-        fast = walk(s, a, h, v, True)
+        fast = walk(s, a, h, v, True, chunk)
         assert [bits(x) for x in fast[:3]] == [bits(x) for x in full[:3]], (kind, s)
         saved += full[3] - fast[3]
     if kind != "odd":

@@ -41,18 +41,23 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", default=",".join(CASES))
     ap.add_argument("--cpu-rounds", type=int, default=1, help="rounds of the CPU oracle per case (0: skip)")
+    ap.add_argument("--reps", type=int, default=5, help="timed solves per case (median reported)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     for name in args.cases.split(","):
         kind, M, d = CASES[name]
         prob = make(kind, M, d, "gpu")
         P.solve(prob, P.SolverConfig(max_rounds=1))  # context + first launches
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        res = P.solve(prob, P.SolverConfig())
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t
+        walls = []
+        for _ in range(args.reps):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            res = P.solve(prob, P.SolverConfig())
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t)
+        wall = float(sorted(walls)[len(walls) // 2])
         line = {"case": name, "problem": kind, "stages": prob.M, "d": d, "gpu_solve_s": wall,
+                "gpu_solve_s_all": [round(w, 5) for w in walls],
                 "rounds": res.total_rounds, "J": res.final_objective, "termination": res.termination,
                 "gpu_s_per_round": wall / res.total_rounds}
         if args.cpu_rounds > 0:

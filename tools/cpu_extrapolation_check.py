@@ -2,6 +2,9 @@
 algorithm -- the oracle's C/OpenMP port -- timed on bounded samples of every
 phase, scaled by d/n): at grid sizes where a FULL CPU step is affordable, time
 the full step phase by phase next to the sampled estimate and report the error.
+(A single uniform sample -- the same few hundred points in every phase,
+value = sampled evaluations / seconds -- was tried: per-call overheads of the
+cheap phases put it 57% off at 2^16, so each phase keeps its own sample size.)
 
     python tools/cpu_extrapolation_check.py [--log2d 14 16] [--cpu-seconds 8]
 
@@ -41,8 +44,9 @@ def main():
         r = (args.window_nodes / 2.0) * p.h0
         cfg = orc.OracleConfig(search_radius=r)
         counts = bench.workload_counts(u0, u1, d, r)
-        est, est_phase, thr, sample, outs = bench.cpu_step_seconds(orc, p, u0, u1, d, r, args.cpu_seconds,
-                                                                   counts["cand0"] / d)
+        q = bench.cpu_sample_step(orc, p, u0, u1, d, r, counts, args.cpu_seconds)
+        est, thr, sample, outs = q["step_s_extrapolated"], q["threads"], q["sample"], q["outs"]
+        est_phase = q["phase_s"]
         full, full_out = {}, {}
         for name, fn in (("local0", lambda: orc.local_update_phase(p, 0, u0, u1, cfg)),
                          ("local1", lambda: orc.local_update_phase(p, 1, u0, u1, cfg)),

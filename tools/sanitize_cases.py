@@ -13,7 +13,8 @@ sanitizer run is also a parity run:
            (UCP_FUSED_MAX_QUERIES=0 is set by this script for that case: run it
            in its own process, e.g. ``... sanitize_cases.py moments``)
   batch    solve_many of 6 instances at d=201 (batched engine work queues)
-  c5       ZeroDelay d=257 and Inventory M=3 d=129, two rounds each
+  c5       ZeroDelay and Inventory M=3 (small and ~2k-4k grids), two rounds each, and the
+           uniform-noise kernels vs the oracle
   mc       Philox Monte-Carlo objective, 2^16 samples
 """
 from __future__ import annotations
@@ -97,8 +98,24 @@ def main(argv):
                 same(r.final_objective, J, f"batch J k={k} sigma={s}")
         elif case == "c5":
             for prob in (P.ZeroDelay(grids=[(-5.0, 5.0, 257), (-6.0, 6.0, 257)]),
-                         P.Inventory(stages=3, grids=[(-3.0, 3.0, 129)] * 3)):
+                         P.Inventory(stages=3, grids=[(-3.0, 3.0, 129)] * 3),
+                         P.ZeroDelay(grids=[(-5.0, 5.0, 3000), (-6.0, 6.0, 2048)]),
+                         P.Inventory(stages=3, grids=[(-3.0, 3.0, 1500)] * 3)):
                 P.solve(prob, P.SolverConfig(max_rounds=2))
+            # the uniform-noise kernels (producer/consumer form) vs the oracle, many stages per CTA
+            rng = np.random.default_rng(9)
+            d, a, h = 4096, -3.0, 6.0 / 4095
+            x = np.sort(rng.uniform(-4.0, 4.0, 3000))
+            x[rng.choice(3000, 40, replace=False)] = rng.uniform(-4.0, 4.0, 40)  # out of order
+            masses = rng.uniform(0.0, 1.0, 3000)
+            same(P.kernels.unif_propagate(masses, x, a, h, d, 1.0), orc.unif_propagate(masses, x, a, h, d, 1.0),
+                 "unif_propagate")
+            y = rng.uniform(-3.2, 3.2, 5000)
+            vals = rng.normal(0.0, 2.0, 3000)
+            got = P.kernels.unif_moments_points(y, x, masses, vals, a, h, d, 1.0)
+            want = orc.unif_moments_points(y, x, masses, vals, a, h, d, 1.0)
+            for k in range(3):
+                same(got[k], want[k], f"unif_moments_points {k}")
         elif case == "mc":
             prob = P.Witsenhausen(grids=[(-25.0, 25.0, 2001)] * 2)
             P.device_monte_carlo_objective(prob, prob.identity_controllers(), 1 << 16, seed=3)
