@@ -941,7 +941,13 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 constexpr int kMomThreads = 128;
 // kUnroll pairs' exp() in flight per thread; the batched engine (few CTAs per
 // SM) instantiates a deeper unroll with a looser register bound.
-template <int kMomUnroll = 4, int kMinBlocks = 6, int kQT = kMomThreads>
+#ifndef UCP_MOM_UNROLL
+#define UCP_MOM_UNROLL 16
+#endif
+#ifndef UCP_MOM_MINB
+#define UCP_MOM_MINB 2
+#endif
+template <int kMomUnroll = UCP_MOM_UNROLL, int kMinBlocks = UCP_MOM_MINB, int kQT = kMomThreads>
 __global__ void __launch_bounds__(kQT, kMinBlocks)
 k_moments(const double* __restrict__ yq, int64_t n, const double2* __restrict__ xw,
           const double2* __restrict__ tails, int64_t m, const double2* __restrict__ tile_mm, double a, double h,
@@ -1494,7 +1500,9 @@ static_assert(WS_NSLOTS <= 24, "workspace slots");
 // have enough query blocks to fill the GPU); env UCP_FUSED_MAX_QUERIES
 const int64_t kFusedMaxQueries = [] {
   const char* e = getenv("UCP_FUSED_MAX_QUERIES");
-  return e ? (int64_t)atoll(e) : (int64_t)16384;  // crossover measured with tools/moments_sweep.py
+  // crossover measured with tools/moments_sweep.py: ~8.7k queries since the
+  // persistent kernel keeps 16 exps in flight (it was 16k at 4)
+  return e ? (int64_t)atoll(e) : (int64_t)8704;
 }();
 // warp-per-point candidate fill below this many points (one thread per point above)
 constexpr int64_t kWarpFillMaxPoints = 1 << 16;

@@ -238,11 +238,13 @@ def test_no_cpu_fallback_and_launches(P):
     assert _lib.LIB_PATH.exists()
 
 
-@pytest.mark.parametrize("nq,m", [(10_000, 4096), (9000, 257), (20_000, 4096), (17_000, 257), (3, 5000)])
+@pytest.mark.parametrize("nq,m", [(8000, 4096), (8704, 257), (10_000, 4096), (9000, 257), (20_000, 4096),
+                                  (17_000, 257), (3, 5000)])
 def test_moments_direct_path_vs_oracle(P, oracle_mod, nq, m):
-    """Both moments kernels on unsorted queries: up to 16,384 queries the fused
-    producer/consumer kernel, above it the persistent tiled kernel (tile
-    skipping, edge blocks, work queue); bitwise vs the oracle."""
+    """Both moments kernels on unsorted queries: up to 8,704 queries (the
+    default UCP_FUSED_MAX_QUERIES) the fused producer/consumer kernel, above
+    it the persistent tiled kernel (tile skipping, edge blocks, work queue);
+    bitwise vs the oracle."""
     rng = np.random.default_rng(nq)
     a, b = -20.0, 20.0
     h = (b - a) / (m - 1)
