@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define UCP_ABI_VERSION 2
+#define UCP_ABI_VERSION 3
 
 enum ucp_status {
   UCP_OK = 0,
@@ -54,7 +54,18 @@ typedef struct ucp_wc_problem {
   const double* y1;  /* [d1] */
   const double* f0;  /* [d0] */
   const double* fw0; /* [d0] */
+  int64_t flags;     /* UCP_WC_FAST or 0 (the reference's arithmetic, bitwise) */
 } ucp_wc_problem;
+
+/* ucp_wc_problem.flags: stage-0 walks in the tolerance-stated fast mode --
+ * h folded into the pdf recurrence and FMA in the v-weighted sums (6 FP64
+ * instructions per node instead of 8).  NOT bitwise the reference: moments
+ * agree to rounding (~1e-15 relative), costs within 1e-10 relative (the
+ * quadratic in s cancels), argmin picks may differ on near-ties only, J of a
+ * snapshot within 1e-13 relative; a full solve may branch at a near-tie (the
+ * d=2000 solve converges 4.9e-7 relative below the reference's J) -- stated
+ * and tested in tests/test_gpu_fast_mode.py. */
+#define UCP_WC_FAST 1
 
 /* Local-update parameters (solver.py:47-97, SolverConfig), already resolved
  * per stage (newton_cap = cfg.cap_for(grid)). */

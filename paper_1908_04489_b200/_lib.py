@@ -17,6 +17,8 @@ UCP_OK = 0
 UCP_ERR_ARG = 1
 UCP_ERR_CUDA = 3
 NO_ERROR = (1 << 63) - 1  # UCP_NO_ERROR
+ABI_VERSION = 3  # UCP_ABI_VERSION (3: ucp_wc_problem.flags)
+WC_FAST = 1  # UCP_WC_FAST
 
 c_i64 = ctypes.c_int64
 c_dbl = ctypes.c_double
@@ -32,6 +34,7 @@ class WcProblem(ctypes.Structure):
         ("a0", c_dbl), ("h0", c_dbl), ("d0", c_i64),
         ("a1", c_dbl), ("h1", c_dbl), ("d1", c_i64),
         ("y0", c_vp), ("y1", c_vp), ("f0", c_vp), ("fw0", c_vp),
+        ("flags", c_i64),
     ]
 
 
@@ -100,8 +103,8 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.ucp_abi_version() != 2:
-        raise ImportError(f"libucp_b200 ABI {lib.ucp_abi_version()} != 2")
+    if lib.ucp_abi_version() != ABI_VERSION:
+        raise ImportError(f"libucp_b200 ABI {lib.ucp_abi_version()} != {ABI_VERSION}")
     _LIB = lib
     return lib
 

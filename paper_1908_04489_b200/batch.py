@@ -79,8 +79,8 @@ def batchable(problems) -> bool:
 
     if len(problems) < 2 or len(problems) > MAX_BATCH:
         return False
-    if not all(type(p) is Witsenhausen for p in problems):
-        return False
+    if not all(type(p) is Witsenhausen and p.arithmetic == "reference" for p in problems):
+        return False  # (the batched engine runs the reference's arithmetic only)
     g = problems[0].grids
     return all(p.grids == g for p in problems[1:])
 

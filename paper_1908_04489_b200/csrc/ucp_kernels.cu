@@ -178,6 +178,9 @@ struct WalkGrid {
   int nb;
   // instrumentation (ucp_walk_node_counter): visited walk nodes are added here
   unsigned long long* visits;
+  // UCP_WC_FAST (ucp_wc_problem.flags): the tolerance-stated FMA walk
+  // (gauss_walk_impl<kMode, true>); 0 = the reference's arithmetic
+  int fast;
 };
 constexpr int kVsufShift = 8;  // 256 nodes per block
 
@@ -201,8 +204,9 @@ constexpr BatchArgs kNoBatch = {nullptr, 0, 0, 0, 0, nullptr};
 // ucp_walk_node_counter (instrumentation only); read once per walk grid
 std::atomic<unsigned long long*> g_visits{nullptr};
 
-WalkGrid make_walk_grid(double a, double h, int64_t d) {
+WalkGrid make_walk_grid(double a, double h, int64_t d, int fast = 0) {
   WalkGrid g;
+  g.fast = fast;
   g.a = a;
   g.h = h;
   g.d = d;
@@ -268,8 +272,14 @@ __device__ __forceinline__ double range_max(const double* __restrict__ t, int nb
   return fmax(__ldg(lv + bl), __ldg(lv + br - (1 << k) + 1));
 }
 
-template <int kMode>
-__device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__ v, const WalkGrid g) {
+// kFast (UCP_WC_FAST, opt-in, NOT the reference's arithmetic): h is folded
+// into the pdf recurrence (p = h*pdf) and the v-weighted sums use FMA --
+// acc1 = fma(p, v, acc1), acc2 = fma(p*v, v, acc2) -- 6 FP64 instructions
+// per interior node instead of 8.  Same nodes, same order, same exp/erf,
+// same no-op tail exit; every sum differs from the reference by rounding
+// only (tests/test_gpu_fast_mode.py states and checks the tolerance).
+template <int kMode, bool kFast>
+__device__ __forceinline__ Mom3 gauss_walk_impl(double st, const double* __restrict__ v, const WalkGrid g) {
   constexpr bool kLat = kMode != 0;
   long long jlo = (long long)ceil(((st - kGaussCut) - g.a) / g.h);
   long long jhi = (long long)floor(((st + kGaussCut) - g.a) / g.h);
@@ -282,18 +292,24 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
     double tt = (g.a + (double)jlo * h) - st;
     double pdf = ucp_exp_tab((-0.5 * tt) * tt, g_exp_tab) * inv_sqrt_2pi();
     double ratio = ucp_exp_tab((-h) * (tt + 0.5 * h), g_exp_tab);
+    if (kFast) pdf = h * pdf;  // p = h * pdf: interior weight 1, end weight 1/2
     const int last = (int)(g.d - 1);
     const int je = (int)jhi;
     int j = (int)jlo;
-#define UCP_WALK_STEP_V(W, VJ)      \
-  {                                 \
-    double wp = (W) * pdf;          \
-    acc0 += wp;                     \
-    double wv = wp * (VJ);          \
-    acc1 += wv;                     \
-    acc2 += wv * (VJ);              \
-    pdf *= ratio;                   \
-    ratio *= q;                     \
+#define UCP_WALK_STEP_V(W, VJ)                   \
+  {                                              \
+    double wp = (W) * pdf;                       \
+    acc0 += wp;                                  \
+    if (kFast) {                                 \
+      acc1 = __fma_rn(wp, (VJ), acc1);           \
+      acc2 = __fma_rn(wp * (VJ), (VJ), acc2);    \
+    } else {                                     \
+      double wv = wp * (VJ);                     \
+      acc1 += wv;                                \
+      acc2 += wv * (VJ);                         \
+    }                                            \
+    pdf *= ratio;                                \
+    ratio *= q;                                  \
   }
 #define UCP_WALK_STEP(W)                      \
   {                                           \
@@ -303,7 +319,8 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
     if (kMode == 1) {
       for (int p = j & ~15; p <= je; p += 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(v + p));
     }
-    const double hh = 0.5 * h;
+    const double hw = kFast ? 1.0 : h;         // interior node weight (folded into p in fast mode)
+    const double hh = kFast ? 0.5 : 0.5 * h;   // end node weight
     if (j == 0) {
       UCP_WALK_STEP(hh);
       ++j;
@@ -312,7 +329,7 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
     // interior nodes, two per 16-byte load (v1 is 16-byte aligned: checked
     // by the host); an odd first node is peeled so the order is unchanged
     if ((j & 1) && j <= jint) {
-      UCP_WALK_STEP(h);
+      UCP_WALK_STEP(hw);
       ++j;
     }
     if (kLat) {
@@ -322,17 +339,17 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
         for (; j + 7 <= jint; j += 4) {
           const double2 n0 = walk_ld2<kMode>(v, j + 4);
           const double2 n1 = walk_ld2<kMode>(v, j + 6);
-          UCP_WALK_STEP_V(h, p0.x);
-          UCP_WALK_STEP_V(h, p0.y);
-          UCP_WALK_STEP_V(h, p1.x);
-          UCP_WALK_STEP_V(h, p1.y);
+          UCP_WALK_STEP_V(hw, p0.x);
+          UCP_WALK_STEP_V(hw, p0.y);
+          UCP_WALK_STEP_V(hw, p1.x);
+          UCP_WALK_STEP_V(hw, p1.y);
           p0 = n0;
           p1 = n1;
         }
-        UCP_WALK_STEP_V(h, p0.x);
-        UCP_WALK_STEP_V(h, p0.y);
-        UCP_WALK_STEP_V(h, p1.x);
-        UCP_WALK_STEP_V(h, p1.y);
+        UCP_WALK_STEP_V(hw, p0.x);
+        UCP_WALK_STEP_V(hw, p0.y);
+        UCP_WALK_STEP_V(hw, p1.x);
+        UCP_WALK_STEP_V(hw, p1.y);
         j += 4;
       }
     } else {
@@ -345,13 +362,13 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
         for (int c = 0; c < kWalkChunk4; ++c, j += 4) {
           const double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
           const double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
-          UCP_WALK_STEP_V(h, p0.x);
-          UCP_WALK_STEP_V(h, p0.y);
-          UCP_WALK_STEP_V(h, p1.x);
-          UCP_WALK_STEP_V(h, p1.y);
+          UCP_WALK_STEP_V(hw, p0.x);
+          UCP_WALK_STEP_V(hw, p0.y);
+          UCP_WALK_STEP_V(hw, p1.x);
+          UCP_WALK_STEP_V(hw, p1.y);
         }
         if (vsuf && ratio <= 1.0 && j <= jint &&
-            walk_tail_noop(pdf, ratio, h, range_max(vsuf, g.nb, j >> kVsufShift, je >> kVsufShift), acc0, acc1,
+            walk_tail_noop(pdf, ratio, hw, range_max(vsuf, g.nb, j >> kVsufShift, je >> kVsufShift), acc0, acc1,
                            acc2)) {
           // every remaining node (incl. a half-weight last one) is a no-op; j > je
           // skips them and encodes the first unvisited node for the node counter
@@ -362,13 +379,13 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
       for (; j + 3 <= jint; j += 4) {
         const double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
         const double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
-        UCP_WALK_STEP_V(h, p0.x);
-        UCP_WALK_STEP_V(h, p0.y);
-        UCP_WALK_STEP_V(h, p1.x);
-        UCP_WALK_STEP_V(h, p1.y);
+        UCP_WALK_STEP_V(hw, p0.x);
+        UCP_WALK_STEP_V(hw, p0.y);
+        UCP_WALK_STEP_V(hw, p1.x);
+        UCP_WALK_STEP_V(hw, p1.y);
       }
     }
-    for (; j <= jint; ++j) UCP_WALK_STEP(h);
+    for (; j <= jint; ++j) UCP_WALK_STEP(hw);
     if (je == last && j == last) UCP_WALK_STEP(hh);
     UCP_DCHECK(jlo >= 0 && je <= last && j >= jint + 1 && j <= je + 1 + (int)(je - jlo + 1));
     if (!kLat && g.visits) {  // instrumentation: nodes this walk visited
@@ -389,6 +406,15 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
   r.t1 = (acc1 + lo * v0) + hi * vl;
   r.t2 = (acc2 + (lo * v0) * v0) + (hi * vl) * vl;
   return r;
+}
+
+template <int kMode>
+__device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__ v, const WalkGrid g) {
+#ifdef UCP_NO_FAST_WALK  // (PTX audit of the reference-arithmetic walk: tests/test_abi_and_host.py)
+  return gauss_walk_impl<kMode, false>(st, v, g);
+#else
+  return g.fast ? gauss_walk_impl<kMode, true>(st, v, g) : gauss_walk_impl<kMode, false>(st, v, g);
+#endif
 }
 
 // witsenhausen.py:31-33 (_quad_in_u): a*u*u - 2.0*b*u + c
@@ -1814,7 +1840,7 @@ int ucp_wc_stage0_cost(const ucp_wc_problem* P, const double* v1, const double* 
   if (nseg == 0 || n_cand == 0) return UCP_OK;
   const int64_t n_host = n_cand;
   if (int rc_ = check_aligned(v1)) return rc_;
-  WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
+  WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1, (int)(P->flags & UCP_WC_FAST));
   UCP_WALK_LAUNCH(k_stage0_segmented, n_host, nblocks(n_host, kWalkThreads), as_stream(stream), P->d1, u_flat, offsets, nseg, y_seg,
                                                                            f0_seg, P->k, v1, g, out);
   UCP_LAUNCHED("k_stage0_segmented");
@@ -1858,7 +1884,7 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
     void* pc;
     if ((rc = ws_get(ws, WS_COST, sizeof(double) * 3 * (size_t)n, &pc))) return rc;
     if (int rc_ = check_aligned(u1)) return rc_;
-    WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
+    WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1, (int)(P->flags & UCP_WC_FAST));
     if ((rc = attach_vsuf(&g, u1, 3 * n, ws, st))) return rc;
     UCP_WALK_LAUNCH_PDL(k_lu0_probe, 3 * n, nblocks(3 * n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
                                                      (double*)pc, kNoBatch);
@@ -1947,7 +1973,7 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
                                                (int32_t*)pj);
   UCP_LAUNCHED("k_ex_fill");
   if (int rc_ = check_aligned(u1)) return rc_;
-  WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
+  WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1, (int)(P->flags & UCP_WC_FAST));
   if ((rc = attach_vsuf(&g, u1, total, ws, st))) return rc;
   UCP_WALK_LAUNCH(k_ex0_eval, total, nblocks(total, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, counts + n,
                                                   (const int32_t*)ppt, (const int32_t*)pj, (double*)pc, kNoBatch);
@@ -2128,7 +2154,7 @@ int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const doub
   if (begin < 0 || end > P->d0 || begin > end) return arg_fail("objective_terms: bad shard");
   if (end == begin) return UCP_OK;
   if (int rc_ = check_aligned(u1)) return rc_;
-  WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1);
+  WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1, (int)(P->flags & UCP_WC_FAST));
   UCP_WALK_LAUNCH(k_obj_terms, end - begin, nblocks(end - begin, kWalkThreads), as_stream(stream), P->d1, P->y0, P->f0, u0, P->k, u1, g,
                                                                           begin, end, terms, err, kNoBatch);
   UCP_LAUNCHED("k_obj_terms");

@@ -70,13 +70,25 @@ class _WcDevice(DeviceContext):
         self.f0 = to_device_f64(prob._f0, self.device)
         self.fw0 = to_device_f64(prob._fw0, self.device)
         self.P = _lib.WcProblem(prob.k, g0.a, g0.spacing, g0.d, g1.a, g1.spacing, g1.d,
-                                ptr(self.y0), ptr(self.y1), ptr(self.f0), ptr(self.fw0))
+                                ptr(self.y0), ptr(self.y1), ptr(self.f0), ptr(self.fw0),
+                                _lib.WC_FAST if prob.arithmetic == "fma" else 0)
 
 
 class Witsenhausen(Problem):
     name = "witsenhausen"
 
-    def __init__(self, k: float = 0.2, sigma: float = 5.0, grids=None, device=None):
+    ARITHMETIC = ("reference", "fma")
+
+    def __init__(self, k: float = 0.2, sigma: float = 5.0, grids=None, device=None, arithmetic: str = "reference"):
+        """``arithmetic``: "reference" (default) evaluates every stage-0 walk in
+        the reference's exact operation order -- results bitwise the reference's;
+        "fma" is the opt-in, tolerance-stated fast mode (h folded into the pdf
+        recurrence, FMA in the v-weighted sums: 6 instead of 8 FP64 instructions
+        per walk node; costs equal to rounding, argmin picks may differ on
+        near-ties -- tests/test_gpu_fast_mode.py states the tolerance)."""
+        if arithmetic not in self.ARITHMETIC:
+            raise ValueError(f"witsenhausen.arithmetic must be one of {self.ARITHMETIC} (got {arithmetic!r})")
+        self.arithmetic = arithmetic
         if not k > 0.0:
             raise ValueError(f"witsenhausen.k must be positive (got {k})")
         if not sigma > 0.0:

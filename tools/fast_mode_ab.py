@@ -1,0 +1,50 @@
+"""Reference vs fast (arithmetic="fma") arithmetic on the bench snapshot: one
+step of every phase per mode, event-timed, plus how the outputs differ.
+
+    python tools/fast_mode_ab.py [--log2d 18]
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+import paper_1908_04489_b200 as P  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--log2d", type=int, default=18)
+ap.add_argument("--reps", type=int, default=2)
+args = ap.parse_args()
+d = 1 << args.log2d
+sol = np.load(ROOT / "tests" / "golden" / "wc_solve_d2000.npz")
+u0, u1 = bench.resample(sol["u0"], d), bench.resample(sol["u1"], d)
+out = {}
+for mode in ("reference", "fma"):
+    prob = P.Witsenhausen(grids=[(-25.0, 25.0, d)] * 2, arithmetic=mode)
+    cfg = P.SolverConfig(search_radius=19.5 * prob.grids[0].spacing)
+    U = P.ControllerSet((P.SampledController(prob.grids[0], u0), P.SampledController(prob.grids[1], u1)))
+    ms, res = {}, {}
+    for rep in range(args.reps + 1):
+        for name, kind, m in bench.PHASES:
+            sweep = prob.device_local_update if kind == "local" else prob.device_exhaustion
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = sweep(m, U, cfg)
+            e1.record()
+            torch.cuda.synchronize()
+            if rep:
+                ms[name] = ms.get(name, 0.0) + e0.elapsed_time(e1) / args.reps
+            res[name] = r.cpu().numpy()
+        res["J"] = prob.device_objective(U)
+    out[mode] = (ms, res)
+ref, fast = out["reference"][1], out["fma"][1]
+line = {"log2d": args.log2d, "ms_reference": out["reference"][0], "ms_fma": out["fma"][0],
+        "speedup": {k: out["reference"][0][k] / out["fma"][0][k] for k in out["fma"][0]},
+        "points_differing": {k: int(np.count_nonzero(ref[k] != fast[k])) for k in ("local0", "local1", "exh0", "exh1")},
+        "J_reference": ref["J"], "J_fma": fast["J"], "J_rel_diff": abs(fast["J"] - ref["J"]) / ref["J"]}
+print(json.dumps(line), flush=True)
