@@ -360,6 +360,11 @@ int ucp_comm_unique_id(unsigned char* id /* [UCP_COMM_ID_BYTES] */);
 int ucp_comm_init(int nranks, int rank, const unsigned char* id, ucp_comm** comm);
 int ucp_comm_destroy(ucp_comm* comm);
 int ucp_allgather_f64(ucp_comm* comm, const double* send, double* recv, int64_t count, void* stream);
+/* Uneven in-place all-gather of a phase's output in the natural layout: rank r
+ * owns buf[bounds[r] .. bounds[r+1]) (bounds: nranks+1 ascending entries, the
+ * work-balanced plan) and every rank ends with the whole vector.  Grouped
+ * ncclBroadcast, one per non-empty shard. */
+int ucp_allgatherv_f64(ucp_comm* comm, double* buf, const int64_t* bounds, void* stream);
 int ucp_allreduce_min_i64(ucp_comm* comm, int64_t* buf, int64_t count, void* stream);
 
 /* ---- instrumentation ------------------------------------------------------

@@ -39,7 +39,7 @@ from .solver import (
 from .verify import OracleConfig, exhaustive_argmin, monte_carlo_objective, windowed_argmin
 from .montecarlo import device_monte_carlo_objective
 from .batch import solve_batch
-from .comm import NcclComm
+from .comm import CommSharding, NcclComm
 from .witsenhausen import Witsenhausen
 from .config5 import Inventory, ZeroDelay
 
@@ -72,7 +72,7 @@ __all__ = [
     "BACKEND", "ControllerSet", "Density", "Gaussian", "Grid", "LOCAL", "NumericError", "Problem",
     "REGISTRY", "RoundReport", "SampledController", "Sharding", "SolveResult", "SolverConfig", "Uniform",
     "Witsenhausen", "ZeroDelay", "Inventory", "adaptive_allocation", "eval_controller", "eval_controller_many", "from_process_group",
-    "init_identity", "local_update_phase", "fd_first", "fd_second", "OracleConfig", "exhaustive_argmin", "monte_carlo_objective", "device_monte_carlo_objective", "solve_batch", "NcclComm",
+    "init_identity", "local_update_phase", "fd_first", "fd_second", "OracleConfig", "exhaustive_argmin", "monte_carlo_objective", "device_monte_carlo_objective", "solve_batch", "NcclComm", "CommSharding",
     "windowed_argmin", "make_grid", "make_problem", "max_workers", "nearest_index",
     "nearest_indices", "newton_or_gradient_step", "node_window_bounds", "partial_exhaustion_phase", "pdf",
     "run_block", "set_workers", "solve", "solve_many", "trapezoid", "window_bounds", "window_indices", "__version__",

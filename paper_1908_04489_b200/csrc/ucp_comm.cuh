@@ -27,6 +27,9 @@ struct NcclApi {
   ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                              cudaStream_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
   bool ok = false;
 };
 
@@ -43,7 +46,11 @@ const NcclApi& nccl_api() {
     a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
     a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
     a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
-    a.ok = a.get_unique_id && a.init_rank && a.destroy && a.all_gather && a.all_reduce && a.error_string;
+    a.broadcast = reinterpret_cast<decltype(a.broadcast)>(dlsym(h, "ncclBroadcast"));
+    a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+    a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+    a.ok = a.get_unique_id && a.init_rank && a.destroy && a.all_gather && a.all_reduce && a.error_string &&
+           a.broadcast && a.group_start && a.group_end;
     return a;
   }();
   return api;
@@ -105,6 +112,31 @@ int ucp_allgather_f64(ucp_comm* comm, const double* send, double* recv, int64_t 
   if (count == 0) return UCP_OK;
   ncclResult_t r = nccl_api().all_gather(send, recv, (size_t)count, ncclFloat64, comm->comm, as_stream(stream));
   if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+  return UCP_OK;
+}
+
+int ucp_allgatherv_f64(ucp_comm* comm, double* buf, const int64_t* bounds, void* stream) {
+  if (!comm || !buf || !bounds) return arg_fail("allgatherv_f64: bad arguments");
+  for (int r = 0; r < comm->nranks; ++r)
+    if (bounds[r] < 0 || bounds[r + 1] < bounds[r]) return arg_fail("allgatherv_f64: bounds must ascend from 0");
+  if (comm->nranks == 1) return UCP_OK;  // the whole vector is this rank's shard
+  // one in-place broadcast per rank (root r sends its shard), grouped so NCCL
+  // runs them as one collective: the uneven form of ncclAllGather
+  const NcclApi& a = nccl_api();
+  ncclResult_t r = a.group_start();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+  for (int q = 0; q < comm->nranks; ++q) {
+    const size_t n = (size_t)(bounds[q + 1] - bounds[q]);
+    if (n == 0) continue;
+    double* p = buf + bounds[q];
+    r = a.broadcast(p, p, n, ncclFloat64, q, comm->comm, as_stream(stream));
+    if (r != ncclSuccess) {
+      a.group_end();
+      return nccl_fail(r, "ncclBroadcast");
+    }
+  }
+  r = a.group_end();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
   return UCP_OK;
 }
 

@@ -323,3 +323,43 @@ def test_sharded_phases_do_not_synchronise(monkeypatch):
     finally:
         torch.cuda.set_sync_debug_mode("default")
     prob.flush_errors(sh)
+
+
+# ------------- the library-communicator backend routes every exchange to it
+def test_comm_sharding_routes_collectives():
+    """CommSharding (paper_1908_04489_b200.comm) sends the phase all-gathers --
+    equal plans in place, work-balanced plans as the uneven all-gather with the
+    plan's bounds -- and the error-slot MIN all-reduce to its communicator
+    (host logic; the NCCL calls themselves run in tests/test_gpu_parity.py)."""
+    from paper_1908_04489_b200.comm import CommSharding
+
+    class FakeComm:
+        def __init__(self):
+            self.calls = []
+
+        def allgather_(self, buf):
+            self.calls.append(("allgather", buf.numel()))
+
+        def allgatherv_(self, buf, bounds):
+            self.calls.append(("allgatherv", tuple(bounds)))
+
+        def allreduce_min_(self, t):
+            self.calls.append(("min", t.numel()))
+
+    comm = FakeComm()
+    sh = CommSharding(rank=1, world=2, comm=comm)
+    d = 1000
+    eq = sh.equal_plan(d)
+    buf = sh.padded_buffer(eq, "cpu")
+    assert sh.gather(buf, eq, d).numel() == d
+    w = torch.ones(d, dtype=torch.int64)
+    w[:100] = 50
+    bal = sh.plan_from_cuts(d, sh.plan_cuts(w).tolist())
+    assert bal != eq and bal[0] == 0 and bal[-1] == d
+    out = sh.gather(sh.padded_buffer(bal, "cpu"), bal, d)
+    assert out.numel() == d
+    sh.allreduce_min_(torch.zeros(6, dtype=torch.int64))
+    assert comm.calls == [("allgather", 1000), ("allgatherv", bal), ("min", 6)]
+    one = CommSharding(rank=0, world=1, comm=comm)
+    one.allreduce_min_(torch.zeros(3, dtype=torch.int64))
+    assert len(comm.calls) == 3  # a single rank exchanges nothing

@@ -385,17 +385,25 @@ def test_deferred_objective_value_and_error_order(P):
 
 
 def test_nccl_comm_single_rank(P):
-    """The C-ABI NCCL plumbing (ucp_comm_*) on one rank: in-place all-gather
-    and MIN all-reduce leave the data as is (multi-rank exchanges go through
-    torch.distributed in the Python host and need one GPU per rank)."""
+    """The library's NCCL communicator (ucp_comm_*) on one rank: the equal and
+    uneven in-place all-gathers and the MIN all-reduce leave the data as is,
+    bad arguments are rejected, and a solve sharded over the communicator is
+    bitwise the unsharded one (multi-rank runs need one GPU per rank)."""
     uid = P.NcclComm.unique_id()
     comm = P.NcclComm(1, 0, uid)
     x = torch.arange(10, dtype=torch.float64, device="cuda")
     comm.allgather_(x)
+    comm.allgatherv_(x, (0, 10))
     e = torch.tensor([5, 3, 9], dtype=torch.int64, device="cuda")
     comm.allreduce_min_(e)
     torch.cuda.synchronize()
     assert x.cpu().tolist() == list(map(float, range(10))) and e.cpu().tolist() == [5, 3, 9]
+    with pytest.raises(ValueError):
+        comm.allgatherv_(x, (4, 2))
+    prob = P.Witsenhausen(grids=[(-25.0, 25.0, 201)] * 2)
+    got = P.solve(prob, P.SolverConfig(max_rounds=3), sharding=comm.sharding())
+    want = P.solve(P.Witsenhausen(grids=[(-25.0, 25.0, 201)] * 2), P.SolverConfig(max_rounds=3))
+    assert got.final_objective == want.final_objective
     comm.close()
     with pytest.raises(ValueError):
         P.NcclComm(2, 5, uid)
