@@ -36,7 +36,8 @@ from .solver import (
     solve,
     solve_many,
 )
-from .verify import OracleConfig, exhaustive_argmin, monte_carlo_objective, windowed_argmin
+from .verify import (OracleConfig, exhaustive_argmin, exhaustive_argmin_many, monte_carlo_objective, windowed_argmin,
+                     windowed_argmin_many)
 from .montecarlo import device_monte_carlo_objective
 from .batch import solve_batch
 from .comm import CommSharding, NcclComm
@@ -73,7 +74,7 @@ __all__ = [
     "REGISTRY", "RoundReport", "SampledController", "Sharding", "SolveResult", "SolverConfig", "Uniform",
     "Witsenhausen", "ZeroDelay", "Inventory", "adaptive_allocation", "eval_controller", "eval_controller_many", "from_process_group",
     "init_identity", "local_update_phase", "fd_first", "fd_second", "OracleConfig", "exhaustive_argmin", "monte_carlo_objective", "device_monte_carlo_objective", "solve_batch", "NcclComm", "CommSharding",
-    "windowed_argmin", "make_grid", "make_problem", "max_workers", "nearest_index",
+    "windowed_argmin", "windowed_argmin_many", "exhaustive_argmin_many", "make_grid", "make_problem", "max_workers", "nearest_index",
     "nearest_indices", "newton_or_gradient_step", "node_window_bounds", "partial_exhaustion_phase", "pdf",
     "run_block", "set_workers", "solve", "solve_many", "trapezoid", "window_bounds", "window_indices", "__version__",
 ]

@@ -231,3 +231,33 @@ def test_check_controllers(P):  # :115-127
                                       for _ in range(problem.M)))
         with pytest.raises(ValueError):
             problem.check_controllers(wrong)
+
+
+@pytest.mark.parametrize("name", ["witsenhausen", "zero_delay", "inventory"])
+def test_batched_windowed_rule_matches_every_swept_point(P, name):
+    """verify.windowed_argmin_many re-derives the partial-exhaustion rule at
+    EVERY grid point in one batched device evaluation (oracle.py:70-95's rule,
+    independent of the sweep kernels' candidate lists and argmin): equal to
+    the device sweep everywhere, and to the one-point form."""
+    prob = {"witsenhausen": P.Witsenhausen(grids=[(-25.0, 25.0, 301)] * 2),
+            "zero_delay": P.ZeroDelay(grids=[(-5.0, 5.0, 201), (-6.0, 6.0, 241)]),
+            "inventory": P.Inventory(grids=[(-3.0, 3.0, 241)] * 2)}[name]
+    rng = np.random.default_rng(3)
+    U = P.ControllerSet(tuple(P.SampledController(g, prob.project(m, np.round(g.points + rng.uniform(-1, 1, g.d), 1)))
+                              for m, g in enumerate(prob.grids)))
+    cfg = P.SolverConfig()
+    for m, g in enumerate(prob.grids):
+        swept = P.partial_exhaustion_phase(prob, m, U, cfg)
+        best = P.windowed_argmin_many(prob, m, g.points, U, cfg.radius_for(g))
+        np.testing.assert_array_equal(prob.project(m, best), swept)
+        i = g.d // 3
+        assert P.windowed_argmin(prob, m, float(g.points[i]), U, cfg.radius_for(g)) == best[i]
+
+
+def test_batched_exhaustive_argmin(P):
+    wc = P.Witsenhausen(grids=[(-25.0, 25.0, 201)] * 2)
+    U = wc.zero_controllers()
+    oc = P.OracleConfig(-10.0, 10.0, 2001)
+    ys = [-5.0, 0.0, 5.0, 12.5]
+    many = P.exhaustive_argmin_many(wc, 0, ys, U, oc)
+    assert [P.exhaustive_argmin(wc, 0, y, U, oc) for y in ys] == many.tolist()
