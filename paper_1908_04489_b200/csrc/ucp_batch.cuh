@@ -340,7 +340,7 @@ int ucp_wc_batch_objective(ucp_wc_batch* b, int lane, const int32_t* ids, int32_
   UCP_WALK_LAUNCH_B(k_obj_terms, nslots * d0, dim3(nblocks(d0, kWalkThreads), nslots), st, D.d1, D.y0, D.f0, D.u0,
                     0.0, D.u1, g, 0, d0, L.terms, err_obj, B);
   UCP_LAUNCHED("k_obj_terms");
-  k_trapezoid<<<nslots, 32, 0, st>>>(L.terms, d0, D.h0, J, err_obj, B);
+  k_trapezoid<<<nslots, kTrapThreads, 0, st>>>(L.terms, d0, D.h0, J, err_obj, B);
   UCP_LAUNCHED("k_trapezoid");
   return UCP_OK;
 }

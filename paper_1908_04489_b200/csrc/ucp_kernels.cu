@@ -592,57 +592,88 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ob
   terms[i] = c;
 }
 
-// kernels.py:136-144: serial ascending trapezoid.  One warp stages chunks
-// through shared memory; lane 0 performs the additions in index order
-// (interior chunk body unrolled so the shared loads run ahead of the
-// dependent adds).
-__global__ void k_trapezoid(const double* __restrict__ x, int64_t n, double spacing, double* out,
-                            int64_t* err, const BatchArgs B) {
+// kernels.py:136-144: serial ascending trapezoid.  The sum is one dependent
+// add chain by definition, so the kernel's job is to keep that chain fed: a
+// loader warp streams 2048-value chunks into a shared-memory double buffer
+// (and finds the first non-finite value) while lane 0 of the adder warp adds
+// in index order with the next 8 values already in registers.  Named
+// barriers FULL (loader arrives, adder waits) / EMPTY (the reverse).  64
+// threads per instance (batched engine: one CTA per slot).
+__device__ __forceinline__ void named_sync(int id, int count);
+__device__ __forceinline__ void named_arrive(int id, int count);
+constexpr int kTrapThreads = 64;
+__global__ void __launch_bounds__(kTrapThreads) k_trapezoid(const double* __restrict__ x, int64_t n, double spacing,
+                                                           double* out, int64_t* err, const BatchArgs B) {
   constexpr int kChunk = 2048;
-  if (B.ids) {  // one warp (CTA) per slot; J and the error slot per instance
+  constexpr int kFull = 1, kEmpty = 3;
+  if (B.ids) {  // one CTA per slot; J and the error slot per instance
     const int b = B.inst(blockIdx.x);
     x += blockIdx.x * B.sslot;
     out += b;
     if (err) err += b * B.serr;
   }
-  __shared__ double buf[kChunk];
-  const int lane = threadIdx.x;
-  double acc = 0.0;
-  int64_t bad = UCP_NO_ERROR;
-  for (int64_t base = 0; base < n; base += kChunk) {
-    const int cnt = (int)(n - base < kChunk ? n - base : kChunk);
-    for (int r = lane; r < cnt; r += 32) {
-      double xv = x[base + r];
-      buf[r] = xv;
-      if (!isfinite(xv) && base + r < bad) bad = base + r;
+  __shared__ __align__(16) double buf[2][kChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  if (warp == 1) {
+    // ---- loader
+    int64_t bad = UCP_NO_ERROR;
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int sb = (int)(c & 1);
+      if (c >= 2) named_sync(kEmpty + sb, kTrapThreads);  // the adder is done with chunk c - 2
+      const int64_t base = c * kChunk;
+      const int cnt = (int)(n - base < kChunk ? n - base : kChunk);
+      for (int r = lane; r < cnt; r += 32) {
+        const double xv = x[base + r];
+        buf[sb][r] = xv;
+        if (!isfinite(xv) && base + r < bad) bad = base + r;
+      }
+      named_arrive(kFull + sb, kTrapThreads);
     }
-    __syncwarp();
+    for (int64_t c = nchunks - 2 > 0 ? nchunks - 2 : 0; c < nchunks; ++c)  // the adder's last EMPTY arrivals
+      named_sync(kEmpty + (int)(c & 1), kTrapThreads);
+    for (int off = 16; off > 0; off >>= 1) {
+      long long o = __shfl_down_sync(0xffffffffu, (long long)bad, off);
+      bad = o < bad ? o : bad;
+    }
+    if (lane == 0 && err && bad != UCP_NO_ERROR) flag_min(err, bad);
+    return;
+  }
+  // ---- adder (lane 0; the warp keeps the barrier protocol)
+  double acc = 0.0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int sb = (int)(c & 1);
+    named_sync(kFull + sb, kTrapThreads);
     if (lane == 0) {
+      const double* bs = buf[sb];
+      const int64_t base = c * kChunk;
+      const int cnt = (int)(n - base < kChunk ? n - base : kChunk);
       int r = 0;
       if (base == 0) {
-        acc = 0.5 * buf[0];
+        acc = 0.5 * bs[0];
         r = 1;
       }
       const int stop = base + cnt == n ? cnt - 1 : cnt;  // index n-1 gets the half weight
-      for (; r + 8 <= stop; r += 8) {
-        double v0 = buf[r], v1 = buf[r + 1], v2 = buf[r + 2], v3 = buf[r + 3];
-        double v4 = buf[r + 4], v5 = buf[r + 5], v6 = buf[r + 6], v7 = buf[r + 7];
-        acc += v0; acc += v1; acc += v2; acc += v3;
-        acc += v4; acc += v5; acc += v6; acc += v7;
+      if (r + 8 <= stop) {
+        double p0 = bs[r], p1 = bs[r + 1], p2 = bs[r + 2], p3 = bs[r + 3];
+        double p4 = bs[r + 4], p5 = bs[r + 5], p6 = bs[r + 6], p7 = bs[r + 7];
+        for (; r + 16 <= stop; r += 8) {
+          const double q0 = bs[r + 8], q1 = bs[r + 9], q2 = bs[r + 10], q3 = bs[r + 11];
+          const double q4 = bs[r + 12], q5 = bs[r + 13], q6 = bs[r + 14], q7 = bs[r + 15];
+          acc += p0; acc += p1; acc += p2; acc += p3;
+          acc += p4; acc += p5; acc += p6; acc += p7;
+          p0 = q0; p1 = q1; p2 = q2; p3 = q3; p4 = q4; p5 = q5; p6 = q6; p7 = q7;
+        }
+        acc += p0; acc += p1; acc += p2; acc += p3;
+        acc += p4; acc += p5; acc += p6; acc += p7;
+        r += 8;
       }
-      for (; r < stop; ++r) acc += buf[r];
-      if (base + cnt == n && n > 1) acc += 0.5 * buf[cnt - 1];
+      for (; r < stop; ++r) acc += bs[r];
+      if (base + cnt == n && n > 1) acc += 0.5 * bs[cnt - 1];
     }
-    __syncwarp();
+    named_arrive(kEmpty + sb, kTrapThreads);
   }
-  for (int off = 16; off > 0; off >>= 1) {
-    long long o = __shfl_down_sync(0xffffffffu, (long long)bad, off);
-    bad = o < bad ? o : bad;
-  }
-  if (lane == 0) {
-    *out = n == 1 ? 0.0 : acc * spacing;
-    if (err && bad != UCP_NO_ERROR) flag_min(err, bad);
-  }
+  if (lane == 0) *out = n == 1 ? 0.0 : acc * spacing;
 }
 
 __global__ void k_segmented_argmin(const double* __restrict__ costs, const int64_t* __restrict__ offsets,
@@ -964,7 +995,10 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 //
 // Persistent CTAs pull 128-query blocks from an atomic counter, the two edge
 // blocks first (they visit the most tiles).
-constexpr int kMomThreads = 128;
+#ifndef UCP_MOM_QT
+#define UCP_MOM_QT 128
+#endif
+constexpr int kMomThreads = UCP_MOM_QT;  // queries (threads) per work item
 // kUnroll pairs' exp() in flight per thread; the batched engine (few CTAs per
 // SM) instantiates a deeper unroll with a looser register bound.
 #ifndef UCP_MOM_UNROLL
@@ -1609,7 +1643,15 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   return UCP_OK;
 }
 
-// Walk launches below one full wave of resident CTAs run the latency-mode walk.
+// Walk launches below kWalkLatencyCtasPerSm CTAs per SM run the latency-mode
+// walk (one prefetching warp per walk group is faster when warps are scarce);
+// from 6 CTAs/SM on the throughput walk (with the no-op tail exit) wins: A/B
+// of 12 / 6 / 4 / 2 -- an 8-rank shard of the 2^20 step's local update 127 ->
+// 107 ms at 6, C1 35.3 -> 35.1 ms, d=14000 1.296 -> 1.281 s (profiles/r2_walk_latency_threshold.log).
+#ifndef UCP_WALK_LAT_CTAS
+#define UCP_WALK_LAT_CTAS 6
+#endif
+constexpr int kWalkLatencyCtasPerSm = UCP_WALK_LAT_CTAS;
 bool walk_latency_mode(int64_t n_walks) {
   static const int sms = [] {  // initialised once, thread-safe (function-local static)
     int dev = 0, n = 0;
@@ -1617,7 +1659,7 @@ bool walk_latency_mode(int64_t n_walks) {
       n = 148;
     return n;
   }();
-  return n_walks < (int64_t)sms * kWalkMinBlocks * kWalkThreads;
+  return n_walks < (int64_t)sms * kWalkLatencyCtasPerSm * kWalkThreads;
 }
 
 // kSmemWalkMax doubles of v1 fit the opt-in shared memory of one CTA
@@ -1783,7 +1825,7 @@ int ucp_gauss_moments_points(const double* y, int64_t n, const double* x, const 
 int ucp_trapezoid_sum(const double* samples, int64_t n, double spacing, double* out, int64_t* err,
                       void* stream) {
   if (n < 1) return arg_fail("trapezoid needs at least one sample");
-  k_trapezoid<<<1, 32, 0, as_stream(stream)>>>(samples, n, spacing, out, err, kNoBatch);
+  k_trapezoid<<<1, kTrapThreads, 0, as_stream(stream)>>>(samples, n, spacing, out, err, kNoBatch);
   UCP_LAUNCHED("k_trapezoid");
   return UCP_OK;
 }

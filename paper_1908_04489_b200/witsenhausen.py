@@ -168,25 +168,59 @@ class Witsenhausen(Problem):
     # waits on the host for its plan.  A phase uses the plan of the latest
     # objective snapshot (the first use per problem computes it directly).
     # Boundaries never change a result bit, only the balance.
+    # Balanced-plan walks stop at their no-op tail about 8.5 sigma past the
+    # centre (the throughput walk's tail exit: 83% of the full windows' nodes at
+    # the bench snapshot), so a walk's cost is its clamped [s - 12, s + 8.5]
+    # span, not the full window; shard_projection measured 17% exhaustion
+    # imbalance at 8 ranks with full windows.
+    WALK_TAIL_SIGMAS = 8.5 if os.environ.get("UCP_TAIL_EXIT", "1") != "0" else 12.0
+
     def _plan_weights(self, key, U: ControllerSet) -> torch.Tensor:
         """Per-point work estimates of plan ``key`` = (stage, scaled): walk nodes
-        for stage 0 (times the window width for exhaustion), in-range support
-        points for stage 1.  Every rank derives them from the same snapshot."""
+        for stage 0 (times the number of distinct-by-run window candidates for
+        exhaustion, the ones the kernels evaluate), in-range support points for
+        stage 1.  Every rank derives them from the same snapshot."""
         m, scaled = key
         D = self.device_context()
         u0, _ = self._uv(U)
         g1 = self.grids[1]
         if m == 0:
             s = D.y0 + u0
-            span = torch.clamp(torch.minimum(s + 12.0, torch.full_like(s, g1.b))
+            span = torch.clamp(torch.minimum(s + self.WALK_TAIL_SIGMAS, torch.full_like(s, g1.b))
                                - torch.maximum(s - 12.0, torch.full_like(s, g1.a)), min=0.0)
             w = (span / g1.spacing).to(torch.int64) + 1
             if scaled is not None:
                 lo, hi = D.window(self, 0, scaled)
-                w = w * (hi - lo + 1)
+                runs = torch.zeros_like(lo)
+                runs[1:] = torch.cumsum((u0[1:] != u0[:-1]).to(torch.int64), 0)
+                w = w * (1 + runs[hi] - runs[lo])
             return w
-        xs = torch.sort(D.y0 + u0).values
-        return (torch.searchsorted(xs, D.y1 + 12.0, right=True) - torch.searchsorted(xs, D.y1 - 12.0)) + 1
+        return self._moments_weights(D.y0 + u0, D.y1)
+
+    @staticmethod
+    def _moments_weights(x1: torch.Tensor, yq: torch.Tensor, tile: int = 256, qblock: int = 128) -> torch.Tensor:
+        """Stage-1 work per query as the moments kernels do it: a 128-query block
+        (ascending grid queries) visits every 256-point support tile (index
+        order) whose [min, max] of x1 comes within 12 of the block's span, all
+        256 pairs of a visited tile (k_moments' tile skipping).  live =
+        #{tiles: max >= ymin - 12} - #{tiles: min > ymax + 12} (min <= max), two
+        sorted counts instead of a block x tile matrix; a NaN in a tile keeps it
+        live.  Returns int64 pairs per query."""
+        d0, d1 = x1.numel(), yq.numel()
+        nt = -(-d0 // tile)
+        pad = nt * tile - d0
+        nan = torch.isnan(x1)
+        lo = torch.nn.functional.pad(torch.where(nan, torch.full_like(x1, -torch.inf), x1), (0, pad),
+                                     value=torch.inf).view(nt, tile).amin(1)
+        hi = torch.nn.functional.pad(torch.where(nan, torch.full_like(x1, torch.inf), x1), (0, pad),
+                                     value=-torch.inf).view(nt, tile).amax(1)
+        nb = -(-d1 // qblock)
+        first = torch.arange(nb, device=yq.device) * qblock
+        ymin, ymax = yq[first], yq[torch.clamp(first + qblock - 1, max=d1 - 1)]
+        reach_lo = nt - torch.searchsorted(torch.sort(hi).values, ymin - 12.0)           # tiles with max >= ymin-12
+        past_hi = nt - torch.searchsorted(torch.sort(lo).values, ymax + 12.0, right=True)  # tiles with min > ymax+12
+        live = torch.clamp(reach_lo - past_hi, min=1)
+        return torch.repeat_interleave(live * tile, qblock)[:d1]
 
     def _plan(self, m: int, U: ControllerSet, sharding: Sharding, radius=None) -> tuple:
         """Shard boundaries for a stage-m phase (``radius``: stage-0 exhaustion
