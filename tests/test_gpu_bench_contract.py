@@ -71,3 +71,17 @@ def test_bench_line_contract_two_ranks():
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
     assert d["time_to_converge"]["J"] == 0.16692114286407383  # sharded C1 solve, bitwise the reference
 
+
+
+def test_bench_two_ranks_balanced_plans_with_parity():
+    """2 ranks at 2^15 points (above UCP_BALANCE_MIN_POINTS: work-balanced,
+    uneven shards and the uneven all-gather) with the N>1 parity check and
+    the fast-arithmetic field: every sampled point of every phase bitwise the
+    oracle's, on the path the driver's multi-GPU run takes."""
+    d = _run_torchrun(2, "--steps", "1", "--warmup", "3", "--log2d", "15", "--cpu-seconds", "2",
+                      "--backend", "gloo", "--same-device")
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["cpu_baseline"] is None  # the CPU baseline is an N=1 figure
+    par = d["parity"]
+    assert all(par[k] == 0 for k in ("local0", "local1", "exh0", "exh1", "objective", "J_from_terms")), par
+    assert min(par["points"].values()) >= 16
+    assert d["fast_mode"]["value"] > 0 and d["fast_mode"]["J_rel_diff_vs_reference_arithmetic"] < 1e-12
