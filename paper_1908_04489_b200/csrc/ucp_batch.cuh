@@ -23,7 +23,9 @@ struct ucp_wc_batch {
     int64_t *offs = nullptr, *totals = nullptr, *counts = nullptr, *chunk_tot = nullptr;
     int32_t *cand_pt = nullptr, *cand_j = nullptr;
     int* counter = nullptr;
+    double* vsuf = nullptr;  // per-slot tail-exit tables of u1 (walk_tail_noop)
   } lane[2];
+  int64_t vstride = 0;  // doubles per slot table
   std::vector<void*> allocs;
 };
 
@@ -198,10 +200,22 @@ int batch_moments(ucp_wc_batch* b, ucp_wc_batch::Lane& L, int S, cudaStream_t st
   return UCP_OK;
 }
 
+// Throughput-mode walks of every slot stop at their no-op tail as in the
+// single-instance path (attach_vsuf): one table per slot, built from that
+// slot's instance u1 (the walks' v1) before the stage-0 kernels read it.
+void batch_attach_vsuf(ucp_wc_batch* b, ucp_wc_batch::Lane& L, WalkGrid* g, int S, int64_t n_walks, cudaStream_t st) {
+  if (!g_tail_exit || walk_latency_mode(n_walks)) return;
+  k_vsuf<<<S, 1024, 0, st>>>(b->D.u1, g->d, g->nb, L.vsuf, L.ids, b->D.ld1, b->vstride);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  g->vsuf = L.vsuf;
+  g->vstride = b->vstride;
+}
+
 int batch_iteration(ucp_wc_batch* b, ucp_wc_batch::Lane& L, int kind, int S, int64_t* err, cudaStream_t st) {
   const ucp_wc_batch_desc& D = b->D;
   const int64_t d0 = D.d0, d1 = D.d1;
   WalkGrid g = make_walk_grid(D.a1, D.h1, D.d1);
+  batch_attach_vsuf(b, L, &g, S, kind == 0 ? S * 3 * d0 : S * b->cbpad, st);  // the widest walk launch
   int rc;
   // ---- stage 0
   if (kind == 0) {
@@ -284,6 +298,9 @@ int ucp_wc_batch_create(const ucp_wc_batch_desc* desc, ucp_wc_batch** out) {
         (rc = balloc(b, &L.xw, B * ntiles * kTile)) || (rc = balloc(b, &L.tile_mm, B * ntiles)) ||
         (rc = balloc(b, &L.counter, 1)))
       break;
+    const int nb1 = (int)((d1 + (1 << kVsufShift) - 1) >> kVsufShift);
+    b->vstride = (int64_t)nb1 * vsuf_levels(nb1);
+    if ((rc = balloc(b, &L.vsuf, B * b->vstride))) break;
     if (l == 1 && ((rc = balloc(b, &L.costs, B * b->cbpad)) || (rc = balloc(b, &L.offs, B * (d0 + 1))) ||
                    (rc = balloc(b, &L.totals, B)) || (rc = balloc(b, &L.counts, B * d0)) ||
                    (rc = balloc(b, &L.chunk_tot, B * ((d0 + kCandThreads - 1) / kCandThreads))) || (rc = balloc(b, &L.cand_pt, B * b->cbpad)) ||
@@ -335,6 +352,7 @@ int ucp_wc_batch_objective(ucp_wc_batch* b, int lane, const int32_t* ids, int32_
   const ucp_wc_batch_desc& D = b->D;
   const int64_t d0 = D.d0;
   WalkGrid g = make_walk_grid(D.a1, D.h1, D.d1);
+  batch_attach_vsuf(b, L, &g, nslots, nslots * d0, st);
   BatchArgs B = batch_args(b, L.ids, d0);
   B.serr = 1;
   UCP_WALK_LAUNCH_B(k_obj_terms, nslots * d0, dim3(nblocks(d0, kWalkThreads), nslots), st, D.d1, D.y0, D.f0, D.u0,

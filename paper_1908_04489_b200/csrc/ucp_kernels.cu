@@ -176,6 +176,7 @@ struct WalkGrid {
   // (see walk_tail_noop / k_vsuf).
   const double* vsuf;
   int nb;
+  int64_t vstride;  // batched engine: slot s's table at vsuf + s * vstride
   // instrumentation (ucp_walk_node_counter): visited walk nodes are added here
   unsigned long long* visits;
   // UCP_WC_FAST (ucp_wc_problem.flags): the tolerance-stated FMA walk
@@ -213,6 +214,7 @@ WalkGrid make_walk_grid(double a, double h, int64_t d, int fast = 0) {
   g.b = a + h * (double)(d - 1);
   g.q = ucp_exp_tab((-h) * h, h_exp_tab);  // same port as the device: bitwise glibc
   g.vsuf = nullptr;
+  g.vstride = 0;
   g.nb = (int)((d + (1 << 8) - 1) >> 8);
   g.visits = g_visits.load(std::memory_order_acquire);
   return g;
@@ -376,6 +378,25 @@ __device__ __forceinline__ Mom3 gauss_walk_impl(double st, const double* __restr
           break;
         }
       }
+      // the rest in 64-node chunks, still checked: a short window (e.g. 960
+      // nodes at d = 2000, the batched engine's sizes) reaches its tail here
+      while (j + 63 <= jint) {
+#pragma unroll 2
+        for (int c = 0; c < 16; ++c, j += 4) {
+          const double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
+          const double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
+          UCP_WALK_STEP_V(hw, p0.x);
+          UCP_WALK_STEP_V(hw, p0.y);
+          UCP_WALK_STEP_V(hw, p1.x);
+          UCP_WALK_STEP_V(hw, p1.y);
+        }
+        if (vsuf && ratio <= 1.0 && j <= jint &&
+            walk_tail_noop(pdf, ratio, hw, range_max(vsuf, g.nb, j >> kVsufShift, je >> kVsufShift), acc0, acc1,
+                           acc2)) {
+          j = 2 * (je + 1) - j;
+          break;
+        }
+      }
       for (; j + 3 <= jint; j += 4) {
         const double2 p0 = __ldg(reinterpret_cast<const double2*>(v + j));
         const double2 p1 = __ldg(reinterpret_cast<const double2*>(v + j + 2));
@@ -501,7 +522,7 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_lu
     u0 += b * B.su0;
     v1 += b * B.su1;
     k = B.kvec[b];
-    cost3 += blockIdx.y * B.sslot;
+    cost3 += blockIdx.y * B.sslot;    if (g.vsuf) g.vsuf += (int64_t)blockIdx.y * g.vstride;  // this slot's tail-exit table
   }
   UCP_WALK_STAGE(v1, g.d);
   if (t >= 3 * n) return;
@@ -544,7 +565,7 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_lu
     k = B.kvec[b];
     cost3 += blockIdx.y * B.sslot;
     out += blockIdx.y * n;
-    err += b * B.serr;
+    err += b * B.serr;    if (g.vsuf) g.vsuf += (int64_t)blockIdx.y * g.vstride;  // this slot's tail-exit table
   }
   UCP_WALK_STAGE(v1, g.d);
   if (t >= n) return;
@@ -583,7 +604,7 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ob
     v1 += b * B.su1;
     k = B.kvec[b];
     terms += blockIdx.y * B.sslot;
-    err += b * B.serr;
+    err += b * B.serr;    if (g.vsuf) g.vsuf += (int64_t)blockIdx.y * g.vstride;  // this slot's tail-exit table
   }
   UCP_WALK_STAGE(v1, g.d);
   if (i >= end) return;
@@ -727,8 +748,13 @@ __global__ void k_flatten_windows(const double* __restrict__ values, const int64
 // (~8 B/node read once plus log2(nb) passes over nb blocks; negligible beside
 // the walks that use it).  Level 0: block maxima; level k: max over 2^k blocks.
 // A non-finite v makes every entry covering it +inf (the walk never exits there).
-__global__ void __launch_bounds__(1024) k_vsuf(const double* __restrict__ v, int64_t d, int nb, double* t) {
+__global__ void __launch_bounds__(1024) k_vsuf(const double* __restrict__ v, int64_t d, int nb, double* t,
+                                                const int32_t* __restrict__ ids, int64_t su1, int64_t tstride) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (ids) {  // batched engine: CTA s builds slot s's table from instance ids[s]'s v
+    v += (int64_t)ids[blockIdx.x] * su1;
+    t += (int64_t)blockIdx.x * tstride;
+  }
   for (int b = warp; b < nb; b += 32) {
     double m = 0.0;
     for (int64_t j = ((int64_t)b << kVsufShift) + lane; j < d && j < ((int64_t)(b + 1) << kVsufShift); j += 32) {
@@ -844,7 +870,7 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ex
     k = B.kvec[b];
     cand_pt += blockIdx.y * B.sslot;
     cand_j += blockIdx.y * B.sslot;
-    costs += blockIdx.y * B.sslot;
+    costs += blockIdx.y * B.sslot;    if (g.vsuf) g.vsuf += (int64_t)blockIdx.y * g.vstride;  // this slot's tail-exit table
   }
   UCP_WALK_STAGE(v1, g.d);
   if (c >= *total) return;
@@ -1708,7 +1734,7 @@ int attach_vsuf(WalkGrid* g, const double* v1, int64_t n_walks, ucp_workspace* w
   if (!g_tail_exit || walk_latency_mode(n_walks)) return UCP_OK;
   void* p;
   if (int rc = ws_get(ws, WS_VSUF, sizeof(double) * (size_t)g->nb * vsuf_levels(g->nb), &p)) return rc;
-  k_vsuf<<<1, 1024, 0, st>>>(v1, g->d, g->nb, (double*)p);
+  k_vsuf<<<1, 1024, 0, st>>>(v1, g->d, g->nb, (double*)p, nullptr, 0, 0);
   UCP_LAUNCHED("k_vsuf");
   g->vsuf = (const double*)p;
   return UCP_OK;
