@@ -102,7 +102,7 @@ def main():
             k: round(v[1] / sum(x[1] for x in agg.values()), 5) for k, v in agg.items()}
     for rep in args.rep:
         for d in full(rep, args.tag + "_" + Path(rep).stem):
-            fam = FAMILY.get(d["kernel"])
+            fam = FAMILY.get(d["kernel"].split("<")[0])
             if fam and args.log2d and "dram__bytes_read.sum" in d:
                 b = to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"])
                 if b == b:  # skip NaN captures
