@@ -363,3 +363,26 @@ def test_comm_sharding_routes_collectives():
     one = CommSharding(rank=0, world=1, comm=comm)
     one.allreduce_min_(torch.zeros(3, dtype=torch.int64))
     assert len(comm.calls) == 3  # a single rank exchanges nothing
+
+
+def test_moments_weights_model_matches_tile_rule():
+    """The stage-1 shard weights (Witsenhausen._moments_weights: live-tile
+    pairs per query from two sorted counts) equal a direct application of the
+    moments kernel's tile-skipping rule per 128-query block, NaN tiles live."""
+    from paper_1908_04489_b200.witsenhausen import Witsenhausen
+
+    rng = np.random.default_rng(5)
+    d = 5000
+    y = torch.from_numpy(np.linspace(-25.0, 25.0, d))
+    x1 = y + torch.from_numpy(np.where(rng.random(d) < 0.5, 6.0, -6.0) - 0.9 * y.numpy())
+    x1[1234] = float("nan")
+    w = Witsenhausen._moments_weights(x1, y)
+    xs, ys = x1.numpy(), y.numpy()
+    for b in range(0, -(-d // 128)):
+        q = ys[b * 128:(b + 1) * 128]
+        live = 0
+        for t in range(-(-d // 256)):
+            xt = xs[t * 256:(t + 1) * 256]
+            if np.isnan(xt).any() or not (q.min() - np.nanmax(xt) > 12 or q.max() - np.nanmin(xt) < -12):
+                live += 1
+        assert int(w[b * 128]) == max(live, 1) * 256, b
