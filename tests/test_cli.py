@@ -63,3 +63,18 @@ def test_numeric_failure_exit_2(tmp_path, monkeypatch):
 
     monkeypatch.setattr(cli, "solve", boom)
     assert cli.main(["solve", "--grid=-25,25,101", "--out", str(tmp_path)]) == 2
+
+
+def test_cli_fast_arithmetic_param():
+    """`--param arithmetic=fma` selects the opt-in fast walk (DESIGN.md §2b);
+    the default stays the reference's arithmetic, and a bad value is a config error."""
+    from paper_1908_04489_b200 import cli
+
+    args = cli.build_parser().parse_args(["solve", "--problem", "witsenhausen", "--param", "arithmetic=fma"])
+    prob, _ = cli.load_run_config(args).build()
+    assert prob.arithmetic == "fma"
+    prob, _ = cli.load_run_config(cli.build_parser().parse_args(["solve", "--problem", "witsenhausen"])).build()
+    assert prob.arithmetic == "reference"
+    with pytest.raises(ValueError):
+        cli.load_run_config(cli.build_parser().parse_args(
+            ["solve", "--problem", "witsenhausen", "--param", "arithmetic=fp32"])).build()
