@@ -66,6 +66,15 @@ typedef struct ucp_wc_problem {
  * d=2000 solve converges 4.9e-7 relative below the reference's J) -- stated
  * and tested in tests/test_gpu_fast_mode.py. */
 #define UCP_WC_FAST 1
+/* ucp_wc_problem.flags (opt-in, tolerance-stated): the stage-0 exhaustion
+ * phase reads each candidate centre's window sums from a table of the
+ * reference's walk at lattice centres a1 + m h1 (built once per phase,
+ * d1 + 24/h1 walks), interpolated by quintic Lagrange over 6 lattice centres,
+ * exact cdf tails added -- O(1) per candidate instead of O(24/h1).  Honoured
+ * when h1 <= 2e-3.  Not used by the local update (its finite differences
+ * would amplify the table's per-node rounding).  Tolerance in
+ * tests/test_gpu_fast_mode.py. */
+#define UCP_WC_TABLE 2
 
 /* Local-update parameters (solver.py:47-97, SolverConfig), already resolved
  * per stage (newton_cap = cfg.cap_for(grid)). */

@@ -19,6 +19,7 @@ UCP_ERR_CUDA = 3
 NO_ERROR = (1 << 63) - 1  # UCP_NO_ERROR
 ABI_VERSION = 3  # UCP_ABI_VERSION (3: ucp_wc_problem.flags)
 WC_FAST = 1  # UCP_WC_FAST
+WC_TABLE = 2  # UCP_WC_TABLE
 
 c_i64 = ctypes.c_int64
 c_dbl = ctypes.c_double

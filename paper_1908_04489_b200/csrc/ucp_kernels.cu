@@ -182,6 +182,11 @@ struct WalkGrid {
   // UCP_WC_FAST (ucp_wc_problem.flags): the tolerance-stated FMA walk
   // (gauss_walk_impl<kMode, true>); 0 = the reference's arithmetic
   int fast;
+  // UCP_WC_TABLE: window sums tabulated at lattice centres a + m h,
+  // m in [tm0, tm0 + tL) (3 planes of tL doubles), read by table_moments;
+  // nullptr = walk every centre
+  const double* table;
+  int64_t tm0, tL;
 };
 constexpr int kVsufShift = 8;  // 256 nodes per block
 
@@ -208,6 +213,8 @@ std::atomic<unsigned long long*> g_visits{nullptr};
 WalkGrid make_walk_grid(double a, double h, int64_t d, int fast = 0) {
   WalkGrid g;
   g.fast = fast;
+  g.table = nullptr;
+  g.tm0 = g.tL = 0;
   g.a = a;
   g.h = h;
   g.d = d;
@@ -280,7 +287,7 @@ __device__ __forceinline__ double range_max(const double* __restrict__ t, int nb
 // per interior node instead of 8.  Same nodes, same order, same exp/erf,
 // same no-op tail exit; every sum differs from the reference by rounding
 // only (tests/test_gpu_fast_mode.py states and checks the tolerance).
-template <int kMode, bool kFast>
+template <int kMode, bool kFast, bool kRaw = false>
 __device__ __forceinline__ Mom3 gauss_walk_impl(double st, const double* __restrict__ v, const WalkGrid g) {
   constexpr bool kLat = kMode != 0;
   long long jlo = (long long)ceil(((st - kGaussCut) - g.a) / g.h);
@@ -419,8 +426,50 @@ __device__ __forceinline__ Mom3 gauss_walk_impl(double st, const double* __restr
 #undef UCP_WALK_STEP
 #undef UCP_WALK_STEP_V
   }
+  Mom3 r;
+  if (kRaw) {  // the window sums alone (the lattice table of UCP_WC_TABLE)
+    r.t0 = acc0;
+    r.t1 = acc1;
+    r.t2 = acc2;
+    return r;
+  }
   double lo = phi_cdf(g.a - st);
   double hi = phi_cdf(st - g.b);
+  const double v0 = walk_ld<kMode>(v, 0), vl = walk_ld<kMode>(v, (int)(g.d - 1));
+  r.t0 = (acc0 + lo) + hi;
+  r.t1 = (acc1 + lo * v0) + hi * vl;
+  r.t2 = (acc2 + (lo * v0) * v0) + (hi * vl) * vl;
+  return r;
+}
+
+// UCP_WC_TABLE (opt-in, tolerance-stated; stage-0 exhaustion only): the window sums of a centre s from
+// the lattice table by quintic Lagrange interpolation over the 6 lattice
+// centres around s, then the exact cdf tails.  The sums are smooth in s (a
+// Gaussian-weighted sum over fixed nodes; nodes cross the +-12 cut at weight
+// phi(12) ~ 6e-32), the lattice spacing is the grid's h, and the table is
+// used only for h <= kTableMaxH: interpolation error ~h^6 |T^(6)| / 720.
+// Outside the lattice the window misses the grid: the sums are exactly 0.
+template <int kMode>
+__device__ __forceinline__ Mom3 table_moments(double st, const double* __restrict__ v, const WalkGrid& g) {
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  const double t = (st - g.a) / g.h;
+  const double fm = floor(t);
+  if (fm >= (double)(g.tm0 + 2) && fm <= (double)(g.tm0 + g.tL - 4)) {
+    const double x = t - fm;
+    const double pa = x + 2.0, pb = x + 1.0, pc = x, pd = x - 1.0, pe = x - 2.0, pf = x - 3.0;
+    const double ab = pa * pb, de = pd * pe, ef = pe * pf;
+    const double w[6] = {pb * pc * de * pf * (-1.0 / 120.0), pa * pc * de * pf * (1.0 / 24.0),
+                         ab * pd * ef * (-1.0 / 12.0),       ab * pc * ef * (1.0 / 12.0),
+                         ab * pc * pd * pf * (-1.0 / 24.0),  ab * pc * de * (1.0 / 120.0)};
+    const double* T = g.table + ((int64_t)fm - 2 - g.tm0);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      acc0 = __fma_rn(w[k], __ldg(T + k), acc0);
+      acc1 = __fma_rn(w[k], __ldg(T + g.tL + k), acc1);
+      acc2 = __fma_rn(w[k], __ldg(T + 2 * g.tL + k), acc2);
+    }
+  }
+  const double lo = phi_cdf(g.a - st), hi = phi_cdf(st - g.b);
   const double v0 = walk_ld<kMode>(v, 0), vl = walk_ld<kMode>(v, (int)(g.d - 1));
   Mom3 r;
   r.t0 = (acc0 + lo) + hi;
@@ -434,6 +483,7 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
 #ifdef UCP_NO_FAST_WALK  // (PTX audit of the reference-arithmetic walk: tests/test_abi_and_host.py)
   return gauss_walk_impl<kMode, false>(st, v, g);
 #else
+  if (g.table) return table_moments<kMode>(st, v, g);
   return g.fast ? gauss_walk_impl<kMode, true>(st, v, g) : gauss_walk_impl<kMode, false>(st, v, g);
 #endif
 }
@@ -483,6 +533,22 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ga
   t0[t] = r.t0;
   t1[t] = r.t1;
   t2[t] = r.t2;
+}
+
+// UCP_WC_TABLE: the window sums (reference arithmetic) at lattice centres
+// a + (tm0 + i) h, i < L, into three planes of L doubles.
+template <int kMode>
+__global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_walk_lattice(
+    const double* __restrict__ v, WalkGrid g, int64_t tm0, int64_t L, double* T) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  UCP_WALK_STAGE(v, g.d);
+  if (i >= L) return;
+  const Mom3 r = gauss_walk_impl<kMode, false, true>(g.a + (double)(tm0 + i) * g.h, v, g);
+  T[i] = r.t0;
+  T[L + i] = r.t1;
+  T[2 * L + i] = r.t2;
 }
 
 // marginal_cost_segmented m=0 over a flat candidate list; the segment of
@@ -1579,7 +1645,7 @@ struct ucp_workspace {
 namespace {
 enum {
   WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS,
-  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_C5_TAB, WS_C5_GT0, WS_C5_GT1, WS_C5_MEMO, WS_C5_FC, WS_C5_GC, WS_VSUF, WS_NSLOTS
+  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_C5_TAB, WS_C5_GT0, WS_C5_GT1, WS_C5_MEMO, WS_C5_FC, WS_C5_GC, WS_VSUF, WS_TABLE, WS_NSLOTS
 };
 static_assert(WS_NSLOTS <= 24, "workspace slots");
 // fused moments below this many queries (above, k_moments' persistent CTAs
@@ -1737,6 +1803,26 @@ int attach_vsuf(WalkGrid* g, const double* v1, int64_t n_walks, ucp_workspace* w
   k_vsuf<<<1, 1024, 0, st>>>(v1, g->d, g->nb, (double*)p, nullptr, 0, 0);
   UCP_LAUNCHED("k_vsuf");
   g->vsuf = (const double*)p;
+  return UCP_OK;
+}
+
+// UCP_WC_TABLE is honoured for grids at least this fine (interpolation error
+// ~ h^6 |T^(6)| / 720 < 1e-15 relative); coarser grids walk every centre.
+constexpr double kTableMaxH = 2e-3;
+
+int attach_table(WalkGrid* g, const ucp_wc_problem* P, const double* v1, ucp_workspace* ws, cudaStream_t st) {
+  if (!(P->flags & UCP_WC_TABLE) || !(P->h1 <= kTableMaxH)) return UCP_OK;
+  const int64_t M = (int64_t)ceil(kGaussCut / P->h1) + 3;  // lattice covers [a - 12 - 3h, b + 12 + 3h]
+  const int64_t tm0 = -M, L = P->d1 + 2 * M;
+  void* pt;
+  if (int rc = ws_get(ws, WS_TABLE, sizeof(double) * 3 * (size_t)L, &pt)) return rc;
+  WalkGrid gl = make_walk_grid(P->a1, P->h1, P->d1, 0);  // the table: the reference's walk
+  if (int rc = attach_vsuf(&gl, v1, L, ws, st)) return rc;
+  UCP_WALK_LAUNCH(k_walk_lattice, L, nblocks(L, kWalkThreads), st, P->d1, v1, gl, tm0, L, (double*)pt);
+  UCP_LAUNCHED("k_walk_lattice");
+  g->table = (const double*)pt;
+  g->tm0 = tm0;
+  g->tL = L;
   return UCP_OK;
 }
 
@@ -1954,6 +2040,9 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
     if (int rc_ = check_aligned(u1)) return rc_;
     WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1, (int)(P->flags & UCP_WC_FAST));
     if ((rc = attach_vsuf(&g, u1, 3 * n, ws, st))) return rc;
+    // (no UCP_WC_TABLE here: the local update's second differences over
+    // h = 1e-4 (1 + |u|) would amplify the table's uncorrelated per-lattice-node
+    // rounding, 1e-14, to 1e-5 in c2 -- measured: J after the phase 1.3e-5 off)
     UCP_WALK_LAUNCH_PDL(k_lu0_probe, 3 * n, nblocks(3 * n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
                                                      (double*)pc, kNoBatch);
     UCP_LAUNCHED("k_lu0_probe");
@@ -2043,6 +2132,7 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
   if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1, (int)(P->flags & UCP_WC_FAST));
   if ((rc = attach_vsuf(&g, u1, total, ws, st))) return rc;
+  if ((rc = attach_table(&g, P, u1, ws, st))) return rc;
   UCP_WALK_LAUNCH(k_ex0_eval, total, nblocks(total, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, counts + n,
                                                   (const int32_t*)ppt, (const int32_t*)pj, (double*)pc, kNoBatch);
   UCP_LAUNCHED("k_ex0_eval");

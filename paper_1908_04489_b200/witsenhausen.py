@@ -71,13 +71,14 @@ class _WcDevice(DeviceContext):
         self.fw0 = to_device_f64(prob._fw0, self.device)
         self.P = _lib.WcProblem(prob.k, g0.a, g0.spacing, g0.d, g1.a, g1.spacing, g1.d,
                                 ptr(self.y0), ptr(self.y1), ptr(self.f0), ptr(self.fw0),
-                                _lib.WC_FAST if prob.arithmetic == "fma" else 0)
+                                {"reference": 0, "fma": _lib.WC_FAST,
+                                 "table": _lib.WC_FAST | _lib.WC_TABLE}[prob.arithmetic])
 
 
 class Witsenhausen(Problem):
     name = "witsenhausen"
 
-    ARITHMETIC = ("reference", "fma")
+    ARITHMETIC = ("reference", "fma", "table")
 
     def __init__(self, k: float = 0.2, sigma: float = 5.0, grids=None, device=None, arithmetic: str = "reference"):
         """``arithmetic``: "reference" (default) evaluates every stage-0 walk in
@@ -85,7 +86,11 @@ class Witsenhausen(Problem):
         "fma" is the opt-in, tolerance-stated fast mode (h folded into the pdf
         recurrence, FMA in the v-weighted sums: 6 instead of 8 FP64 instructions
         per walk node; costs equal to rounding, argmin picks may differ on
-        near-ties -- tests/test_gpu_fast_mode.py states the tolerance)."""
+        near-ties -- tests/test_gpu_fast_mode.py states the tolerance);
+        "table" adds, on grids with h1 <= 2e-3, lattice-tabulated window sums
+        for the stage-0 exhaustion phase (the reference's walk at lattice
+        centres, quintic interpolation: O(1) per candidate; same tolerance
+        statement), the FMA walk elsewhere."""
         if arithmetic not in self.ARITHMETIC:
             raise ValueError(f"witsenhausen.arithmetic must be one of {self.ARITHMETIC} (got {arithmetic!r})")
         self.arithmetic = arithmetic

@@ -84,4 +84,6 @@ def test_bench_two_ranks_balanced_plans_with_parity():
     par = d["parity"]
     assert all(par[k] == 0 for k in ("local0", "local1", "exh0", "exh1", "objective", "J_from_terms")), par
     assert min(par["points"].values()) >= 16
-    assert d["fast_mode"]["value"] > 0 and d["fast_mode"]["J_rel_diff_vs_reference_arithmetic"] < 1e-12
+    for arith in ("fma", "table"):
+        f = d["fast_mode"][arith]
+        assert f["value"] > 0 and f["J_rel_diff_vs_reference_arithmetic"] < 1e-12 and f["points_differing"]["exh1"] == 0

@@ -17,6 +17,10 @@ north_star: "stated tolerance if a fast path is offered"):
   reference's 0.16692114286407383 -- so the north star's 1e-9 per-iteration J
   bound holds per snapshot, and a converged fast solve is checked to 1e-6.
 
+arithmetic="table" additionally reads stage-0 exhaustion costs from a lattice
+table of the reference's walk (quintic interpolation, h1 <= 2e-3): same
+statements for its picks (near-ties only) and the objective after the phase.
+
 The default (arithmetic="reference") stays bitwise the reference -- every
 other GPU test runs it."""
 import numpy as np
@@ -111,3 +115,46 @@ def test_batch_engine_declines_fast_problems(P):
 
     assert not batchable([P.Witsenhausen(arithmetic="fma"), P.Witsenhausen(arithmetic="fma")])
     assert batchable([P.Witsenhausen(), P.Witsenhausen(k=0.3)])
+
+
+# ---------------------------------------------------- arithmetic="table"
+def test_table_exhaustion_picks_are_near_ties(P, golden):
+    """arithmetic="table": stage-0 exhaustion candidates read the lattice table
+    (quintic interpolation of the reference's walk at lattice centres).  Picks
+    differ from the reference's only on exact-cost near-ties (1e-10), and the
+    objective of the new controller is within 1e-12 of the reference's."""
+    d = 1 << 16
+    u0, u1 = _snapshot(golden, d)
+    exact = P.Witsenhausen(grids=[(*SPAN, d)] * 2)
+    table = P.Witsenhausen(grids=[(*SPAN, d)] * 2, arithmetic="table")
+    cfg = P.SolverConfig(search_radius=19.5 * exact.grids[0].spacing)
+    U = [P.ControllerSet((P.SampledController(p.grids[0], u0), P.SampledController(p.grids[1], u1)))
+         for p in (exact, table)]
+    ge = P.partial_exhaustion_phase(exact, 0, U[0], cfg)
+    gt = P.partial_exhaustion_phase(table, 0, U[1], cfg)
+    diff = np.flatnonzero(ge != gt)
+    assert diff.size <= d // 1000, diff.size
+    if diff.size:
+        y = exact.grids[0].points[diff]
+        two = np.stack([ge[diff], gt[diff]], axis=1).ravel()
+        c = exact.marginal_cost_segmented(0, two, np.arange(0, two.size + 1, 2, dtype=np.int64), y, U[0])
+        c = c.reshape(-1, 2)
+        assert (np.abs(c[:, 1] - c[:, 0]) <= 1e-10 * np.abs(c[:, 0])).all()
+
+    def J(u):
+        return exact.objective(P.ControllerSet((P.SampledController(exact.grids[0], u),
+                                                P.SampledController(exact.grids[1], u1))))
+
+    assert abs(J(gt) - J(ge)) <= 1e-12 * J(ge)
+
+
+def test_table_not_used_on_coarse_grids(P, golden):
+    """h1 > 2e-3 (d = 2000: h = 0.025): the table would interpolate too coarsely,
+    so "table" falls back to the FMA walk -- bitwise the "fma" results."""
+    u0, u1 = _snapshot(golden, 2000)
+    outs = []
+    for mode in ("fma", "table"):
+        p = P.Witsenhausen(arithmetic=mode)
+        U = P.ControllerSet((P.SampledController(p.grids[0], u0), P.SampledController(p.grids[1], u1)))
+        outs.append(P.partial_exhaustion_phase(p, 0, U, P.SolverConfig()))
+    assert outs[0].tobytes() == outs[1].tobytes()

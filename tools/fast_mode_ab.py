@@ -24,7 +24,8 @@ d = 1 << args.log2d
 sol = np.load(ROOT / "tests" / "golden" / "wc_solve_d2000.npz")
 u0, u1 = bench.resample(sol["u0"], d), bench.resample(sol["u1"], d)
 out = {}
-for mode in ("reference", "fma"):
+MODES = ("reference", "fma", "table")
+for mode in MODES:
     prob = P.Witsenhausen(grids=[(-25.0, 25.0, d)] * 2, arithmetic=mode)
     cfg = P.SolverConfig(search_radius=19.5 * prob.grids[0].spacing)
     U = P.ControllerSet((P.SampledController(prob.grids[0], u0), P.SampledController(prob.grids[1], u1)))
@@ -42,9 +43,30 @@ for mode in ("reference", "fma"):
             res[name] = r.cpu().numpy()
         res["J"] = prob.device_objective(U)
     out[mode] = (ms, res)
-ref, fast = out["reference"][1], out["fma"][1]
-line = {"log2d": args.log2d, "ms_reference": out["reference"][0], "ms_fma": out["fma"][0],
-        "speedup": {k: out["reference"][0][k] / out["fma"][0][k] for k in out["fma"][0]},
-        "points_differing": {k: int(np.count_nonzero(ref[k] != fast[k])) for k in ("local0", "local1", "exh0", "exh1")},
-        "J_reference": ref["J"], "J_fma": fast["J"], "J_rel_diff": abs(fast["J"] - ref["J"]) / ref["J"]}
+ref = out["reference"][1]
+# the objective (reference arithmetic) of each mode's new stage-0 controller after
+# local0 and after exh0: do rounding-ambiguous decisions move J?
+jprob = P.Witsenhausen(grids=[(-25.0, 25.0, d)] * 2)
+
+
+def J_of(u0_new):
+    return jprob.objective(P.ControllerSet((P.SampledController(jprob.grids[0], u0_new),
+                                            P.SampledController(jprob.grids[1], u1))))
+
+
+J_after = {m: {ph: J_of(out[m][1][ph]) for ph in ("local0", "exh0")} for m in MODES}
+line = {"log2d": args.log2d, "ms_reference": out["reference"][0]}
+for mode in MODES[1:]:
+    fast = out[mode][1]
+    line[mode] = {"ms": out[mode][0], "speedup": {k: out["reference"][0][k] / out[mode][0][k] for k in out[mode][0]},
+                  "points_differing": {k: int(np.count_nonzero(ref[k] != fast[k]))
+                                       for k in ("local0", "local1", "exh0", "exh1")},
+                  "J": fast["J"], "J_rel_diff": abs(fast["J"] - ref["J"]) / ref["J"],
+                  "J_after_phase_rel_diff": {ph: (J_after[mode][ph] - J_after["reference"][ph]) / J_after["reference"][ph]
+                                             for ph in ("local0", "exh0")},
+                  "local0_points_rel_diff_above_1e-9": int(np.count_nonzero(
+                      np.abs(fast["local0"] - ref["local0"]) > 1e-9 * np.maximum(np.abs(ref["local0"]), 1e-300))),
+                  "max_rel_diff_local0": float(np.max(np.abs(fast["local0"] - ref["local0"]) /
+                                                      np.maximum(np.abs(ref["local0"]), 1e-300)))}
+line["J_reference"] = ref["J"]
 print(json.dumps(line), flush=True)
