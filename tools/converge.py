@@ -27,9 +27,11 @@ ap.add_argument("--d", type=int, default=14000)
 ap.add_argument("--warm", action="store_true")
 ap.add_argument("--radius-nodes", type=float, default=None)
 ap.add_argument("--max-rounds", type=int, default=10000)
+ap.add_argument("--arithmetic", default="reference", choices=["reference", "fma", "table"],
+                help="Witsenhausen arithmetic (the non-reference ones are opt-in, tolerance-stated)")
 args = ap.parse_args()
 
-prob = P.Witsenhausen(grids=[(-25.0, 25.0, args.d)] * 2)
+prob = P.Witsenhausen(grids=[(-25.0, 25.0, args.d)] * 2, arithmetic=args.arithmetic)
 h = prob.grids[0].spacing
 cfg = P.SolverConfig(max_rounds=args.max_rounds,
                      search_radius=None if args.radius_nodes is None else (args.radius_nodes / 2.0) * h)
@@ -55,7 +57,7 @@ def progress(r):
 res = P.solve(prob, cfg, initial=initial, on_round=progress)
 torch.cuda.synchronize()
 wall = time.perf_counter() - t
-print(json.dumps({"d": args.d, "warm": args.warm, "search_radius": cfg.radius_for(prob.grids[0]),
+print(json.dumps({"d": args.d, "warm": args.warm, "arithmetic": args.arithmetic, "search_radius": cfg.radius_for(prob.grids[0]),
                   "wall_s": wall, "rounds": res.total_rounds, "termination": res.termination,
                   "final_J": res.final_objective,
                   "per_round": [[r.round_index, r.objective, r.local_iters, r.exhaustion_iters, round(r.wall_ms, 1)]
