@@ -16,6 +16,8 @@ sanitizer run is also a parity run:
   c5       ZeroDelay and Inventory M=3 (small and ~2k-4k grids), two rounds each, and the
            uniform-noise kernels vs the oracle
   mc       Philox Monte-Carlo objective, 2^16 samples
+  table    d=2^15 exhaustion in the opt-in table arithmetic (k_walk_lattice +
+           table_moments) vs the reference arithmetic: picks equal but for near-ties
 """
 from __future__ import annotations
 
@@ -26,7 +28,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
-CASES = ("smoke", "block", "walk", "moments", "batch", "c5", "mc")
+CASES = ("smoke", "block", "walk", "moments", "batch", "c5", "mc", "table")
 
 
 def main(argv):
@@ -119,6 +121,20 @@ def main(argv):
         elif case == "mc":
             prob = P.Witsenhausen(grids=[(-25.0, 25.0, 2001)] * 2)
             P.device_monte_carlo_objective(prob, prob.identity_controllers(), 1 << 16, seed=3)
+        elif case == "table":
+            d = 1 << 15
+            res = P.solve(P.Witsenhausen(), P.SolverConfig(max_rounds=2))
+            yc, y = np.linspace(-25, 25, 2000), np.linspace(-25, 25, d)
+            u0 = np.interp(y, yc, res.controllers.values(0))
+            u1 = np.interp(y, yc, res.controllers.values(1))
+            outs = []
+            for arith in ("reference", "table"):
+                prob = P.Witsenhausen(grids=[(-25.0, 25.0, d)] * 2, arithmetic=arith)
+                U = P.ControllerSet((P.SampledController(prob.grids[0], u0), P.SampledController(prob.grids[1], u1)))
+                cfg = P.SolverConfig(search_radius=19.5 * prob.grids[0].spacing)
+                outs.append(P.partial_exhaustion_phase(prob, 0, U, cfg))
+            ndiff = int(np.count_nonzero(outs[0] != outs[1]))
+            assert ndiff <= d // 1000, f"table picks differ at {ndiff} points"
         else:
             raise SystemExit(f"unknown case {case!r}; one of {CASES}")
         torch.cuda.synchronize()
