@@ -47,6 +47,8 @@ def main():
     ap.add_argument("--log2d", type=int, default=20)
     ap.add_argument("--ns", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--window-nodes", type=int, default=39)
+    ap.add_argument("--no-rank-warmup", action="store_true",
+                    help="skip the untimed pass per rank (large grids; the plan read-back is then timed, ~ms)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     d = 1 << args.log2d
@@ -74,7 +76,8 @@ def main():
         per_rank = []
         for r in range(n):
             sh = Rank(rank=r, world=n)
-            rank_step(sh, False)  # plan cache + warm
+            if not args.no_rank_warmup:
+                rank_step(sh, False)  # plan cache + warm
             per_rank.append(rank_step(sh, True))
         t = np.array(per_rank)  # [rank, phase] ms
         step = float(t.max(axis=0).sum())
