@@ -1482,6 +1482,95 @@ k_mom_fused(const double* __restrict__ yq, int64_t n, const double* __restrict__
   }
 }
 
+// Opt-in (UCP_WC_TABLE), tolerance-stated stage-1 moments of a tile of
+// kFgtQ consecutive grid queries by a Taylor (Hermite) expansion about the
+// tile centre yc: with t = yc - x and d = y - yc,
+//   phi(y - x) = sum_k d^k / k! phi^(k)(t),  phi^(k)(t) = (-1)^k He_k(t) phi(t),
+// so M_m(y) = sum_k d^k / k! A_km with A_km = sum_i w_i x_i^m (-1)^k He_k(t_i)
+// phi(t_i): one exp and kFgtK Hermite terms per (tile, source) pair instead
+// of one exp per (query, source) pair.  |d| <= 64 h and |t| <= 12 + 64 h, so
+// the series' k-th term is ~(64 h (12 + 64 h))^k / k!: used for h <= 1e-4
+// (< 2e-18 relative at kFgtK = 10).  Sources within 12 + 64 h of yc are
+// included (the reference cuts at 12 per query: the extra terms weigh
+// phi(12) ~ 6e-32).  The partial sums are reduced over the CTA in a fixed
+// order: deterministic.  The two edge queries (grid ends: factor 1/2 and the
+// cdf tails) are recomputed exactly afterwards (run_moments).
+constexpr int kFgtK = 10, kFgtQ = 128;
+constexpr double kFgtMaxH = 1e-4;
+__global__ void __launch_bounds__(kFgtQ) k_mom_fgt(const double* __restrict__ yq, int64_t nq,
+                                                   const double2* __restrict__ xw, int64_t m,
+                                                   const double2* __restrict__ tile_mm, double* o0, double* o1,
+                                                   double* o2) {
+  __shared__ __align__(16) uint64_t stab[256];
+  __shared__ double red[3 * kFgtK][kFgtQ + 1];
+  __shared__ double sA[3 * kFgtK];
+  for (int r = threadIdx.x; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
+  UCP_SYNC();
+  const ucp_exp_entry* stab2 = reinterpret_cast<const ucp_exp_entry*>(stab);
+  const int64_t q0 = (int64_t)blockIdx.x * kFgtQ;
+  const int64_t qn = nq - q0 < kFgtQ ? nq - q0 : kFgtQ;
+  const double ylo = yq[q0], yhi = yq[q0 + qn - 1];
+  const double yc = 0.5 * (ylo + yhi), cut = kGaussCut + 0.5 * (yhi - ylo);
+  const double INV = inv_sqrt_2pi();
+  double A[kFgtK][3];
+#pragma unroll
+  for (int k = 0; k < kFgtK; ++k) A[k][0] = A[k][1] = A[k][2] = 0.0;
+  const int64_t ntiles = (m + kTile - 1) / kTile;
+  for (int64_t tile = 0; tile < ntiles; ++tile) {
+    const double2 mm = tile_mm[tile];
+    if (yc - mm.y > cut || yc - mm.x < -cut) continue;  // a NaN tile is (-inf, inf): visited
+    const int64_t base = tile * kTile;
+    for (int r = threadIdx.x; r < kTile; r += kFgtQ) {
+      const double2 s = xw[base + r];  // padding is (+inf, 0): out of reach
+      const double t = yc - s.x;
+      if (!(fabs(t) <= cut)) continue;
+      const double e = ucp_exp_core((-0.5 * t) * t, stab2) * INV * s.y;
+      const double x = s.x, x2 = x * x;
+      double hm = 1.0, h0 = t;  // He_{k-1}, He_k
+      double c = e;             // (-1)^k He_k(t) e at k = 0
+      A[0][0] += c;
+      A[0][1] += c * x;
+      A[0][2] += c * x2;
+#pragma unroll
+      for (int k = 1; k < kFgtK; ++k) {
+        c = (k & 1) ? -h0 * e : h0 * e;
+        A[k][0] += c;
+        A[k][1] += c * x;
+        A[k][2] += c * x2;
+        const double hn = t * h0 - (double)k * hm;
+        hm = h0;
+        h0 = hn;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kFgtK; ++k)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) red[3 * k + j][threadIdx.x] = A[k][j];
+  UCP_SYNC();
+  if (threadIdx.x < 3 * kFgtK) {  // fixed-order sums over the CTA's threads
+    double acc = 0.0;
+    for (int r = 0; r < kFgtQ; ++r) acc += red[threadIdx.x][r];
+    sA[threadIdx.x] = acc;
+  }
+  UCP_SYNC();
+  if (threadIdx.x >= qn) return;
+  const int64_t q = q0 + threadIdx.x;
+  const double dq = yq[q] - yc;
+  double r0 = 0.0, r1 = 0.0, r2 = 0.0;  // Horner in d with 1/k! folded in
+#pragma unroll
+  for (int k = kFgtK - 1; k >= 0; --k) {
+    const double f = dq / (double)(k + 1);
+    r0 = r0 * f + sA[3 * k];
+    r1 = r1 * f + sA[3 * k + 1];
+    r2 = r2 * f + sA[3 * k + 2];
+  }
+  // r_j = sum_k A_kj d^k / k!  (Horner: ((A_9 d/10 + A_8) d/9 + ...) d/1 + A_0)
+  o0[q] = r0;
+  o1[q] = r1;
+  o2[q] = r2;
+}
+
 // Stage-1 candidates: C1(u, y) = A u^2 - 2 B u + C (witsenhausen.py:73-78).
 __global__ void k_stage1_segmented(const double* __restrict__ u_flat, const int64_t* __restrict__ offsets,
                                    int64_t nseg, const double* __restrict__ m0,
@@ -1697,7 +1786,7 @@ int ws_get(ucp_workspace* ws, int slot, size_t bytes, void** out) {
 // x1 = y0 + u0 and per-tile min/max, then the moments of `nq` queries.
 int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0, const double* w,
                 int64_t m, double a, double h, int64_t d, double* o0, double* o1, double* o2,
-                ucp_workspace* ws, cudaStream_t st) {
+                ucp_workspace* ws, cudaStream_t st, int64_t grid_begin = -1) {
   if (nq <= 0) return UCP_OK;
   void *px1, *ptile, *pctr, *ptails;
   int rc;
@@ -1712,6 +1801,20 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   UCP_CHECK(launch_pdl(k_x1_prepare, dim3((unsigned)ntiles), dim3(kTile), 0, st, y0, u0, w, m, a, h, b, (double*)px1,
                        (double2*)pxw, (double2*)ptails, (double2*)ptile, kNoBatch));
   UCP_LAUNCHED("k_x1_prepare");
+  if (grid_begin >= 0 && h <= kFgtMaxH && nq >= kFgtQ) {
+    // UCP_WC_TABLE: the queries are grid points grid_begin.. : expansion moments,
+    // then the (at most two) grid-end queries exactly
+    k_mom_fgt<<<nblocks(nq, kFgtQ), kFgtQ, 0, st>>>(yq, nq, (const double2*)pxw, m, (const double2*)ptile, o0, o1,
+                                                    o2);
+    UCP_LAUNCHED("k_mom_fgt");
+    for (int64_t e : {(int64_t)0, d - 1}) {
+      const int64_t lq = e - grid_begin;
+      if (lq < 0 || lq >= nq || (e == d - 1 && d - 1 == 0)) continue;
+      int rc2 = run_moments(yq + lq, 1, y0, u0, w, m, a, h, d, o0 + lq, o1 + lq, o2 + lq, ws, st);
+      if (rc2) return rc2;
+    }
+    return UCP_OK;
+  }
   if (nq <= kFusedMaxQueries) {
     smem_opt_in(reinterpret_cast<const void*>(k_mom_fused), kFSmem);
     UCP_CHECK(launch_pdl(k_mom_fused, dim3(nblocks(nq, kFQ)), dim3(kFThreads), kFSmem, st, yq, nq, (const double*)px1,
@@ -2055,7 +2158,7 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
   if ((rc = ws_get(ws, WS_MOM, sizeof(double) * 3 * (size_t)n, &pm))) return rc;
   double* m0 = (double*)pm;
   if ((rc = run_moments(P->y1 + begin, n, P->y0, u0, P->fw0, P->d0, P->a1, P->h1, P->d1, m0, m0 + n,
-                        m0 + 2 * n, ws, st)))
+                        m0 + 2 * n, ws, st, (P->flags & UCP_WC_TABLE) ? begin : -1)))
     return rc;
   UCP_CHECK(launch_pdl(k_lu1, dim3(nblocks(n, 256)), dim3(256), 0, st, (const double*)u1, (const double*)m0,
                        (const double*)(m0 + n), (const double*)(m0 + 2 * n), *lp, begin, n, out, err, kNoBatch));
@@ -2080,7 +2183,7 @@ int ucp_wc_exhaustion(const ucp_wc_problem* P, int stage, const double* u0, cons
     if ((rc = ws_get(ws, WS_MOM, sizeof(double) * 3 * (size_t)n, &pm))) return rc;
     double* m0 = (double*)pm;
     if ((rc = run_moments(P->y1 + begin, n, P->y0, u0, P->fw0, P->d0, P->a1, P->h1, P->d1, m0, m0 + n,
-                          m0 + 2 * n, ws, st)))
+                          m0 + 2 * n, ws, st, (P->flags & UCP_WC_TABLE) ? begin : -1)))
       return rc;
     k_ex1<<<nblocks(n, 256), 256, 0, st>>>(u1, m0, m0 + n, m0 + 2 * n, win_lo, win_hi, begin, n, out, err,
                                            kNoBatch);

@@ -158,3 +158,45 @@ def test_table_not_used_on_coarse_grids(P, golden):
         U = P.ControllerSet((P.SampledController(p.grids[0], u0), P.SampledController(p.grids[1], u1)))
         outs.append(P.partial_exhaustion_phase(p, 0, U, P.SolverConfig()))
     assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_table_stage1_expansion_moments(P, golden):
+    """arithmetic="table" at h1 <= 1e-4 (d = 2^19: h = 9.5e-5): the stage-1
+    moments of interior grid queries come from a 10-term Hermite expansion
+    about each 128-query tile's centre (k_mom_fgt), the two grid ends exactly.
+    The moments agree to ~3e-16 relative; the local update's Newton step
+    divides a second difference of the cost by (1e-4 (1 + |u|))^2, which turns
+    that into value differences up to ~3e-7 (measured 2.6e-7; the reference's
+    own rounding noise is of the same size).  Stated tolerance: local-update
+    values within 2e-6, exhaustion picks differ only on exact-cost near-ties
+    (1e-10), and the objective after either phase within 1e-12 relative
+    (measured 4e-14 and 1e-14: tools/fast_mode_ab.py)."""
+    d = 1 << 19
+    u0, u1 = _snapshot(golden, d)
+    exact = P.Witsenhausen(grids=[(*SPAN, d)] * 2)
+    table = P.Witsenhausen(grids=[(*SPAN, d)] * 2, arithmetic="table")
+    cfg = P.SolverConfig(search_radius=19.5 * exact.grids[0].spacing)
+    U = [P.ControllerSet((P.SampledController(p.grids[0], u0), P.SampledController(p.grids[1], u1)))
+         for p in (exact, table)]
+    le = P.local_update_phase(exact, 1, U[0], cfg)
+    lt = P.local_update_phase(table, 1, U[1], cfg)
+    assert (lt != le).any()  # the expansion is live at this h
+    assert lt[0] == le[0] and lt[-1] == le[-1]  # grid ends: exact moments
+    assert np.max(np.abs(lt - le)) <= 2e-6, np.max(np.abs(lt - le))
+    ge = P.partial_exhaustion_phase(exact, 1, U[0], cfg)
+    gt = P.partial_exhaustion_phase(table, 1, U[1], cfg)
+    diff = np.flatnonzero(ge != gt)
+    assert diff.size <= d // 1000, diff.size
+    if diff.size:
+        y = exact.grids[1].points[diff]
+        two = np.stack([ge[diff], gt[diff]], axis=1).ravel()
+        c = exact.marginal_cost_segmented(1, two, np.arange(0, two.size + 1, 2, dtype=np.int64), y, U[0])
+        c = c.reshape(-1, 2)
+        assert (np.abs(c[:, 1] - c[:, 0]) <= 1e-10 * np.abs(c[:, 0])).all()
+
+    def J(u):
+        return exact.objective(P.ControllerSet((P.SampledController(exact.grids[0], u0),
+                                                P.SampledController(exact.grids[1], u))))
+
+    assert abs(J(gt) - J(ge)) <= 1e-12 * J(ge)
+    assert abs(J(lt) - J(le)) <= 1e-12 * J(le)

@@ -44,17 +44,19 @@ for mode in MODES:
         res["J"] = prob.device_objective(U)
     out[mode] = (ms, res)
 ref = out["reference"][1]
-# the objective (reference arithmetic) of each mode's new stage-0 controller after
-# local0 and after exh0: do rounding-ambiguous decisions move J?
+# the objective (reference arithmetic) of each mode's new controller after
+# each phase (the other stage's snapshot fixed): do rounding-ambiguous decisions move J?
 jprob = P.Witsenhausen(grids=[(-25.0, 25.0, d)] * 2)
 
 
-def J_of(u0_new):
-    return jprob.objective(P.ControllerSet((P.SampledController(jprob.grids[0], u0_new),
-                                            P.SampledController(jprob.grids[1], u1))))
+def J_of(u_new, m):
+    v = (u_new, u1) if m == 0 else (u0, u_new)
+    return jprob.objective(P.ControllerSet((P.SampledController(jprob.grids[0], v[0]),
+                                            P.SampledController(jprob.grids[1], v[1]))))
 
 
-J_after = {m: {ph: J_of(out[m][1][ph]) for ph in ("local0", "exh0")} for m in MODES}
+PH = ("local0", "local1", "exh0", "exh1")
+J_after = {m: {ph: J_of(out[m][1][ph], int(ph[-1])) for ph in PH} for m in MODES}
 line = {"log2d": args.log2d, "ms_reference": out["reference"][0]}
 for mode in MODES[1:]:
     fast = out[mode][1]
@@ -63,7 +65,8 @@ for mode in MODES[1:]:
                                        for k in ("local0", "local1", "exh0", "exh1")},
                   "J": fast["J"], "J_rel_diff": abs(fast["J"] - ref["J"]) / ref["J"],
                   "J_after_phase_rel_diff": {ph: (J_after[mode][ph] - J_after["reference"][ph]) / J_after["reference"][ph]
-                                             for ph in ("local0", "exh0")},
+                                             for ph in PH},
+                  "max_abs_diff": {k: float(np.max(np.abs(fast[k] - ref[k]))) for k in PH},
                   "local0_points_rel_diff_above_1e-9": int(np.count_nonzero(
                       np.abs(fast["local0"] - ref["local0"]) > 1e-9 * np.maximum(np.abs(ref["local0"]), 1e-300))),
                   "max_rel_diff_local0": float(np.max(np.abs(fast["local0"] - ref["local0"]) /
