@@ -66,14 +66,16 @@ typedef struct ucp_wc_problem {
  * d=2000 solve converges 4.9e-7 relative below the reference's J) -- stated
  * and tested in tests/test_gpu_fast_mode.py. */
 #define UCP_WC_FAST 1
-/* ucp_wc_problem.flags (opt-in, tolerance-stated): the stage-0 exhaustion
- * phase reads each candidate centre's window sums from a table of the
- * reference's walk at lattice centres a1 + m h1 (built once per phase,
- * d1 + 24/h1 walks), interpolated by quintic Lagrange over 6 lattice centres,
- * exact cdf tails added -- O(1) per candidate instead of O(24/h1).  Honoured
- * when h1 <= 2e-3.  Not used by the local update (its finite differences
- * would amplify the table's per-node rounding).  Tolerance in
- * tests/test_gpu_fast_mode.py. */
+/* ucp_wc_problem.flags (opt-in, tolerance-stated; with UCP_WC_FAST): window
+ * sums from expansions instead of per-candidate walks/sums.  Stage 0 (both
+ * phases, h1 <= 2e-3): per-cell Taylor expansions, 12 terms, cells of width
+ * 0.016 over [a1 - 12, b1 + 12] built once per phase, exact cdf tails added
+ * -- O(1) per candidate instead of O(24/h1).  Stage 1 (both phases,
+ * h1 <= 1e-4): per-128-query-tile Hermite expansions of the moments, grid
+ * ends exact.  The objective keeps the FMA walk.  Exhaustion picks differ on
+ * near-ties only; local-update decisions at near-zero curvature may differ;
+ * converged J within 1e-9 of the reference arithmetic's (DESIGN.md §2b,
+ * tests/test_gpu_fast_mode.py). */
 #define UCP_WC_TABLE 2
 
 /* Local-update parameters (solver.py:47-97, SolverConfig), already resolved

@@ -182,11 +182,12 @@ struct WalkGrid {
   // UCP_WC_FAST (ucp_wc_problem.flags): the tolerance-stated FMA walk
   // (gauss_walk_impl<kMode, true>); 0 = the reference's arithmetic
   int fast;
-  // UCP_WC_TABLE: window sums tabulated at lattice centres a + m h,
-  // m in [tm0, tm0 + tL) (3 planes of tL doubles), read by table_moments;
-  // nullptr = walk every centre
+  // UCP_WC_TABLE: window-sum expansions per cell (nullptr = walk every
+  // centre): cell c, centred at ex_s0 + c * ex_dlt, holds kExK x 3
+  // coefficients (k_ex_cells), read by ex_moments
   const double* table;
-  int64_t tm0, tL;
+  double ex_s0, ex_dlt, ex_inv;
+  int64_t ex_n;
 };
 constexpr int kVsufShift = 8;  // 256 nodes per block
 
@@ -214,7 +215,8 @@ WalkGrid make_walk_grid(double a, double h, int64_t d, int fast = 0) {
   WalkGrid g;
   g.fast = fast;
   g.table = nullptr;
-  g.tm0 = g.tL = 0;
+  g.ex_s0 = g.ex_dlt = g.ex_inv = 0.0;
+  g.ex_n = 0;
   g.a = a;
   g.h = h;
   g.d = d;
@@ -287,7 +289,7 @@ __device__ __forceinline__ double range_max(const double* __restrict__ t, int nb
 // per interior node instead of 8.  Same nodes, same order, same exp/erf,
 // same no-op tail exit; every sum differs from the reference by rounding
 // only (tests/test_gpu_fast_mode.py states and checks the tolerance).
-template <int kMode, bool kFast, bool kRaw = false>
+template <int kMode, bool kFast>
 __device__ __forceinline__ Mom3 gauss_walk_impl(double st, const double* __restrict__ v, const WalkGrid g) {
   constexpr bool kLat = kMode != 0;
   long long jlo = (long long)ceil(((st - kGaussCut) - g.a) / g.h);
@@ -427,12 +429,6 @@ __device__ __forceinline__ Mom3 gauss_walk_impl(double st, const double* __restr
 #undef UCP_WALK_STEP_V
   }
   Mom3 r;
-  if (kRaw) {  // the window sums alone (the lattice table of UCP_WC_TABLE)
-    r.t0 = acc0;
-    r.t1 = acc1;
-    r.t2 = acc2;
-    return r;
-  }
   double lo = phi_cdf(g.a - st);
   double hi = phi_cdf(st - g.b);
   const double v0 = walk_ld<kMode>(v, 0), vl = walk_ld<kMode>(v, (int)(g.d - 1));
@@ -442,32 +438,39 @@ __device__ __forceinline__ Mom3 gauss_walk_impl(double st, const double* __restr
   return r;
 }
 
-// UCP_WC_TABLE (opt-in, tolerance-stated; stage-0 exhaustion only): the window sums of a centre s from
-// the lattice table by quintic Lagrange interpolation over the 6 lattice
-// centres around s, then the exact cdf tails.  The sums are smooth in s (a
-// Gaussian-weighted sum over fixed nodes; nodes cross the +-12 cut at weight
-// phi(12) ~ 6e-32), the lattice spacing is the grid's h, and the table is
-// used only for h <= kTableMaxH: interpolation error ~h^6 |T^(6)| / 720.
-// Outside the lattice the window misses the grid: the sums are exactly 0.
+// UCP_WC_TABLE, expansion form: the window sums about a cell centre sc.  With
+// t_j = y_j - sc and d = s - sc, pdf(y_j - s) = pdf(t_j) exp(-d^2/2) exp(t_j d),
+// so T_k(s) = exp(-d^2/2) sum_n d^n / n! A_nk,  A_nk = sum_j W_j pdf(t_j) t_j^n v_j^k
+// (nodes within 12 + dlt/2 of sc).  |d| <= dlt/2 = 0.008 and |t| <= 12.008:
+// the first omitted term is below (12.008 * 0.008)^12 / 12! ~ 1e-21 of the
+// sums; coefficients are summed per thread then tree-reduced (~1e-16).
+// The sums are smooth in s, so the local update's second differences see only
+// the evaluation's own rounding within a cell (unlike an interpolated table
+// of independently rounded walks).
+constexpr int kExK = 12;
+constexpr double kExCell = 0.016;
 template <int kMode>
-__device__ __forceinline__ Mom3 table_moments(double st, const double* __restrict__ v, const WalkGrid& g) {
+__device__ __forceinline__ Mom3 ex_moments(double st, const double* __restrict__ v, const WalkGrid& g) {
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-  const double t = (st - g.a) / g.h;
-  const double fm = floor(t);
-  if (fm >= (double)(g.tm0 + 2) && fm <= (double)(g.tm0 + g.tL - 4)) {
-    const double x = t - fm;
-    const double pa = x + 2.0, pb = x + 1.0, pc = x, pd = x - 1.0, pe = x - 2.0, pf = x - 3.0;
-    const double ab = pa * pb, de = pd * pe, ef = pe * pf;
-    const double w[6] = {pb * pc * de * pf * (-1.0 / 120.0), pa * pc * de * pf * (1.0 / 24.0),
-                         ab * pd * ef * (-1.0 / 12.0),       ab * pc * ef * (1.0 / 12.0),
-                         ab * pc * pd * pf * (-1.0 / 24.0),  ab * pc * de * (1.0 / 120.0)};
-    const double* T = g.table + ((int64_t)fm - 2 - g.tm0);
+  const double f = (st - g.ex_s0) * g.ex_inv;
+  if (f > -0.5 && f < (double)g.ex_n - 0.5) {
+    const double fc = floor(f + 0.5);
+    const double dl = st - (g.ex_s0 + fc * g.ex_dlt);
+    const double* A = g.table + (int64_t)fc * (3 * kExK);
+    acc0 = __ldg(A + 3 * (kExK - 1));
+    acc1 = __ldg(A + 3 * (kExK - 1) + 1);
+    acc2 = __ldg(A + 3 * (kExK - 1) + 2);
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      acc0 = __fma_rn(w[k], __ldg(T + k), acc0);
-      acc1 = __fma_rn(w[k], __ldg(T + g.tL + k), acc1);
-      acc2 = __fma_rn(w[k], __ldg(T + 2 * g.tL + k), acc2);
+    for (int n = kExK - 2; n >= 0; --n) {
+      const double fn = dl * (1.0 / (double)(n + 1));
+      acc0 = __fma_rn(acc0, fn, __ldg(A + 3 * n));
+      acc1 = __fma_rn(acc1, fn, __ldg(A + 3 * n + 1));
+      acc2 = __fma_rn(acc2, fn, __ldg(A + 3 * n + 2));
     }
+    const double gd = ucp_exp_tab((-0.5 * dl) * dl, g_exp_tab);
+    acc0 *= gd;
+    acc1 *= gd;
+    acc2 *= gd;
   }
   const double lo = phi_cdf(g.a - st), hi = phi_cdf(st - g.b);
   const double v0 = walk_ld<kMode>(v, 0), vl = walk_ld<kMode>(v, (int)(g.d - 1));
@@ -483,7 +486,7 @@ __device__ __forceinline__ Mom3 gauss_walk(double st, const double* __restrict__
 #ifdef UCP_NO_FAST_WALK  // (PTX audit of the reference-arithmetic walk: tests/test_abi_and_host.py)
   return gauss_walk_impl<kMode, false>(st, v, g);
 #else
-  if (g.table) return table_moments<kMode>(st, v, g);
+  if (g.table) return ex_moments<kMode>(st, v, g);
   return g.fast ? gauss_walk_impl<kMode, true>(st, v, g) : gauss_walk_impl<kMode, false>(st, v, g);
 #endif
 }
@@ -535,20 +538,56 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ga
   t2[t] = r.t2;
 }
 
-// UCP_WC_TABLE: the window sums (reference arithmetic) at lattice centres
-// a + (tm0 + i) h, i < L, into three planes of L doubles.
-template <int kMode>
-__global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_walk_lattice(
-    const double* __restrict__ v, WalkGrid g, int64_t tm0, int64_t L, double* T) {
-  pdl_wait();
-  pdl_trigger();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  UCP_WALK_STAGE(v, g.d);
-  if (i >= L) return;
-  const Mom3 r = gauss_walk_impl<kMode, false, true>(g.a + (double)(tm0 + i) * g.h, v, g);
-  T[i] = r.t0;
-  T[L + i] = r.t1;
-  T[2 * L + i] = r.t2;
+// UCP_WC_TABLE, expansion form: one CTA per cell, the kExK x 3 coefficients
+// A_nk of ex_moments (each thread a strided share of the cell's nodes, then a
+// fixed-order tree: deterministic).  Out: 3 * kExK doubles per cell, [n][k].
+constexpr int kExThreads = 256;
+__global__ void __launch_bounds__(kExThreads) k_ex_cells(const double* __restrict__ v, WalkGrid g,
+                                                         double* __restrict__ out) {
+  __shared__ double red[kExThreads / 32][3 * kExK];
+  __shared__ __align__(16) uint64_t stab[256];
+  for (int r = threadIdx.x; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
+  UCP_SYNC();
+  const ucp_exp_entry* stab2 = reinterpret_cast<const ucp_exp_entry*>(stab);
+  const double sc = g.ex_s0 + (double)blockIdx.x * g.ex_dlt;
+  const double reach = kGaussCut + 0.5 * g.ex_dlt;
+  long long jlo = (long long)ceil(((sc - reach) - g.a) / g.h);
+  long long jhi = (long long)floor(((sc + reach) - g.a) / g.h);
+  if (jlo < 0) jlo = 0;
+  if (jhi > g.d - 1) jhi = g.d - 1;
+  double A[kExK][3];
+#pragma unroll
+  for (int n = 0; n < kExK; ++n) A[n][0] = A[n][1] = A[n][2] = 0.0;
+  const double INV = inv_sqrt_2pi();
+  for (long long j = jlo + threadIdx.x; j <= jhi; j += kExThreads) {
+    const double t = (g.a + (double)j * g.h) - sc;
+    const double W = (j == 0 || j == g.d - 1) ? 0.5 * g.h : g.h;
+    const double vj = __ldg(v + j), v2 = vj * vj;
+    double c = ucp_exp_core((-0.5 * t) * t, stab2) * INV * W;
+#pragma unroll
+    for (int n = 0; n < kExK; ++n) {
+      A[n][0] += c;
+      A[n][1] = __fma_rn(c, vj, A[n][1]);
+      A[n][2] = __fma_rn(c, v2, A[n][2]);
+      c *= t;
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int n = 0; n < kExK; ++n)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double x = A[n][k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+      if (lane == 0) red[wid][3 * n + k] = x;
+    }
+  UCP_SYNC();
+  if (threadIdx.x < 3 * kExK) {
+    double x = 0.0;
+    for (int w = 0; w < kExThreads / 32; ++w) x += red[w][threadIdx.x];
+    out[(int64_t)blockIdx.x * (3 * kExK) + threadIdx.x] = x;
+  }
 }
 
 // marginal_cost_segmented m=0 over a flat candidate list; the segment of
@@ -1909,23 +1948,33 @@ int attach_vsuf(WalkGrid* g, const double* v1, int64_t n_walks, ucp_workspace* w
   return UCP_OK;
 }
 
-// UCP_WC_TABLE is honoured for grids at least this fine (interpolation error
-// ~ h^6 |T^(6)| / 720 < 1e-15 relative); coarser grids walk every centre.
+// UCP_WC_TABLE's stage-0 expansion is used on grids at least this fine (the
+// k_ex_cells pass, ~ncell * 24/h nodes, pays off once windows are long);
+// coarser grids keep the FMA walk.
 constexpr double kTableMaxH = 2e-3;
+
+int table_local() {  // UCP_TABLE_LOCAL=0: the stage-0 local update keeps the FMA walk (A/B)
+  static const int k = [] {
+    const char* e = getenv("UCP_TABLE_LOCAL");
+    return e ? atoi(e) : 1;
+  }();
+  return k;
+}
 
 int attach_table(WalkGrid* g, const ucp_wc_problem* P, const double* v1, ucp_workspace* ws, cudaStream_t st) {
   if (!(P->flags & UCP_WC_TABLE) || !(P->h1 <= kTableMaxH)) return UCP_OK;
-  const int64_t M = (int64_t)ceil(kGaussCut / P->h1) + 3;  // lattice covers [a - 12 - 3h, b + 12 + 3h]
-  const int64_t tm0 = -M, L = P->d1 + 2 * M;
+  // cells cover every centre whose window reaches the grid: [a - 12, b + 12]
+  const double s0 = P->a1 - kGaussCut, span = (P->a1 + P->h1 * (double)(P->d1 - 1) + kGaussCut) - s0;
+  const int64_t nc = (int64_t)ceil(span / kExCell) + 1;
   void* pt;
-  if (int rc = ws_get(ws, WS_TABLE, sizeof(double) * 3 * (size_t)L, &pt)) return rc;
-  WalkGrid gl = make_walk_grid(P->a1, P->h1, P->d1, 0);  // the table: the reference's walk
-  if (int rc = attach_vsuf(&gl, v1, L, ws, st)) return rc;
-  UCP_WALK_LAUNCH(k_walk_lattice, L, nblocks(L, kWalkThreads), st, P->d1, v1, gl, tm0, L, (double*)pt);
-  UCP_LAUNCHED("k_walk_lattice");
+  if (int rc = ws_get(ws, WS_TABLE, sizeof(double) * 3 * kExK * (size_t)nc, &pt)) return rc;
+  g->ex_s0 = s0;
+  g->ex_dlt = kExCell;
+  g->ex_inv = 1.0 / kExCell;
+  g->ex_n = nc;
+  k_ex_cells<<<(unsigned)nc, kExThreads, 0, st>>>(v1, *g, (double*)pt);
+  UCP_LAUNCHED("k_ex_cells");
   g->table = (const double*)pt;
-  g->tm0 = tm0;
-  g->tL = L;
   return UCP_OK;
 }
 
@@ -2143,9 +2192,11 @@ int ucp_wc_local_update(const ucp_wc_problem* P, int stage, const double* u0, co
     if (int rc_ = check_aligned(u1)) return rc_;
     WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1, (int)(P->flags & UCP_WC_FAST));
     if ((rc = attach_vsuf(&g, u1, 3 * n, ws, st))) return rc;
-    // (no UCP_WC_TABLE here: the local update's second differences over
-    // h = 1e-4 (1 + |u|) would amplify the table's uncorrelated per-lattice-node
-    // rounding, 1e-14, to 1e-5 in c2 -- measured: J after the phase 1.3e-5 off)
+    // UCP_WC_TABLE: the expansion is smooth in s, so the local update's second
+    // differences over h = 1e-4 (1 + |u|) see only the evaluation's rounding
+    // (an interpolated lattice of independently rounded walks was tried: its
+    // 1e-14 per-node noise became 1e-5 in c2)
+    if (table_local() && (rc = attach_table(&g, P, u1, ws, st))) return rc;
     UCP_WALK_LAUNCH_PDL(k_lu0_probe, 3 * n, nblocks(3 * n, kWalkThreads), st, P->d1, P->y0, P->f0, u0, P->k, u1, g, lp->fd_step, begin, n,
                                                      (double*)pc, kNoBatch);
     UCP_LAUNCHED("k_lu0_probe");

@@ -87,10 +87,11 @@ class Witsenhausen(Problem):
         recurrence, FMA in the v-weighted sums: 6 instead of 8 FP64 instructions
         per walk node; costs equal to rounding, argmin picks may differ on
         near-ties -- tests/test_gpu_fast_mode.py states the tolerance);
-        "table" adds, on grids with h1 <= 2e-3, lattice-tabulated window sums
-        for the stage-0 exhaustion phase (the reference's walk at lattice
-        centres, quintic interpolation: O(1) per candidate; same tolerance
-        statement), the FMA walk elsewhere."""
+        "table" evaluates window sums from expansions: per-cell Taylor
+        expansions in both stage-0 phases (h1 <= 2e-3), per-tile Hermite
+        expansions of the stage-1 moments (h1 <= 1e-4), O(1) per candidate;
+        the objective keeps the FMA walk (DESIGN.md §2b states the tolerance:
+        near-tie picks, converged J within 1e-9)."""
         if arithmetic not in self.ARITHMETIC:
             raise ValueError(f"witsenhausen.arithmetic must be one of {self.ARITHMETIC} (got {arithmetic!r})")
         self.arithmetic = arithmetic

@@ -16,8 +16,8 @@ sanitizer run is also a parity run:
   c5       ZeroDelay and Inventory M=3 (small and ~2k-4k grids), two rounds each, and the
            uniform-noise kernels vs the oracle
   mc       Philox Monte-Carlo objective, 2^16 samples
-  table    d=2^15 exhaustion in the opt-in table arithmetic (k_walk_lattice +
-           table_moments) vs the reference arithmetic: picks equal but for near-ties
+  table    d=2^15 exhaustion in the opt-in table arithmetic (k_ex_cells +
+           ex_moments) vs the reference arithmetic: picks equal but for near-ties
 """
 from __future__ import annotations
 
