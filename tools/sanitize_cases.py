@@ -17,7 +17,8 @@ sanitizer run is also a parity run:
            uniform-noise kernels vs the oracle
   mc       Philox Monte-Carlo objective, 2^16 samples
   table    d=2^15 exhaustion in the opt-in table arithmetic (k_ex_cells +
-           ex_moments) vs the reference arithmetic: picks equal but for near-ties
+           ex_moments) vs the reference arithmetic: picks equal but for near-ties;
+           d=2^19 local updates of both stages (cells; k_mom_fgt)
 """
 from __future__ import annotations
 
@@ -135,6 +136,20 @@ def main(argv):
                 outs.append(P.partial_exhaustion_phase(prob, 0, U, cfg))
             ndiff = int(np.count_nonzero(outs[0] != outs[1]))
             assert ndiff <= d // 1000, f"table picks differ at {ndiff} points"
+            # the local update on the cells (stage 0) and, at h1 <= 1e-4, the
+            # stage-1 expansion moments (k_mom_fgt, grid ends exact)
+            d = 1 << 19
+            y = np.linspace(-25, 25, d)
+            u0 = np.interp(y, yc, res.controllers.values(0))
+            u1 = np.interp(y, yc, res.controllers.values(1))
+            outs = []
+            for arith in ("reference", "table"):
+                prob = P.Witsenhausen(grids=[(-25.0, 25.0, d)] * 2, arithmetic=arith)
+                U = P.ControllerSet((P.SampledController(prob.grids[0], u0), P.SampledController(prob.grids[1], u1)))
+                cfg = P.SolverConfig(search_radius=19.5 * prob.grids[0].spacing)
+                outs.append((P.local_update_phase(prob, 0, U, cfg), P.local_update_phase(prob, 1, U, cfg)))
+            assert np.isfinite(outs[1][0]).all()
+            assert np.max(np.abs(outs[1][1] - outs[0][1])) <= 2e-6, "table stage-1 local update"
         else:
             raise SystemExit(f"unknown case {case!r}; one of {CASES}")
         torch.cuda.synchronize()
