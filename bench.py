@@ -563,8 +563,8 @@ def run_ours(args):
             del fprob, FU, fouts
         fast["what"] = ("opt-in arithmetic, NOT bitwise (tolerance stated in DESIGN.md §2b and "
                         "tests/test_gpu_fast_mode.py): 'fma' = FMA walk; 'table' = stage-0 window sums from per-cell "
-                        "Taylor expansions (h1 <= 2e-3) + Hermite-expansion stage-1 moments (h1 <= 1e-4), "
-                        "objective by the FMA walk")
+                        "Taylor expansions (objective included; the reference walk's rounding bias reproduced) + "
+                        "per-tile Hermite-expansion stage-1 moments, grids with h1 <= 2e-3")
 
     # the step's outputs on the host (one untimed step on the same snapshot): the
     # parity check against the oracle's results on the cpu_baseline sample points

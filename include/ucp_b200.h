@@ -67,12 +67,14 @@ typedef struct ucp_wc_problem {
  * and tested in tests/test_gpu_fast_mode.py. */
 #define UCP_WC_FAST 1
 /* ucp_wc_problem.flags (opt-in, tolerance-stated; with UCP_WC_FAST): window
- * sums from expansions instead of per-candidate walks/sums.  Stage 0 (both
- * phases, h1 <= 2e-3): per-cell Taylor expansions, 12 terms, cells of width
- * 0.016 over [a1 - 12, b1 + 12] built once per phase, exact cdf tails added
- * -- O(1) per candidate instead of O(24/h1).  Stage 1 (both phases,
- * h1 <= 1e-4): per-128-query-tile Hermite expansions of the moments, grid
- * ends exact.  The objective keeps the FMA walk.  Exhaustion picks differ on
+ * sums from expansions instead of per-candidate walks/sums, on grids with
+ * h1 <= 2e-3.  Stage 0 (both phases; the objective through
+ * ucp_wc_objective_terms_ws): per-cell Taylor expansions, 12 terms, cells of
+ * width 0.016 over [a1 - 12, b1 + 12] built once per call, the reference
+ * walk's first-order rounding bias reproduced, exact cdf tails added -- O(1)
+ * per candidate instead of O(24/h1).  Stage 1 (both phases): Hermite
+ * expansions of the moments per tile of floor(0.016/h1) queries, grid ends
+ * exact.  Exhaustion picks differ on
  * near-ties only; local-update decisions at near-zero curvature may differ;
  * converged J within 1e-9 of the reference arithmetic's (DESIGN.md §2b,
  * tests/test_gpu_fast_mode.py). */
@@ -192,6 +194,13 @@ int ucp_wc_run_block_graph(const ucp_wc_problem* P, int kind, int iters, double*
 int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const double* u1,
                            int64_t begin, int64_t end, double* terms, int64_t* err,
                            void* stream);
+/* The same with a workspace: under UCP_WC_TABLE the integrand's window sums
+ * come from the expansion cells (built in ws) instead of the FMA walk --
+ * J within ~1e-10 relative of the walk's (tests/test_gpu_fast_mode.py).
+ * Without UCP_WC_TABLE identical to ucp_wc_objective_terms. */
+int ucp_wc_objective_terms_ws(const ucp_wc_problem* P, const double* u0, const double* u1,
+                              int64_t begin, int64_t end, double* terms, int64_t* err,
+                              ucp_workspace* ws, void* stream);
 
 /* ---- config 5: uniform-noise kernels and the other UCP examples -----------
  * kernels.py:488-615 (numba bodies); rad = noise half-width. */

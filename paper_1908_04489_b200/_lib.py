@@ -78,6 +78,8 @@ SIGNATURES = {
                                        c_vp, c_vp]),
     "ucp_wc_objective_terms": (c_int, [ctypes.POINTER(WcProblem), c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
                                        c_vp]),
+    "ucp_wc_objective_terms_ws": (c_int, [ctypes.POINTER(WcProblem), c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
+                                          c_vp, c_vp]),
     "ucp_fp64_probe": (c_int, [c_int, c_int, c_int, c_vp, c_vp]),
     "ucp_walk_node_counter": (c_int, [c_vp]),
 }

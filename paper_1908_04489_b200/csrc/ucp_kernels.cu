@@ -187,6 +187,7 @@ struct WalkGrid {
   // coefficients (k_ex_cells), read by ex_moments
   const double* table;
   double ex_s0, ex_dlt, ex_inv;
+  double ex_ih, ex_dq2;  // 1/h and dq/2 (the reference walk's bias, ex_moments)
   int64_t ex_n;
 };
 constexpr int kVsufShift = 8;  // 256 nodes per block
@@ -215,7 +216,7 @@ WalkGrid make_walk_grid(double a, double h, int64_t d, int fast = 0) {
   WalkGrid g;
   g.fast = fast;
   g.table = nullptr;
-  g.ex_s0 = g.ex_dlt = g.ex_inv = 0.0;
+  g.ex_s0 = g.ex_dlt = g.ex_inv = g.ex_ih = g.ex_dq2 = 0.0;
   g.ex_n = 0;
   g.a = a;
   g.h = h;
@@ -440,44 +441,67 @@ __device__ __forceinline__ Mom3 gauss_walk_impl(double st, const double* __restr
 
 // UCP_WC_TABLE, expansion form: the window sums about a cell centre sc.  With
 // t_j = y_j - sc and d = s - sc, pdf(y_j - s) = pdf(t_j) exp(-d^2/2) exp(t_j d),
-// so T_k(s) = exp(-d^2/2) sum_n d^n / n! A_nk,  A_nk = sum_j W_j pdf(t_j) t_j^n v_j^k
-// (nodes within 12 + dlt/2 of sc).  |d| <= dlt/2 = 0.008 and |t| <= 12.008:
-// the first omitted term is below (12.008 * 0.008)^12 / 12! ~ 1e-21 of the
-// sums; coefficients are summed per thread then tree-reduced (~1e-16).
+// so S_pk(s) = sum_j W_j pdf(y_j - s) t_j^p v_j^k = exp(-d^2/2) sum_n d^n / n! A_(n+p)k,
+// A_nk = sum_j W_j pdf(t_j) t_j^n v_j^k (nodes within 12 + dlt/2 of sc).
+// |d| <= dlt/2 = 0.008 and |t| <= 12.008: the first omitted term is below
+// (12.008 * 0.008)^12 / 12! ~ 1e-21 of the sums; coefficients are summed per
+// thread then tree-reduced (~1e-16).
+//
+// S_0k are the TRUE window sums.  The reference's walk is not: its pdf
+// recurrence multiplies by ratio_i = ratio_0 q^i with q = fl(exp(-h^2)), so
+// node m = j - jlo of the window carries the factor (1 + dq)^(m(m-1)/2),
+// dq = fl(q)/q - 1 -- a bias up to 1.4e-7 relative at h = 4.8e-5 (checked
+// against the oracle's walk).  ex_moments reproduces it to first order,
+//   T_k = S_0k + dq/2 sum_j W_j pdf v_j^k m_j (m_j - 1),  m_j = t_j / h + c,
+// c = (sc - a)/h - jlo(s), i.e. from S_0k, S_1k, S_2k; what remains is the
+// walk's per-step rounding (~3e-10 relative at 2^20, 1e-10 at 2^18).
 // The sums are smooth in s, so the local update's second differences see only
 // the evaluation's own rounding within a cell (unlike an interpolated table
 // of independently rounded walks).
-constexpr int kExK = 12;
+constexpr int kExK = 12, kExRows = kExK + 2;
 constexpr double kExCell = 0.016;
+// UCP_WC_TABLE's expansions are used on grids at least this fine (the
+// k_ex_cells pass, ~ncell * 24/h nodes, pays off once windows are long; a
+// stage-1 tile then holds >= 8 queries); coarser grids keep the FMA walk and
+// the direct moments.
+constexpr double kTableMaxH = 2e-3;
 template <int kMode>
 __device__ __forceinline__ Mom3 ex_moments(double st, const double* __restrict__ v, const WalkGrid& g) {
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  double acc[3] = {0.0, 0.0, 0.0};
   const double f = (st - g.ex_s0) * g.ex_inv;
   if (f > -0.5 && f < (double)g.ex_n - 0.5) {
     const double fc = floor(f + 0.5);
-    const double dl = st - (g.ex_s0 + fc * g.ex_dlt);
-    const double* A = g.table + (int64_t)fc * (3 * kExK);
-    acc0 = __ldg(A + 3 * (kExK - 1));
-    acc1 = __ldg(A + 3 * (kExK - 1) + 1);
-    acc2 = __ldg(A + 3 * (kExK - 1) + 2);
+    const double sc = g.ex_s0 + fc * g.ex_dlt;
+    const double dl = st - sc;
+    const double* A = g.table + (int64_t)fc * (3 * kExRows);
+    double S[3][3];  // [p][k]
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) S[p][k] = __ldg(A + 3 * (kExK - 1 + p) + k);
 #pragma unroll
     for (int n = kExK - 2; n >= 0; --n) {
       const double fn = dl * (1.0 / (double)(n + 1));
-      acc0 = __fma_rn(acc0, fn, __ldg(A + 3 * n));
-      acc1 = __fma_rn(acc1, fn, __ldg(A + 3 * n + 1));
-      acc2 = __fma_rn(acc2, fn, __ldg(A + 3 * n + 2));
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) S[p][k] = __fma_rn(S[p][k], fn, __ldg(A + 3 * (n + p) + k));
     }
+    long long jlo = (long long)ceil(((st - kGaussCut) - g.a) / g.h);  // the walk's first node
+    if (jlo < 0) jlo = 0;
+    const double c = (sc - g.a) * g.ex_ih - (double)jlo;
+    const double b0 = c * (c - 1.0), b1 = (2.0 * c - 1.0) * g.ex_ih, b2 = g.ex_ih * g.ex_ih;
     const double gd = ucp_exp_tab((-0.5 * dl) * dl, g_exp_tab);
-    acc0 *= gd;
-    acc1 *= gd;
-    acc2 *= gd;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      acc[k] = gd * (S[0][k] + g.ex_dq2 * ((S[2][k] * b2 + S[1][k] * b1) + S[0][k] * b0));
   }
   const double lo = phi_cdf(g.a - st), hi = phi_cdf(st - g.b);
   const double v0 = walk_ld<kMode>(v, 0), vl = walk_ld<kMode>(v, (int)(g.d - 1));
   Mom3 r;
-  r.t0 = (acc0 + lo) + hi;
-  r.t1 = (acc1 + lo * v0) + hi * vl;
-  r.t2 = (acc2 + (lo * v0) * v0) + (hi * vl) * vl;
+  r.t0 = (acc[0] + lo) + hi;
+  r.t1 = (acc[1] + lo * v0) + hi * vl;
+  r.t2 = (acc[2] + (lo * v0) * v0) + (hi * vl) * vl;
   return r;
 }
 
@@ -538,13 +562,14 @@ __global__ void __launch_bounds__(kWalkThreads, kMode ? 1 : kWalkMinBlocks) k_ga
   t2[t] = r.t2;
 }
 
-// UCP_WC_TABLE, expansion form: one CTA per cell, the kExK x 3 coefficients
-// A_nk of ex_moments (each thread a strided share of the cell's nodes, then a
-// fixed-order tree: deterministic).  Out: 3 * kExK doubles per cell, [n][k].
+// UCP_WC_TABLE, expansion form: one CTA per cell, the kExRows x 3
+// coefficients A_nk of ex_moments (each thread a strided share of the cell's
+// nodes, then a fixed-order tree: deterministic).  Out: 3 * kExRows doubles
+// per cell, [n][k].
 constexpr int kExThreads = 256;
 __global__ void __launch_bounds__(kExThreads) k_ex_cells(const double* __restrict__ v, WalkGrid g,
                                                          double* __restrict__ out) {
-  __shared__ double red[kExThreads / 32][3 * kExK];
+  __shared__ double red[kExThreads / 32][3 * kExRows];
   __shared__ __align__(16) uint64_t stab[256];
   for (int r = threadIdx.x; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
   UCP_SYNC();
@@ -555,9 +580,9 @@ __global__ void __launch_bounds__(kExThreads) k_ex_cells(const double* __restric
   long long jhi = (long long)floor(((sc + reach) - g.a) / g.h);
   if (jlo < 0) jlo = 0;
   if (jhi > g.d - 1) jhi = g.d - 1;
-  double A[kExK][3];
+  double A[kExRows][3];
 #pragma unroll
-  for (int n = 0; n < kExK; ++n) A[n][0] = A[n][1] = A[n][2] = 0.0;
+  for (int n = 0; n < kExRows; ++n) A[n][0] = A[n][1] = A[n][2] = 0.0;
   const double INV = inv_sqrt_2pi();
   for (long long j = jlo + threadIdx.x; j <= jhi; j += kExThreads) {
     const double t = (g.a + (double)j * g.h) - sc;
@@ -565,7 +590,7 @@ __global__ void __launch_bounds__(kExThreads) k_ex_cells(const double* __restric
     const double vj = __ldg(v + j), v2 = vj * vj;
     double c = ucp_exp_core((-0.5 * t) * t, stab2) * INV * W;
 #pragma unroll
-    for (int n = 0; n < kExK; ++n) {
+    for (int n = 0; n < kExRows; ++n) {
       A[n][0] += c;
       A[n][1] = __fma_rn(c, vj, A[n][1]);
       A[n][2] = __fma_rn(c, v2, A[n][2]);
@@ -574,7 +599,7 @@ __global__ void __launch_bounds__(kExThreads) k_ex_cells(const double* __restric
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int n = 0; n < kExK; ++n)
+  for (int n = 0; n < kExRows; ++n)
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       double x = A[n][k];
@@ -583,10 +608,10 @@ __global__ void __launch_bounds__(kExThreads) k_ex_cells(const double* __restric
       if (lane == 0) red[wid][3 * n + k] = x;
     }
   UCP_SYNC();
-  if (threadIdx.x < 3 * kExK) {
+  if (threadIdx.x < 3 * kExRows) {
     double x = 0.0;
     for (int w = 0; w < kExThreads / 32; ++w) x += red[w][threadIdx.x];
-    out[(int64_t)blockIdx.x * (3 * kExK) + threadIdx.x] = x;
+    out[(int64_t)blockIdx.x * (3 * kExRows) + threadIdx.x] = x;
   }
 }
 
@@ -1521,33 +1546,32 @@ k_mom_fused(const double* __restrict__ yq, int64_t n, const double* __restrict__
   }
 }
 
-// Opt-in (UCP_WC_TABLE), tolerance-stated stage-1 moments of a tile of
-// kFgtQ consecutive grid queries by a Taylor (Hermite) expansion about the
-// tile centre yc: with t = yc - x and d = y - yc,
+// Opt-in (UCP_WC_TABLE), tolerance-stated stage-1 moments of a tile of qper
+// consecutive grid queries by a Taylor (Hermite) expansion about the tile
+// centre yc: with t = yc - x and d = y - yc,
 //   phi(y - x) = sum_k d^k / k! phi^(k)(t),  phi^(k)(t) = (-1)^k He_k(t) phi(t),
 // so M_m(y) = sum_k d^k / k! A_km with A_km = sum_i w_i x_i^m (-1)^k He_k(t_i)
 // phi(t_i): one exp and kFgtK Hermite terms per (tile, source) pair instead
-// of one exp per (query, source) pair.  |d| <= 64 h and |t| <= 12 + 64 h, so
-// the series' k-th term is ~(64 h (12 + 64 h))^k / k!: used for h <= 1e-4
-// (< 2e-18 relative at kFgtK = 10).  Sources within 12 + 64 h of yc are
-// included (the reference cuts at 12 per query: the extra terms weigh
-// phi(12) ~ 6e-32).  The partial sums are reduced over the CTA in a fixed
-// order: deterministic.  The two edge queries (grid ends: factor 1/2 and the
-// cdf tails) are recomputed exactly afterwards (run_moments).
-constexpr int kFgtK = 10, kFgtQ = 128;
-constexpr double kFgtMaxH = 1e-4;
-__global__ void __launch_bounds__(kFgtQ) k_mom_fgt(const double* __restrict__ yq, int64_t nq,
-                                                   const double2* __restrict__ xw, int64_t m,
-                                                   const double2* __restrict__ tile_mm, double* o0, double* o1,
-                                                   double* o2) {
+// of one exp per (query, source) pair.  The tile spans at most kExCell
+// (qper = floor(kExCell / h) queries), so |d| <= 0.008 and |t| <= 12.008:
+// the k-th term is ~(0.096)^k / k!, < 1e-21 at kFgtK = 12.  Sources within
+// 12 + span/2 of yc are included (the reference cuts at 12 per query: the
+// extra terms weigh phi(12) ~ 6e-32).  Partial sums are reduced over the CTA
+// in a fixed order: deterministic.  The two edge queries (grid ends: factor
+// 1/2 and the cdf tails) are recomputed exactly afterwards (run_moments).
+constexpr int kFgtK = 12, kFgtThreads = 128;
+__global__ void __launch_bounds__(kFgtThreads) k_mom_fgt(const double* __restrict__ yq, int64_t nq, int qper,
+                                                         const double2* __restrict__ xw, int64_t m,
+                                                         const double2* __restrict__ tile_mm, double* o0,
+                                                         double* o1, double* o2) {
   __shared__ __align__(16) uint64_t stab[256];
-  __shared__ double red[3 * kFgtK][kFgtQ + 1];
+  __shared__ double red[kFgtThreads / 32][3 * kFgtK];
   __shared__ double sA[3 * kFgtK];
   for (int r = threadIdx.x; r < 256; r += blockDim.x) stab[r] = g_exp_tab[r];
   UCP_SYNC();
   const ucp_exp_entry* stab2 = reinterpret_cast<const ucp_exp_entry*>(stab);
-  const int64_t q0 = (int64_t)blockIdx.x * kFgtQ;
-  const int64_t qn = nq - q0 < kFgtQ ? nq - q0 : kFgtQ;
+  const int64_t q0 = (int64_t)blockIdx.x * qper;
+  const int64_t qn = nq - q0 < qper ? nq - q0 : qper;
   const double ylo = yq[q0], yhi = yq[q0 + qn - 1];
   const double yc = 0.5 * (ylo + yhi), cut = kGaussCut + 0.5 * (yhi - ylo);
   const double INV = inv_sqrt_2pi();
@@ -1559,55 +1583,60 @@ __global__ void __launch_bounds__(kFgtQ) k_mom_fgt(const double* __restrict__ yq
     const double2 mm = tile_mm[tile];
     if (yc - mm.y > cut || yc - mm.x < -cut) continue;  // a NaN tile is (-inf, inf): visited
     const int64_t base = tile * kTile;
-    for (int r = threadIdx.x; r < kTile; r += kFgtQ) {
+    for (int r = threadIdx.x; r < kTile; r += kFgtThreads) {
       const double2 s = xw[base + r];  // padding is (+inf, 0): out of reach
       const double t = yc - s.x;
       if (!(fabs(t) <= cut)) continue;
       const double e = ucp_exp_core((-0.5 * t) * t, stab2) * INV * s.y;
       const double x = s.x, x2 = x * x;
       double hm = 1.0, h0 = t;  // He_{k-1}, He_k
-      double c = e;             // (-1)^k He_k(t) e at k = 0
-      A[0][0] += c;
-      A[0][1] += c * x;
-      A[0][2] += c * x2;
+      A[0][0] += e;
+      A[0][1] = __fma_rn(e, x, A[0][1]);
+      A[0][2] = __fma_rn(e, x2, A[0][2]);
 #pragma unroll
       for (int k = 1; k < kFgtK; ++k) {
-        c = (k & 1) ? -h0 * e : h0 * e;
+        const double c = (k & 1) ? -h0 * e : h0 * e;  // (-1)^k He_k(t) e
         A[k][0] += c;
-        A[k][1] += c * x;
-        A[k][2] += c * x2;
+        A[k][1] = __fma_rn(c, x, A[k][1]);
+        A[k][2] = __fma_rn(c, x2, A[k][2]);
         const double hn = t * h0 - (double)k * hm;
         hm = h0;
         h0 = hn;
       }
     }
   }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < kFgtK; ++k)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) red[3 * k + j][threadIdx.x] = A[k][j];
+    for (int j = 0; j < 3; ++j) {
+      double x = A[k][j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+      if (lane == 0) red[wid][3 * k + j] = x;
+    }
   UCP_SYNC();
-  if (threadIdx.x < 3 * kFgtK) {  // fixed-order sums over the CTA's threads
+  if (threadIdx.x < 3 * kFgtK) {  // fixed-order sums over the CTA's warps
     double acc = 0.0;
-    for (int r = 0; r < kFgtQ; ++r) acc += red[threadIdx.x][r];
+    for (int w = 0; w < kFgtThreads / 32; ++w) acc += red[w][threadIdx.x];
     sA[threadIdx.x] = acc;
   }
   UCP_SYNC();
-  if (threadIdx.x >= qn) return;
-  const int64_t q = q0 + threadIdx.x;
-  const double dq = yq[q] - yc;
-  double r0 = 0.0, r1 = 0.0, r2 = 0.0;  // Horner in d with 1/k! folded in
+  for (int64_t i = threadIdx.x; i < qn; i += kFgtThreads) {
+    const int64_t q = q0 + i;
+    const double dq = yq[q] - yc;
+    double r0 = sA[3 * (kFgtK - 1)], r1 = sA[3 * (kFgtK - 1) + 1], r2 = sA[3 * (kFgtK - 1) + 2];
 #pragma unroll
-  for (int k = kFgtK - 1; k >= 0; --k) {
-    const double f = dq / (double)(k + 1);
-    r0 = r0 * f + sA[3 * k];
-    r1 = r1 * f + sA[3 * k + 1];
-    r2 = r2 * f + sA[3 * k + 2];
+    for (int k = kFgtK - 2; k >= 0; --k) {  // sum_k A_k d^k / k!, Horner with 1/(k+1) folded in
+      const double f = dq * (1.0 / (double)(k + 1));
+      r0 = __fma_rn(r0, f, sA[3 * k]);
+      r1 = __fma_rn(r1, f, sA[3 * k + 1]);
+      r2 = __fma_rn(r2, f, sA[3 * k + 2]);
+    }
+    o0[q] = r0;
+    o1[q] = r1;
+    o2[q] = r2;
   }
-  // r_j = sum_k A_kj d^k / k!  (Horner: ((A_9 d/10 + A_8) d/9 + ...) d/1 + A_0)
-  o0[q] = r0;
-  o1[q] = r1;
-  o2[q] = r2;
 }
 
 // Stage-1 candidates: C1(u, y) = A u^2 - 2 B u + C (witsenhausen.py:73-78).
@@ -1840,11 +1869,12 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
   UCP_CHECK(launch_pdl(k_x1_prepare, dim3((unsigned)ntiles), dim3(kTile), 0, st, y0, u0, w, m, a, h, b, (double*)px1,
                        (double2*)pxw, (double2*)ptails, (double2*)ptile, kNoBatch));
   UCP_LAUNCHED("k_x1_prepare");
-  if (grid_begin >= 0 && h <= kFgtMaxH && nq >= kFgtQ) {
+  if (grid_begin >= 0 && h <= kTableMaxH && nq >= 2) {
     // UCP_WC_TABLE: the queries are grid points grid_begin.. : expansion moments,
     // then the (at most two) grid-end queries exactly
-    k_mom_fgt<<<nblocks(nq, kFgtQ), kFgtQ, 0, st>>>(yq, nq, (const double2*)pxw, m, (const double2*)ptile, o0, o1,
-                                                    o2);
+    const int qper = (int)fmin(floor(kExCell / h), 65536.0);
+    k_mom_fgt<<<(unsigned)((nq + qper - 1) / qper), kFgtThreads, 0, st>>>(yq, nq, qper, (const double2*)pxw, m,
+                                                                          (const double2*)ptile, o0, o1, o2);
     UCP_LAUNCHED("k_mom_fgt");
     for (int64_t e : {(int64_t)0, d - 1}) {
       const int64_t lq = e - grid_begin;
@@ -1948,10 +1978,6 @@ int attach_vsuf(WalkGrid* g, const double* v1, int64_t n_walks, ucp_workspace* w
   return UCP_OK;
 }
 
-// UCP_WC_TABLE's stage-0 expansion is used on grids at least this fine (the
-// k_ex_cells pass, ~ncell * 24/h nodes, pays off once windows are long);
-// coarser grids keep the FMA walk.
-constexpr double kTableMaxH = 2e-3;
 
 int table_local() {  // UCP_TABLE_LOCAL=0: the stage-0 local update keeps the FMA walk (A/B)
   static const int k = [] {
@@ -1967,7 +1993,11 @@ int attach_table(WalkGrid* g, const ucp_wc_problem* P, const double* v1, ucp_wor
   const double s0 = P->a1 - kGaussCut, span = (P->a1 + P->h1 * (double)(P->d1 - 1) + kGaussCut) - s0;
   const int64_t nc = (int64_t)ceil(span / kExCell) + 1;
   void* pt;
-  if (int rc = ws_get(ws, WS_TABLE, sizeof(double) * 3 * kExK * (size_t)nc, &pt)) return rc;
+  if (int rc = ws_get(ws, WS_TABLE, sizeof(double) * 3 * kExRows * (size_t)nc, &pt)) return rc;
+  // dq = fl(q)/q - 1 for the walk's q = fl(exp(-h^2)) (g->q, the same bits):
+  // fl(q) - 1 is exact (Sterbenz), expm1 resolves q - 1 to ~1 ulp of h^2
+  g->ex_dq2 = 0.5 * (((g->q - 1.0) - expm1(-P->h1 * P->h1)) / g->q);
+  g->ex_ih = 1.0 / P->h1;
   g->ex_s0 = s0;
   g->ex_dlt = kExCell;
   g->ex_inv = 1.0 / kExCell;
@@ -2461,12 +2491,20 @@ int ucp_wc_run_block_graph(const ucp_wc_problem* P, int kind, int iters, double*
 
 int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const double* u1, int64_t begin,
                            int64_t end, double* terms, int64_t* err, void* stream) {
+  return ucp_wc_objective_terms_ws(P, u0, u1, begin, end, terms, err, nullptr, stream);
+}
+
+int ucp_wc_objective_terms_ws(const ucp_wc_problem* P, const double* u0, const double* u1, int64_t begin,
+                              int64_t end, double* terms, int64_t* err, ucp_workspace* ws, void* stream) {
   int rc = check_problem(P);
   if (rc) return rc;
   if (begin < 0 || end > P->d0 || begin > end) return arg_fail("objective_terms: bad shard");
   if (end == begin) return UCP_OK;
   if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1, (int)(P->flags & UCP_WC_FAST));
+  // UCP_WC_TABLE with a workspace: the integrand from the expansion cells
+  // (with the reference walk's bias, ex_moments); without one, the FMA walk
+  if (ws && (rc = attach_table(&g, P, u1, ws, as_stream(stream)))) return rc;
   UCP_WALK_LAUNCH(k_obj_terms, end - begin, nblocks(end - begin, kWalkThreads), as_stream(stream), P->d1, P->y0, P->f0, u0, P->k, u1, g,
                                                                           begin, end, terms, err, kNoBatch);
   UCP_LAUNCHED("k_obj_terms");

@@ -87,10 +87,11 @@ class Witsenhausen(Problem):
         recurrence, FMA in the v-weighted sums: 6 instead of 8 FP64 instructions
         per walk node; costs equal to rounding, argmin picks may differ on
         near-ties -- tests/test_gpu_fast_mode.py states the tolerance);
-        "table" evaluates window sums from expansions: per-cell Taylor
-        expansions in both stage-0 phases (h1 <= 2e-3), per-tile Hermite
-        expansions of the stage-1 moments (h1 <= 1e-4), O(1) per candidate;
-        the objective keeps the FMA walk (DESIGN.md §2b states the tolerance:
+        "table" (grids with h1 <= 2e-3) evaluates window sums from
+        expansions, O(1) per candidate: per-cell Taylor expansions in both
+        stage-0 phases and the objective (the reference walk's rounding bias
+        reproduced), per-tile Hermite expansions of the stage-1 moments
+        (DESIGN.md §2b states the tolerance: J of a snapshot within 1e-9,
         near-tie picks, converged J within 1e-9)."""
         if arithmetic not in self.ARITHMETIC:
             raise ValueError(f"witsenhausen.arithmetic must be one of {self.ARITHMETIC} (got {arithmetic!r})")
@@ -343,8 +344,8 @@ class Witsenhausen(Problem):
         begin, end = sharding.shard(bounds)
         buf = sharding.padded_buffer(bounds, D.device)
         jbits = torch.empty(1, dtype=I64, device=D.device)
-        _lib.call("ucp_wc_objective_terms", ctypes.byref(D.P), ptr(u0), ptr(u1), begin, end,
-                  sharding.rank_ptr(buf, bounds), err.data_ptr(), D.stream)
+        _lib.call("ucp_wc_objective_terms_ws", ctypes.byref(D.P), ptr(u0), ptr(u1), begin, end,
+                  sharding.rank_ptr(buf, bounds), err.data_ptr(), D.ws, D.stream)
         terms = sharding.gather(buf, bounds, g.d)
         sharding.allreduce_min_(err)
         _lib.call("ucp_trapezoid_sum", ptr(terms), g.d, g.spacing, jbits.data_ptr(), None, D.stream)
@@ -362,8 +363,8 @@ class Witsenhausen(Problem):
         bounds = self._plan(0, U, sharding)
         begin, end = sharding.shard(bounds)
         buf = sharding.padded_buffer(bounds, D.device)
-        _lib.call("ucp_wc_objective_terms", ctypes.byref(D.P), ptr(u0), ptr(u1), begin, end,
-                  sharding.rank_ptr(buf, bounds), res.data_ptr(), D.stream)
+        _lib.call("ucp_wc_objective_terms_ws", ctypes.byref(D.P), ptr(u0), ptr(u1), begin, end,
+                  sharding.rank_ptr(buf, bounds), res.data_ptr(), D.ws, D.stream)
         terms = sharding.gather(buf, bounds, g.d)
         sharding.allreduce_min_(res)
         bad = int(D.errors.flush(sharding, extra=res)[0])

@@ -18,8 +18,8 @@ north_star: "stated tolerance if a fast path is offered"):
   bound holds per snapshot, and a converged fast solve is checked to 1e-6.
 
 arithmetic="table" evaluates the window sums from expansions:
-stage-0 per-cell Taylor expansions in both stage-0 phases (h1 <= 2e-3) and
-stage-1 per-tile Hermite expansions (h1 <= 1e-4).  Exhaustion picks differ
+stage-0 per-cell Taylor expansions in both stage-0 phases and the objective,
+stage-1 per-tile Hermite expansions in both stage-1 phases (h1 <= 2e-3).  Exhaustion picks differ
 only on near-ties, the objective after an exhaustion phase within 1e-12; the
 local update is checked through converged solves (its per-snapshot decisions
 at near-zero curvature differ, see test_table_solve_converges_to_reference_J).
@@ -107,6 +107,23 @@ def test_fast_objective_of_a_snapshot(P, golden):
     assert abs(J[1] - J[0]) <= 1e-13 * J[0], J
 
 
+@pytest.mark.parametrize("log2d", [16, 18, 20])
+def test_table_objective_of_a_snapshot(P, golden, log2d):
+    """arithmetic="table" computes J's integrand from the expansion cells with
+    the reference walk's first-order bias (q = fl(exp(-h^2)) compounding over
+    the window: 1.4e-7 relative at 2^20) reproduced: J within 1e-9 relative of
+    the reference arithmetic's (the north star's per-iteration bound)."""
+    d = 1 << log2d
+    u0, u1 = _snapshot(golden, d)
+    J = []
+    for mode in ("reference", "table"):
+        p = P.Witsenhausen(grids=[(*SPAN, d)] * 2, arithmetic=mode)
+        J.append(p.objective(P.ControllerSet((P.SampledController(p.grids[0], u0),
+                                              P.SampledController(p.grids[1], u1)))))
+    assert J[1] != J[0]  # the expansion is live
+    assert abs(J[1] - J[0]) <= 1e-9 * J[0], (J, (J[1] - J[0]) / J[0])
+
+
 def test_fast_solve_converges_near_reference_J(P):
     res = P.solve(P.Witsenhausen(arithmetic="fma"), P.SolverConfig())
     assert res.termination == "converged"
@@ -164,9 +181,10 @@ def test_table_not_used_on_coarse_grids(P, golden):
 
 
 def test_table_stage1_expansion_moments(P, golden):
-    """arithmetic="table" at h1 <= 1e-4 (d = 2^19: h = 9.5e-5): the stage-1
-    moments of interior grid queries come from a 10-term Hermite expansion
-    about each 128-query tile's centre (k_mom_fgt), the two grid ends exactly.
+    """arithmetic="table" (d = 2^19: h = 9.5e-5): the stage-1 moments of
+    interior grid queries come from a 12-term Hermite expansion about the
+    centre of each tile of floor(0.016 / h) queries (k_mom_fgt), the two grid
+    ends exactly.
     The moments agree to ~3e-16 relative; the local update's Newton step
     divides a second difference of the cost by (1e-4 (1 + |u|))^2, which turns
     that into value differences up to ~3e-7 (measured 2.6e-7; the reference's
