@@ -564,7 +564,7 @@ def run_ours(args):
         fast["what"] = ("opt-in arithmetic, NOT bitwise (tolerance stated in DESIGN.md §2b and "
                         "tests/test_gpu_fast_mode.py): 'fma' = FMA walk; 'table' = stage-0 window sums from per-cell "
                         "Taylor expansions (objective included; the reference walk's rounding bias reproduced) + "
-                        "per-tile Hermite-expansion stage-1 moments, grids with h1 <= 2e-3")
+                        "per-tile Taylor-expansion stage-1 moments, grids with h1 <= 2e-3")
 
     # the step's outputs on the host (one untimed step on the same snapshot): the
     # parity check against the oracle's results on the cpu_baseline sample points

@@ -72,12 +72,12 @@ typedef struct ucp_wc_problem {
  * ucp_wc_objective_terms_ws): per-cell Taylor expansions, 12 terms, cells of
  * width 0.016 over [a1 - 12, b1 + 12] built once per call, the reference
  * walk's first-order rounding bias reproduced, exact cdf tails added -- O(1)
- * per candidate instead of O(24/h1).  Stage 1 (both phases): Hermite
+ * per candidate instead of O(24/h1).  Stage 1 (both phases): Taylor
  * expansions of the moments per tile of floor(0.016/h1) queries, grid ends
- * exact.  Exhaustion picks differ on
- * near-ties only; local-update decisions at near-zero curvature may differ;
- * converged J within 1e-9 of the reference arithmetic's (DESIGN.md §2b,
- * tests/test_gpu_fast_mode.py). */
+ * completed with the cdf tails.  J of a snapshot within 1e-9 of the
+ * reference arithmetic's; exhaustion picks differ on near-ties only;
+ * local-update decisions at near-zero curvature may differ; converged J
+ * within 1e-9 (tests/test_gpu_fast_mode.py). */
 #define UCP_WC_TABLE 2
 
 /* Local-update parameters (solver.py:47-97, SolverConfig), already resolved

@@ -1547,18 +1547,17 @@ k_mom_fused(const double* __restrict__ yq, int64_t n, const double* __restrict__
 }
 
 // Opt-in (UCP_WC_TABLE), tolerance-stated stage-1 moments of a tile of qper
-// consecutive grid queries by a Taylor (Hermite) expansion about the tile
-// centre yc: with t = yc - x and d = y - yc,
-//   phi(y - x) = sum_k d^k / k! phi^(k)(t),  phi^(k)(t) = (-1)^k He_k(t) phi(t),
-// so M_m(y) = sum_k d^k / k! A_km with A_km = sum_i w_i x_i^m (-1)^k He_k(t_i)
-// phi(t_i): one exp and kFgtK Hermite terms per (tile, source) pair instead
+// consecutive grid queries by a Taylor expansion about the tile centre yc:
+// with t = x - yc and d = y - yc, phi(y - x) = phi(t) exp(-d^2/2) exp(t d), so
+//   M_m(y) = exp(-d^2/2) sum_n d^n / n! A_nm,  A_nm = sum_i w_i x_i^m phi(t_i) t_i^n:
+// one exp and kFgtK (1 mul + 1 add + 2 FMA) per (tile, source) pair instead
 // of one exp per (query, source) pair.  The tile spans at most kExCell
 // (qper = floor(kExCell / h) queries), so |d| <= 0.008 and |t| <= 12.008:
-// the k-th term is ~(0.096)^k / k!, < 1e-21 at kFgtK = 12.  Sources within
+// the first omitted term is ~(0.096)^12 / 12! < 1e-21.  Sources within
 // 12 + span/2 of yc are included (the reference cuts at 12 per query: the
 // extra terms weigh phi(12) ~ 6e-32).  Partial sums are reduced over the CTA
-// in a fixed order: deterministic.  The two edge queries (grid ends: factor
-// 1/2 and the cdf tails) are recomputed exactly afterwards (run_moments).
+// in a fixed order: deterministic.  The two grid-end queries (factor 1/2 and
+// the cdf tails) are completed by k_edge_tails / k_edge_finish.
 constexpr int kFgtK = 12, kFgtThreads = 128;
 __global__ void __launch_bounds__(kFgtThreads) k_mom_fgt(const double* __restrict__ yq, int64_t nq, int qper,
                                                          const double2* __restrict__ xw, int64_t m,
@@ -1585,23 +1584,16 @@ __global__ void __launch_bounds__(kFgtThreads) k_mom_fgt(const double* __restric
     const int64_t base = tile * kTile;
     for (int r = threadIdx.x; r < kTile; r += kFgtThreads) {
       const double2 s = xw[base + r];  // padding is (+inf, 0): out of reach
-      const double t = yc - s.x;
+      const double t = s.x - yc;
       if (!(fabs(t) <= cut)) continue;
-      const double e = ucp_exp_core((-0.5 * t) * t, stab2) * INV * s.y;
       const double x = s.x, x2 = x * x;
-      double hm = 1.0, h0 = t;  // He_{k-1}, He_k
-      A[0][0] += e;
-      A[0][1] = __fma_rn(e, x, A[0][1]);
-      A[0][2] = __fma_rn(e, x2, A[0][2]);
+      double c = ucp_exp_core((-0.5 * t) * t, stab2) * INV * s.y;
 #pragma unroll
-      for (int k = 1; k < kFgtK; ++k) {
-        const double c = (k & 1) ? -h0 * e : h0 * e;  // (-1)^k He_k(t) e
+      for (int k = 0; k < kFgtK; ++k) {
         A[k][0] += c;
         A[k][1] = __fma_rn(c, x, A[k][1]);
         A[k][2] = __fma_rn(c, x2, A[k][2]);
-        const double hn = t * h0 - (double)k * hm;
-        hm = h0;
-        h0 = hn;
+        c *= t;
       }
     }
   }
@@ -1627,16 +1619,67 @@ __global__ void __launch_bounds__(kFgtThreads) k_mom_fgt(const double* __restric
     const double dq = yq[q] - yc;
     double r0 = sA[3 * (kFgtK - 1)], r1 = sA[3 * (kFgtK - 1) + 1], r2 = sA[3 * (kFgtK - 1) + 2];
 #pragma unroll
-    for (int k = kFgtK - 2; k >= 0; --k) {  // sum_k A_k d^k / k!, Horner with 1/(k+1) folded in
+    for (int k = kFgtK - 2; k >= 0; --k) {  // sum_n A_n d^n / n!, Horner with 1/(n+1) folded in
       const double f = dq * (1.0 / (double)(k + 1));
       r0 = __fma_rn(r0, f, sA[3 * k]);
       r1 = __fma_rn(r1, f, sA[3 * k + 1]);
       r2 = __fma_rn(r2, f, sA[3 * k + 2]);
     }
-    o0[q] = r0;
-    o1[q] = r1;
-    o2[q] = r2;
+    const double gd = ucp_exp_core((-0.5 * dq) * dq, stab2);
+    o0[q] = gd * r0;
+    o1[q] = gd * r1;
+    o2[q] = gd * r2;
   }
+}
+
+// Grid-end queries of the expansion path (kernels.py:466-482): the reference
+// gives them factor 1/2 on the Gaussian part plus the cdf tails
+// phi_cdf(a - x)/h (first node) and phi_cdf(x - b)/h (last node) over EVERY
+// support point.  k_edge_tails: per-CTA partial sums of w x^m tail (left and
+// right, 6 values); k_edge_finish (one warp): fixed-order total, then
+// o[edge] = 0.5 * o[edge] + tails.  Deterministic; 2 launches instead of two
+// single-query exact passes over the whole support.
+constexpr int kEdgeThreads = 256, kEdgeBlocks = 296;
+__global__ void __launch_bounds__(kEdgeThreads) k_edge_tails(const double2* __restrict__ xw,
+                                                             const double2* __restrict__ tails, int64_t m,
+                                                             double* __restrict__ part) {
+  __shared__ double red[kEdgeThreads / 32][6];
+  double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * kEdgeThreads + threadIdx.x; i < m; i += (int64_t)gridDim.x * kEdgeThreads) {
+    const double2 s = xw[i], tl = tails[i];
+    const double wl = tl.x * s.y, wr = tl.y * s.y;
+    acc[0] += wl;
+    acc[1] = __fma_rn(wl, s.x, acc[1]);
+    acc[2] = __fma_rn(wl * s.x, s.x, acc[2]);
+    acc[3] += wr;
+    acc[4] = __fma_rn(wr, s.x, acc[4]);
+    acc[5] = __fma_rn(wr * s.x, s.x, acc[5]);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    double x = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) red[wid][k] = x;
+  }
+  UCP_SYNC();
+  if (threadIdx.x < 6) {
+    double x = 0.0;
+    for (int w = 0; w < kEdgeThreads / 32; ++w) x += red[w][threadIdx.x];
+    part[(int64_t)blockIdx.x * 6 + threadIdx.x] = x;
+  }
+}
+__global__ void k_edge_finish(const double* __restrict__ part, int nblk, int64_t lq_left, int64_t lq_right,
+                              double* o0, double* o1, double* o2) {
+  const int k = threadIdx.x;
+  if (k >= 6) return;
+  double x = 0.0;
+  for (int b = 0; b < nblk; ++b) x += part[(int64_t)b * 6 + k];
+  const int64_t lq = k < 3 ? lq_left : lq_right;
+  if (lq < 0) return;
+  double* o = (k % 3 == 0) ? o0 : (k % 3 == 1 ? o1 : o2);
+  o[lq] = 0.5 * o[lq] + x;
 }
 
 // Stage-1 candidates: C1(u, y) = A u^2 - 2 B u + C (witsenhausen.py:73-78).
@@ -1802,7 +1845,7 @@ struct ucp_workspace {
 namespace {
 enum {
   WS_X1 = 0, WS_TILE, WS_MOM, WS_COST, WS_COUNT, WS_CAND_PT, WS_CAND_J, WS_TOTAL, WS_TAILS,
-  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_C5_TAB, WS_C5_GT0, WS_C5_GT1, WS_C5_MEMO, WS_C5_FC, WS_C5_GC, WS_VSUF, WS_TABLE, WS_NSLOTS
+  WS_C5_F0, WS_C5_F1, WS_C5_G0, WS_C5_G1, WS_C5_ONE, WS_XW, WS_C5_TAB, WS_C5_GT0, WS_C5_GT1, WS_C5_MEMO, WS_C5_FC, WS_C5_GC, WS_VSUF, WS_TABLE, WS_EDGE, WS_NSLOTS
 };
 static_assert(WS_NSLOTS <= 24, "workspace slots");
 // fused moments below this many queries (above, k_moments' persistent CTAs
@@ -1876,11 +1919,15 @@ int run_moments(const double* yq, int64_t nq, const double* y0, const double* u0
     k_mom_fgt<<<(unsigned)((nq + qper - 1) / qper), kFgtThreads, 0, st>>>(yq, nq, qper, (const double2*)pxw, m,
                                                                           (const double2*)ptile, o0, o1, o2);
     UCP_LAUNCHED("k_mom_fgt");
-    for (int64_t e : {(int64_t)0, d - 1}) {
-      const int64_t lq = e - grid_begin;
-      if (lq < 0 || lq >= nq || (e == d - 1 && d - 1 == 0)) continue;
-      int rc2 = run_moments(yq + lq, 1, y0, u0, w, m, a, h, d, o0 + lq, o1 + lq, o2 + lq, ws, st);
-      if (rc2) return rc2;
+    const int64_t ll = grid_begin == 0 ? 0 : -1;                          // first grid node here?
+    const int64_t lr = grid_begin + nq == d && d > 1 ? nq - 1 : -1;      // last grid node here?
+    if (ll >= 0 || lr >= 0) {
+      void* pe;
+      if ((rc = ws_get(ws, WS_EDGE, sizeof(double) * 6 * kEdgeBlocks, &pe))) return rc;
+      k_edge_tails<<<kEdgeBlocks, kEdgeThreads, 0, st>>>((const double2*)pxw, (const double2*)ptails, m, (double*)pe);
+      UCP_LAUNCHED("k_edge_tails");
+      k_edge_finish<<<1, 32, 0, st>>>((const double*)pe, kEdgeBlocks, ll, lr, o0, o1, o2);
+      UCP_LAUNCHED("k_edge_finish");
     }
     return UCP_OK;
   }

@@ -90,7 +90,7 @@ class Witsenhausen(Problem):
         "table" (grids with h1 <= 2e-3) evaluates window sums from
         expansions, O(1) per candidate: per-cell Taylor expansions in both
         stage-0 phases and the objective (the reference walk's rounding bias
-        reproduced), per-tile Hermite expansions of the stage-1 moments
+        reproduced), per-tile Taylor expansions of the stage-1 moments
         (DESIGN.md §2b states the tolerance: J of a snapshot within 1e-9,
         near-tie picks, converged J within 1e-9)."""
         if arithmetic not in self.ARITHMETIC:
