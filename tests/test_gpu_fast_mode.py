@@ -244,3 +244,23 @@ def test_table_solve_converges_to_reference_J(P, golden):
         assert res.termination == "converged", (mode, res.termination)
         Js.append(res.final_objective)
     assert abs(Js[1] - Js[0]) <= 1e-9 * Js[0], Js
+
+
+def test_table_nonfinite_raises(P, golden):
+    """A non-finite stage-1 value poisons every expansion cell whose reach
+    contains it (the reference: every window that contains it); the error
+    slots still fire, so the phases and the objective raise NumericError like
+    the reference arithmetic (the reported grid point may differ)."""
+    d = 1 << 15
+    u0, u1 = _snapshot(golden, d)
+    u1 = u1.copy()
+    u1[d // 2 + 77] = 1e200  # (s - u1)^2 overflows
+    for mode in ("reference", "table"):
+        prob = P.Witsenhausen(grids=[(*SPAN, d)] * 2, arithmetic=mode)
+        U = P.ControllerSet((P.SampledController(prob.grids[0], u0), P.SampledController(prob.grids[1], u1)))
+        cfg = P.SolverConfig(search_radius=19.5 * prob.grids[0].spacing)
+        for fn in (P.local_update_phase, P.partial_exhaustion_phase):
+            with pytest.raises(P.NumericError):
+                fn(prob, 0, U, cfg)
+        with pytest.raises(P.NumericError):
+            prob.objective(U)
