@@ -20,6 +20,7 @@
 #include <vector>
 #include <mutex>
 #include <shared_mutex>
+#include <map>
 #include <set>
 #include <unordered_set>
 #include <cub/block/block_reduce.cuh>
@@ -584,11 +585,25 @@ __global__ void __launch_bounds__(kExThreads) k_ex_cells(const double* __restric
 #pragma unroll
   for (int n = 0; n < kExRows; ++n) A[n][0] = A[n][1] = A[n][2] = 0.0;
   const double INV = inv_sqrt_2pi();
-  for (long long j = jlo + threadIdx.x; j <= jhi; j += kExThreads) {
+  // a thread's nodes are kExThreads apart (D = kExThreads h): pdf(t + D) =
+  // pdf(t) r, r(t + D) = r(t) exp(-D^2), re-anchored with fresh exps every
+  // kExAnchor nodes (the recurrence's rounding then stays ~kExAnchor^2 ulp)
+  constexpr int kExAnchor = 16;
+  const double D = (double)kExThreads * g.h;
+  const double qD = ucp_exp_core(-(D * D), stab2);
+  double pdf = 0.0, ratio = 0.0;
+  int it = 0;
+  for (long long j = jlo + threadIdx.x; j <= jhi; j += kExThreads, ++it) {
     const double t = (g.a + (double)j * g.h) - sc;
+    if ((it & (kExAnchor - 1)) == 0) {
+      pdf = ucp_exp_core((-0.5 * t) * t, stab2) * INV;
+      ratio = ucp_exp_core(-t * D - 0.5 * D * D, stab2);
+    }
     const double W = (j == 0 || j == g.d - 1) ? 0.5 * g.h : g.h;
     const double vj = __ldg(v + j), v2 = vj * vj;
-    double c = ucp_exp_core((-0.5 * t) * t, stab2) * INV * W;
+    double c = pdf * W;
+    pdf *= ratio;
+    ratio *= qD;
 #pragma unroll
     for (int n = 0; n < kExRows; ++n) {
       A[n][0] += c;
@@ -825,6 +840,220 @@ __global__ void __launch_bounds__(kTrapThreads) k_trapezoid(const double* __rest
     named_arrive(kEmpty + sb, kTrapThreads);
   }
   if (lane == 0) *out = n == 1 ? 0.0 : acc * spacing;
+}
+
+// ---- The same serial sum, bitwise, in parallel (large n; problem.py:110-127
+// via kernels.py:136-144: acc = x0/2; acc += x_i, i = 1..n-2; acc += x_(n-1)/2).
+// While the running sum S stays inside one binade [2^(E+52), 2^(E+53)) (or its
+// negative), every S is a multiple of u = 2^E and fl(S + a) = S + u * rnd(a/u)
+// exactly: with a/u = k + f (k = floor, 0 <= f < 1) the increment is k, k + 1
+// for f > 1/2, and for the tie f = 1/2 the even one of N + k, N + k + 1
+// (N = S/u) -- only ties depend on the state, through N's parity.  So a chunk
+// of kTzL addends reduces, for each parity of N at its start, to an exact
+// integer increment, the output parity and the min/max running increment
+// (k_tz_decompose, one thread per chunk, E proposed by an approximate prefix:
+// k_tz_chunks + k_tz_plan).  One warp then walks the chunks in order
+// (k_tz_final): a chunk whose exact start has exponent E and whose running N
+// stays inside [2^52 + 1, 2^53 - 1] in magnitude (so every exact intermediate
+// sum is inside the binade and rounds on u's grid) is applied as N += inc;
+// any other chunk (binade crossings, zero or non-finite sums, huge addends,
+// E guessed wrong) is added serially in order.  Either way every addition is
+// the reference's, so the result is bitwise the serial kernel's.
+constexpr int kTzL = 1024;           // addends per chunk
+constexpr int64_t kTzMinN = 32768;   // below: the serial kernel
+// per-(device, stream) grow-only scratch of the chunked trapezoid (calls on
+// one stream are ordered; cudaFree of an outgrown buffer synchronises)
+int tz_scratch(cudaStream_t st, size_t bytes, void** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> bufs;
+  int dev = 0;
+  UCP_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto& b = bufs[{dev, st}];
+  if (b.second < bytes) {
+    if (b.first) UCP_CHECK(cudaFree(b.first));
+    b.first = nullptr;
+    b.second = 0;
+    UCP_CHECK(cudaMalloc(&b.first, bytes));
+    b.second = bytes;
+  }
+  *out = b.first;
+  return UCP_OK;
+}
+int tz_parallel() {  // UCP_TZ_PARALLEL=0: always the serial kernel (A/B)
+  static const int k = [] {
+    const char* e = getenv("UCP_TZ_PARALLEL");
+    return e ? atoi(e) : 1;
+  }();
+  return k;
+}
+struct TzRec {
+  long long inc[2], mn[2], mx[2];  // per start parity: increment, min / max running increment
+  int e, flags;                    // flags: bit 0 usable, bit 1 / 2 output parity for start parity 0 / 1
+};
+__device__ __forceinline__ int64_t tz_lo(int64_t c) { return 1 + c * kTzL; }  // first addend of chunk c
+__device__ __forceinline__ double tz_addend(const double* x, int64_t n, int64_t i) {
+  return i == n - 1 ? 0.5 * x[n - 1] : x[i];
+}
+// K1: one warp per chunk: approximate chunk sum; first non-finite sample -> err
+__global__ void k_tz_chunks(const double* __restrict__ x, int64_t n, int64_t nch, double* csum, int64_t* err) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= nch) return;
+  const int64_t lo = tz_lo(c), hi = lo + kTzL < n ? lo + kTzL : n;  // addends [lo, hi), hi <= n
+  double acc = 0.0;
+  long long bad = UCP_NO_ERROR;
+  if (c == 0 && lane == 0 && !isfinite(x[0])) bad = 0;
+  for (int64_t i = lo + lane; i < hi; i += 32) {
+    const double xv = x[i];
+    if (!isfinite(xv) && i < bad) bad = i;
+    acc += i == n - 1 ? 0.5 * xv : xv;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_down_sync(0xffffffffu, acc, o);
+    const long long ob = __shfl_down_sync(0xffffffffu, bad, o);
+    bad = ob < bad ? ob : bad;
+  }
+  if (lane == 0) {
+    csum[c] = acc;
+    if (err && bad != UCP_NO_ERROR) flag_min(err, bad);
+  }
+}
+// K2: one CTA: approximate running sum at each chunk start -> proposed exponent
+__global__ void __launch_bounds__(1024) k_tz_plan(const double* __restrict__ x, const double* __restrict__ csum,
+                                                  int64_t nch, TzRec* rec) {
+  __shared__ double sc[1024];
+  __shared__ double carry;
+  if (threadIdx.x == 0) carry = 0.5 * x[0];
+  UCP_SYNC();
+  for (int64_t b = 0; b < nch; b += 1024) {
+    const int64_t c = b + threadIdx.x;
+    const double v = c < nch ? csum[c] : 0.0;
+    sc[threadIdx.x] = v;
+    UCP_SYNC();
+    for (int o = 1; o < 1024; o <<= 1) {  // inclusive Hillis-Steele scan (approximate: E is only a proposal)
+      const double add = threadIdx.x >= o ? sc[threadIdx.x - o] : 0.0;
+      UCP_SYNC();
+      sc[threadIdx.x] += add;
+      UCP_SYNC();
+    }
+    const double start = carry + (sc[threadIdx.x] - v);
+    if (c < nch) {
+      int e = INT_MIN;
+      if (isfinite(start) && start != 0.0) {
+        const int lg = ilogb(start);
+        if (lg >= -960 && lg <= 1000) e = lg - 52;
+      }
+      rec[c].e = e;
+    }
+    UCP_SYNC();
+    if (threadIdx.x == 1023) carry = carry + sc[1023];
+    UCP_SYNC();
+  }
+}
+// K3: one thread per chunk: the exact integer form for both start parities
+__global__ void k_tz_decompose(const double* __restrict__ x, int64_t n, int64_t nch, TzRec* rec) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nch) return;
+  const int e = rec[c].e;
+  int flags = 0;
+  long long inc[2] = {0, 0}, mn[2] = {0, 0}, mx[2] = {0, 0};
+  int par[2] = {0, 1};
+  if (e != INT_MIN) {
+    flags = 1;
+    const int64_t lo = tz_lo(c), hi = lo + kTzL < n ? lo + kTzL : n;
+    for (int64_t i = lo; i < hi; ++i) {
+      const double q = ldexp(tz_addend(x, n, i), -e);  // exact: |a| >= 2^-1074 and e >= -1012
+      // a non-finite addend, or one (or a running increment) that leaves the
+      // binade by itself: serial (also keeps the int64 sums far from overflow)
+      if (!(fabs(q) < 0x1p54) || inc[0] > (1LL << 55) || inc[0] < -(1LL << 55)) {
+        flags = 0;
+        break;
+      }
+      // q = k + f, k = floor(q), classified from |q| = K + F (F = |q| - K is
+      // exact for |q| >= 0; 1 - F for q < 0 need not be): up = f > 1/2, tie = f == 1/2
+      const double r = fabs(q), K = floor(r), F = r - K;
+      long long k;
+      bool up, tie;
+      if (q >= 0.0) {
+        k = (long long)K;
+        up = F > 0.5;
+        tie = F == 0.5;
+      } else if (F == 0.0) {
+        k = -(long long)K;
+        up = tie = false;
+      } else {
+        k = -(long long)K - 1;
+        up = F < 0.5;
+        tie = F == 0.5;
+      }
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const long long d = k + (up ? 1 : (tie ? (long long)((par[p] + (int)(k & 1)) & 1) : 0));
+        inc[p] += d;
+        par[p] = (int)((par[p] + (int)(d & 1)) & 1);
+        mn[p] = inc[p] < mn[p] ? inc[p] : mn[p];
+        mx[p] = inc[p] > mx[p] ? inc[p] : mx[p];
+      }
+    }
+  }
+  TzRec r;
+  r.e = e;
+  r.flags = flags | (par[0] << 1) | (par[1] << 2);
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    r.inc[p] = inc[p];
+    r.mn[p] = mn[p];
+    r.mx[p] = mx[p];
+  }
+  rec[c] = r;
+}
+// K4: one warp walks the chunks in order (lane 0 holds the exact sum)
+constexpr int kTzBatch = 128;  // records staged per smem batch
+__global__ void __launch_bounds__(32) k_tz_final(const double* __restrict__ x, int64_t n, int64_t nch,
+                                                 const TzRec* __restrict__ rec, double spacing, double* out) {
+  __shared__ TzRec srec[kTzBatch];
+  __shared__ double sx[kTzL];
+  const int lane = threadIdx.x;
+  double S = 0.5 * x[0];
+  const long long lo52 = (1LL << 52) + 1, hi53 = (1LL << 53) - 1;
+  for (int64_t b = 0; b < nch; b += kTzBatch) {
+    const int nb = (int)(nch - b < kTzBatch ? nch - b : kTzBatch);
+    __syncwarp();
+    for (int r = lane; r < nb; r += 32) srec[r] = rec[b + r];
+    __syncwarp();
+    for (int r = 0; r < nb; ++r) {
+      const int64_t c = b + r;
+      int fast = 0;
+      if (lane == 0) {
+        const TzRec& R = srec[r];
+        if ((R.flags & 1) && isfinite(S) && S != 0.0 && ilogb(S) - 52 == R.e) {
+          const long long N = (long long)ldexp(S, -R.e);  // |N| in [2^52, 2^53): exact
+          const int p = (int)(N & 1);
+          const long long lo = N + R.mn[p], hi = N + R.mx[p];
+          const bool ok = N > 0 ? (lo >= lo52 && hi <= hi53) : (hi <= -lo52 && lo >= -hi53);
+          if (ok) {
+            S = ldexp((double)(N + R.inc[p]), R.e);
+            fast = 1;
+          }
+        }
+      }
+      fast = __shfl_sync(0xffffffffu, fast, 0);
+      if (fast) continue;
+      // serial chunk: the warp stages the addends, lane 0 adds them in order
+      const int64_t lo = tz_lo(c), hi = lo + kTzL < n ? lo + kTzL : n;
+      for (int64_t i = lo + lane; i < hi; i += 32) sx[i - lo] = x[i];
+      __syncwarp();
+      if (lane == 0) {
+        const int cnt = (int)(hi - lo);
+        const int stop = hi == n ? cnt - 1 : cnt;
+        for (int t = 0; t < stop; ++t) S += sx[t];
+        if (hi == n) S += 0.5 * sx[cnt - 1];
+      }
+      __syncwarp();
+    }
+  }
+  if (lane == 0) *out = S * spacing;
 }
 
 __global__ void k_segmented_argmin(const double* __restrict__ costs, const int64_t* __restrict__ offsets,
@@ -1578,12 +1807,30 @@ __global__ void __launch_bounds__(kFgtThreads) k_mom_fgt(const double* __restric
 #pragma unroll
   for (int k = 0; k < kFgtK; ++k) A[k][0] = A[k][1] = A[k][2] = 0.0;
   const int64_t ntiles = (m + kTile - 1) / kTile;
-  for (int64_t tile = 0; tile < ntiles; ++tile) {
-    const double2 mm = tile_mm[tile];
-    if (yc - mm.y > cut || yc - mm.x < -cut) continue;  // a NaN tile is (-inf, inf): visited
-    const int64_t base = tile * kTile;
-    for (int r = threadIdx.x; r < kTile; r += kFgtThreads) {
-      const double2 s = xw[base + r];  // padding is (+inf, 0): out of reach
+  // live tiles only (a NaN tile is (-inf, inf): visited); each thread owns
+  // kTile / kFgtThreads sources of a tile, the next live tile's sources are
+  // loaded while this one's are expanded (L2 latency behind the FP64 work)
+  auto next_live = [&](int64_t tile) {
+    for (; tile < ntiles; ++tile) {
+      const double2 mm = tile_mm[tile];
+      if (!(yc - mm.y > cut || yc - mm.x < -cut)) break;
+    }
+    return tile;
+  };
+  constexpr int kPer = kTile / kFgtThreads;
+  double2 cur[kPer], nxt[kPer];
+  int64_t tile = next_live(0);
+  if (tile < ntiles)
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) cur[r] = xw[tile * kTile + r * kFgtThreads + threadIdx.x];
+  while (tile < ntiles) {
+    const int64_t nt = next_live(tile + 1);
+    if (nt < ntiles)
+#pragma unroll
+      for (int r = 0; r < kPer; ++r) nxt[r] = xw[nt * kTile + r * kFgtThreads + threadIdx.x];
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const double2 s = cur[r];  // padding is (+inf, 0): out of reach
       const double t = s.x - yc;
       if (!(fabs(t) <= cut)) continue;
       const double x = s.x, x2 = x * x;
@@ -1596,6 +1843,9 @@ __global__ void __launch_bounds__(kFgtThreads) k_mom_fgt(const double* __restric
         c *= t;
       }
     }
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) cur[r] = nxt[r];
+    tile = nt;
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -2166,7 +2416,27 @@ int ucp_gauss_moments_points(const double* y, int64_t n, const double* x, const 
 int ucp_trapezoid_sum(const double* samples, int64_t n, double spacing, double* out, int64_t* err,
                       void* stream) {
   if (n < 1) return arg_fail("trapezoid needs at least one sample");
-  k_trapezoid<<<1, kTrapThreads, 0, as_stream(stream)>>>(samples, n, spacing, out, err, kNoBatch);
+  cudaStream_t st = as_stream(stream);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (n >= kTzMinN && tz_parallel() && cudaStreamIsCapturing(st, &cs) == cudaSuccess &&
+      cs == cudaStreamCaptureStatusNone) {
+    // the chunked exact form (k_tz_*): bitwise the serial sum
+    const int64_t nch = (n - 1 + kTzL - 1) / kTzL;
+    void* scratch = nullptr;
+    if (int rc = tz_scratch(st, nch * (sizeof(double) + sizeof(TzRec)), &scratch)) return rc;
+    double* csum = (double*)scratch;
+    TzRec* rec = (TzRec*)(csum + nch);
+    k_tz_chunks<<<(unsigned)((nch * 32 + 255) / 256), 256, 0, st>>>(samples, n, nch, csum, err);
+    UCP_LAUNCHED("k_tz_chunks");
+    k_tz_plan<<<1, 1024, 0, st>>>(samples, csum, nch, rec);
+    UCP_LAUNCHED("k_tz_plan");
+    k_tz_decompose<<<nblocks(nch, 128), 128, 0, st>>>(samples, n, nch, rec);
+    UCP_LAUNCHED("k_tz_decompose");
+    k_tz_final<<<1, 32, 0, st>>>(samples, n, nch, rec, spacing, out);
+    UCP_LAUNCHED("k_tz_final");
+    return UCP_OK;
+  }
+  k_trapezoid<<<1, kTrapThreads, 0, st>>>(samples, n, spacing, out, err, kNoBatch);
   UCP_LAUNCHED("k_trapezoid");
   return UCP_OK;
 }

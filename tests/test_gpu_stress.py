@@ -27,7 +27,7 @@ def stress_lib():
     return _build.build_stress()
 
 
-@pytest.mark.parametrize("cases", ["smoke block walk batch c5 mc table", "moments"])
+@pytest.mark.parametrize("cases", ["smoke block walk batch c5 mc table tz", "moments"])
 @pytest.mark.parametrize("rep", [0, 1])
 def test_stress_build_bitwise(stress_lib, cases, rep):
     env = dict(os.environ, UCP_B200_LIB=str(stress_lib), CUDA_LAUNCH_BLOCKING="1")

@@ -19,6 +19,8 @@ sanitizer run is also a parity run:
   table    d=2^15 exhaustion in the opt-in table arithmetic (k_ex_cells +
            ex_moments) vs the reference arithmetic: picks equal but for near-ties;
            d=2^19 local updates of both stages (cells; k_mom_fgt)
+  tz       the chunked exact trapezoid (k_tz_*) on 2^17-sample sequences with
+           ties, sign changes and binade crossings vs the oracle's serial sum
 """
 from __future__ import annotations
 
@@ -29,7 +31,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
-CASES = ("smoke", "block", "walk", "moments", "batch", "c5", "mc", "table")
+CASES = ("smoke", "block", "walk", "moments", "batch", "c5", "mc", "table", "tz")
 
 
 def main(argv):
@@ -150,6 +152,14 @@ def main(argv):
                 outs.append((P.local_update_phase(prob, 0, U, cfg), P.local_update_phase(prob, 1, U, cfg)))
             assert np.isfinite(outs[1][0]).all()
             assert np.max(np.abs(outs[1][1] - outs[0][1])) <= 2e-6, "table stage-1 local update"
+        elif case == "tz":
+            rng = np.random.default_rng(17)
+            n = 1 << 17
+            seqs = [rng.normal(0, 1, n), np.concatenate([[2.0 ** 54], rng.integers(-7, 8, n - 1).astype(float)]),
+                    np.concatenate([rng.uniform(0, 1, n // 2), -rng.uniform(0, 1, n - n // 2)]),
+                    rng.uniform(0, 0.3, n)]
+            for x in seqs:
+                same(P.kernels.trapezoid_sum(x, 0.01), orc.trapezoid_sum(x, 0.01), "chunked trapezoid")
         else:
             raise SystemExit(f"unknown case {case!r}; one of {CASES}")
         torch.cuda.synchronize()
