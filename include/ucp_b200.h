@@ -194,10 +194,11 @@ int ucp_wc_run_block_graph(const ucp_wc_problem* P, int kind, int iters, double*
 int ucp_wc_objective_terms(const ucp_wc_problem* P, const double* u0, const double* u1,
                            int64_t begin, int64_t end, double* terms, int64_t* err,
                            void* stream);
-/* The same with a workspace: under UCP_WC_TABLE the integrand's window sums
- * come from the expansion cells (built in ws) instead of the FMA walk --
- * J within ~1e-10 relative of the walk's (tests/test_gpu_fast_mode.py).
- * Without UCP_WC_TABLE identical to ucp_wc_objective_terms. */
+/* The same with a workspace: the walks stop at their provably no-op tail
+ * (range-max table built in ws; bitwise the same terms, ~17% fewer nodes at
+ * 2^20), and under UCP_WC_TABLE the integrand's window sums come from the
+ * expansion cells instead of the FMA walk -- J within ~1e-10 relative of the
+ * walk's (tests/test_gpu_fast_mode.py). */
 int ucp_wc_objective_terms_ws(const ucp_wc_problem* P, const double* u0, const double* u1,
                               int64_t begin, int64_t end, double* terms, int64_t* err,
                               ucp_workspace* ws, void* stream);

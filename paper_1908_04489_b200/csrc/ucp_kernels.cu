@@ -2819,8 +2819,10 @@ int ucp_wc_objective_terms_ws(const ucp_wc_problem* P, const double* u0, const d
   if (end == begin) return UCP_OK;
   if (int rc_ = check_aligned(u1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1, (int)(P->flags & UCP_WC_FAST));
-  // UCP_WC_TABLE with a workspace: the integrand from the expansion cells
-  // (with the reference walk's bias, ex_moments); without one, the FMA walk
+  // with a workspace: the walks' no-op tail exit (result-invariant, as in the
+  // phases) and, under UCP_WC_TABLE, the integrand from the expansion cells
+  // (with the reference walk's bias, ex_moments)
+  if (ws && (rc = attach_vsuf(&g, u1, end - begin, ws, as_stream(stream)))) return rc;
   if (ws && (rc = attach_table(&g, P, u1, ws, as_stream(stream)))) return rc;
   UCP_WALK_LAUNCH(k_obj_terms, end - begin, nblocks(end - begin, kWalkThreads), as_stream(stream), P->d1, P->y0, P->f0, u0, P->k, u1, g,
                                                                           begin, end, terms, err, kNoBatch);
