@@ -88,3 +88,25 @@ def test_chunked_trapezoid_first_nonfinite_index(P):
                   torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
         assert int(err.item()) == bad
+
+
+def test_chunked_trapezoid_concurrent_streams(P, oracle_mod):
+    """Per-stream scratch: interleaved calls on two streams, each bitwise."""
+    from paper_1908_04489_b200 import _lib
+
+    rng = np.random.default_rng(3)
+    n = 1 << 18
+    xs = [rng.normal(0, 1, n), rng.uniform(0, 0.3, n)]
+    want = [oracle_mod.trapezoid_sum(x, 0.25) for x in xs]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    dev = [torch.from_numpy(x).cuda() for x in xs]
+    outs = [torch.empty(8, dtype=torch.float64, device="cuda") for _ in xs]
+    torch.cuda.synchronize()
+    for rep in range(8):
+        for k in range(2):
+            _lib.call("ucp_trapezoid_sum", dev[k].data_ptr(), n, 0.25, outs[k][rep:].data_ptr(), None,
+                      streams[k].cuda_stream)
+    torch.cuda.synchronize()
+    for k in range(2):
+        got = outs[k].cpu().numpy()
+        assert all(np.float64(g).tobytes() == np.float64(want[k]).tobytes() for g in got), k
