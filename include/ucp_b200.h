@@ -145,6 +145,13 @@ int ucp_device_libm(int which, const double* x, int64_t n, double* out, void* st
 int ucp_wc_stage0_cost(const ucp_wc_problem* P, const double* v1, const double* u_flat,
                        int64_t n_cand, const int64_t* offsets, const double* y_seg,
                        const double* f0_seg, int64_t nseg, double* out, void* stream);
+/* The same with a workspace: the walks stop at their provably no-op tail
+ * (same bits), and under UCP_WC_TABLE the costs come from the expansion
+ * cells, as in the problem's phases. */
+int ucp_wc_stage0_cost_ws(const ucp_wc_problem* P, const double* v1, const double* u_flat,
+                          int64_t n_cand, const int64_t* offsets, const double* y_seg,
+                          const double* f0_seg, int64_t nseg, double* out, ucp_workspace* ws,
+                          void* stream);
 /* witsenhausen.py:71-78 (m=1); u0 = U.values(0). */
 int ucp_wc_stage1_cost(const ucp_wc_problem* P, const double* u0, const double* u_flat,
                        int64_t n_cand, const int64_t* offsets, const double* y_seg, int64_t nseg,

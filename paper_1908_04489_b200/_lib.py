@@ -65,6 +65,8 @@ SIGNATURES = {
     "ucp_flatten_windows": (c_int, [c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "ucp_wc_stage0_cost": (c_int, [ctypes.POINTER(WcProblem), c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64,
                                    c_vp, c_vp]),
+    "ucp_wc_stage0_cost_ws": (c_int, [ctypes.POINTER(WcProblem), c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64,
+                                      c_vp, c_vp, c_vp]),
     "ucp_wc_stage1_cost": (c_int, [ctypes.POINTER(WcProblem), c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp,
                                    c_vp, c_vp]),
     "ucp_wc_local_update": (c_int, [ctypes.POINTER(WcProblem), c_int, c_vp, c_vp, ctypes.POINTER(LocalParams),

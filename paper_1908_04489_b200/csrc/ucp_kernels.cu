@@ -2487,6 +2487,12 @@ int ucp_device_libm(int which, const double* x, int64_t n, double* out, void* st
 int ucp_wc_stage0_cost(const ucp_wc_problem* P, const double* v1, const double* u_flat, int64_t n_cand,
                        const int64_t* offsets, const double* y_seg, const double* f0_seg, int64_t nseg,
                        double* out, void* stream) {
+  return ucp_wc_stage0_cost_ws(P, v1, u_flat, n_cand, offsets, y_seg, f0_seg, nseg, out, nullptr, stream);
+}
+
+int ucp_wc_stage0_cost_ws(const ucp_wc_problem* P, const double* v1, const double* u_flat, int64_t n_cand,
+                          const int64_t* offsets, const double* y_seg, const double* f0_seg, int64_t nseg,
+                          double* out, ucp_workspace* ws, void* stream) {
   int rc = check_problem(P);
   if (rc) return rc;
   if (nseg < 0 || n_cand < 0) return arg_fail("stage0_cost: bad sizes");
@@ -2494,6 +2500,10 @@ int ucp_wc_stage0_cost(const ucp_wc_problem* P, const double* v1, const double* 
   const int64_t n_host = n_cand;
   if (int rc_ = check_aligned(v1)) return rc_;
   WalkGrid g = make_walk_grid(P->a1, P->h1, P->d1, (int)(P->flags & UCP_WC_FAST));
+  // with a workspace: the no-op tail exit (same bits) and, under UCP_WC_TABLE,
+  // the expansion cells -- as in the phases
+  if (ws && (rc = attach_vsuf(&g, v1, n_host, ws, as_stream(stream)))) return rc;
+  if (ws && (rc = attach_table(&g, P, v1, ws, as_stream(stream)))) return rc;
   UCP_WALK_LAUNCH(k_stage0_segmented, n_host, nblocks(n_host, kWalkThreads), as_stream(stream), P->d1, u_flat, offsets, nseg, y_seg,
                                                                            f0_seg, P->k, v1, g, out);
   UCP_LAUNCHED("k_stage0_segmented");

@@ -160,8 +160,8 @@ class Witsenhausen(Problem):
             yd = to_device_f64(y_centers, D.device)
             if m == 0:
                 f0 = to_device_f64(pdf(self._state_density, y_centers), D.device)
-                _lib.call("ucp_wc_stage0_cost", ctypes.byref(D.P), ptr(u1), ptr(ud), n, ptr(od), ptr(yd),
-                          ptr(f0), nseg, ptr(out), D.stream)
+                _lib.call("ucp_wc_stage0_cost_ws", ctypes.byref(D.P), ptr(u1), ptr(ud), n, ptr(od), ptr(yd),
+                          ptr(f0), nseg, ptr(out), D.ws, D.stream)
             else:
                 _lib.call("ucp_wc_stage1_cost", ctypes.byref(D.P), ptr(u0), ptr(ud), n, ptr(od), ptr(yd),
                           nseg, ptr(out), D.ws, D.stream)
